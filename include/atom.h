@@ -1,0 +1,180 @@
+/*
+ * atom.h -- C-ABI of libatom: the per-peer training step of Atom (arXiv 2403.10504) on B200.
+ *
+ * The method (PAPER.md = P, SPEC.md = S, line numbers):
+ *   - the whole model lives in host memory; contiguous runs of transformer layers
+ *     ("sub-models") are swapped into the GPU and executed one after another
+ *     ("houses the entire model in a single server's host memory ... memory
+ *     swapping technique to transfer model portions to the GPU");
+ *   - the partition is chosen offline so that every sub-model fits and the compute of
+ *     one sub-model overlaps the loading of the next, with gradient accumulation over
+ *     C mini-batches stretching the compute (Algorithm 1);
+ *   - one stream executes, another prefetches the next sub-model "immediately after the
+ *     current sub-model starts"; the last forward sub-model and the first sub-model are
+ *     not swapped out;
+ *   - whole-model replicas ("peers") train independently and periodically average their
+ *     parameters with an allreduce.
+ *
+ * Calls: atom_plan (static analysis, pure host), atom_peer_create, atom_step (one swapped
+ * forward + backward + update), atom_sync (peer averaging), plus inspection calls.
+ *
+ * Conventions
+ *   - Every function returns atom_status (0 = ATOM_OK).  No C++ exception crosses the ABI.
+ *     On failure atom_last_error() returns a thread-local message naming the violated
+ *     constraint or the failing CUDA/NCCL call.
+ *   - Pointers are plain host or device pointers as stated per argument.  Input buffers are
+ *     only read during the call.  The device arena is caller-owned (allocated by PyTorch);
+ *     pinned host arenas, streams, events and the NCCL communicator are library-owned and
+ *     released by atom_peer_destroy.
+ *   - After a CUDA or NCCL failure a peer is poisoned: every later call on it returns
+ *     ATOM_E_STATE.
+ *   - Canonical parameter order (init_params / atom_get_params): nodes E, B_0..B_{L-1}, H;
+ *     E = wte[V,d], wpe[T,d]; block = ln1.g[d], ln1.b[d], W_qkv[3d,d], b_qkv[3d], W_o[d,d],
+ *     b_o[d], ln2.g[d], ln2.b[d], W_fc[4d,d], b_fc[4d], W_pr[d,4d], b_pr[d];
+ *     H = lnf.g[d], lnf.b[d], W_lm[V,d] (untied, no bias).  Row-major, fp32, unpadded.
+ */
+#ifndef ATOM_H
+#define ATOM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ATOM_OK = 0,
+  ATOM_E_INVALID = -1,    /* invalid configuration / argument (S:61 InvalidConfig)             */
+  ATOM_E_INFEASIBLE = -2, /* no partition / no C satisfies the constraints        */
+  ATOM_E_CAPACITY = -3,   /* device arena smaller than plan.device_bytes (S:230 CapacityViolated) */
+  ATOM_E_CUDA = -4,
+  ATOM_E_NCCL = -5,
+  ATOM_E_OOM = -6,        /* pinned host allocation failed                                        */
+  ATOM_E_STATE = -7       /* peer poisoned by an earlier failure                                 */
+} atom_status;
+
+enum { ATOM_FP32 = 0, ATOM_BF16 = 1 };        /* compute dtype of weights and activations       */
+enum { ATOM_ACT_STASH = 1 };                  /* activation policy: stash every block's tensors  */
+#define ATOM_MAX_SEG 256
+
+/* Model and training configuration.  Caller-owned, read-only during every call. */
+typedef struct {
+  int32_t n_layer, d_model, n_head, seq_len, vocab, micro_batch; /* L, d, h, T, V, b (b sequences/micro-batch) */
+  int32_t dtype;          /* ATOM_FP32 (parity path, SIMT kernels) | ATOM_BF16 (performance path, tcgen05)   */
+  int32_t C;              /* micro-batches per step; 0 = planner picks the smallest feasible C       */
+  int32_t max_C;          /* upper end of the C search (default 64)                                  */
+  int32_t act_policy;     /* ATOM_ACT_STASH                                                                 */
+  int32_t overlap_check;  /* 1 = enforce the compute >= load constraints (Alg. 1 line 4); 0 = memory only    */
+  int64_t peak_flops;     /* FLOP/s of the analytic cost model (e.g. measured bf16 GEMM peak)               */
+  int64_t d2h_bw;         /* device->host bytes/s; 0 = same as link_bw                                       */
+  int64_t state_budget;   /* 0 = none; else cap on device bytes of model state (resident segment 1 + slots):
+                             the paper's sub-model "GPU capacity"                         */
+  const int64_t* cost_table; /* NULL = analytic; else 2*(L+2) int64 {t_f_ns, t_b_ns} per node (profiled) */
+  const int32_t* forced_ends; /* NULL = search; else n_forced ascending segment end-node indices to validate */
+  int32_t n_forced;
+  float lr, beta1, beta2, eps, weight_decay; /* AdamW (eps/wd: torch defaults, R19)          */
+  int32_t warmup_steps;   /* linear warm-up length in steps (3000)                                    */
+  int32_t sync_every;     /* average parameters every K steps; 0 = only when atom_sync() asks               */
+} atom_model_cfg;
+
+/* The plan: plain data, fixed capacity, no pointers.  Produced by atom_plan. */
+typedef struct {
+  int32_t n_seg;                  /* S: number of sub-models                                            */
+  int32_t seg_end[ATOM_MAX_SEG];  /* last node index of each sub-model (nodes 0=E, 1..L blocks, L+1=H)  */
+  int32_t C;                      /* micro-batches per step                                             */
+  int32_t nslot;                  /* rotating device slots for sub-models 2..S (0, 2 or 3)              */
+  int64_t cut_bytes;              /* activation bytes crossing sub-model boundaries per micro-batch      */
+  int64_t r1_bytes;               /* resident sub-model 1 (weights + grad + master + m + v)              */
+  int64_t slot_bytes;             /* one slot: the largest swapped sub-model's state                    */
+  int64_t stash_bytes;            /* activation stash                                                   */
+  int64_t work_bytes;             /* working set                                                        */
+  int64_t device_bytes;           /* total device arena = r1 + nslot*slot + stash + work                 */
+  int64_t pred_step_ns;           /* integer-time simulation of one step (3 lanes)                      */
+  int64_t pred_hidden_ppm;        /* predicted share of copy time overlapped by compute (ppm)           */
+  int64_t pred_h2d_B, pred_d2h_B; /* host<->device bytes per step                                       */
+  int64_t pred_flops;             /* model FLOPs per step (fwd + bwd)                                   */
+  int64_t hbm_budget, link_bw;    /* the inputs the plan was made for                                   */
+} atom_plan_t;
+
+/* Static analysis.  Pure, deterministic, no device needed.
+ * hbm_budget: max device arena bytes; link_bw: host->device bytes/s.
+ * Objective: min total cut bytes, then fewer sub-models, then the
+ * lexicographically smallest end vector; C = smallest feasible.
+ * Errors: ATOM_E_INVALID (bad cfg), ATOM_E_INFEASIBLE (message names the first violated constraint). */
+atom_status atom_plan(const atom_model_cfg* cfg, int64_t hbm_budget, int64_t link_bw, atom_plan_t* out);
+
+/* The step program as canonical text, one op per line:
+ *   "<lane> <KIND> <seg> <mb|-> <slot|-> <waits|->"   lanes: compute h2d d2h comm.
+ * sync != 0 emits a parameter-averaging step.  Writes at most cap bytes (NUL-terminated when it
+ * fits); *len = full length without the NUL.  ATOM_E_INVALID if buf is too small. */
+atom_status atom_plan_schedule(const atom_plan_t* plan, int32_t sync, char* buf, int64_t cap, int64_t* len);
+
+/* NCCL unique id for peer averaging (128 bytes written to out).  Call on one rank and
+ * broadcast it (e.g. through a torch.distributed group). */
+atom_status atom_nccl_unique_id(void* out128);
+
+typedef struct atom_peer atom_peer; /* opaque, library-owned */
+
+/* Create one peer (one whole-model replica) on CUDA device `device`.
+ *   device_arena / arena_bytes: caller-owned device memory (>= plan->device_bytes, 256-byte aligned);
+ *   init_params: host fp32 [N] in canonical order, or NULL to draw the minGPT init on the device
+ *                from `seed` (normal(0, 0.02), residual projections 0.02/sqrt(2L), biases 0, LN 1/0);
+ *   nccl_id: 128-byte id from atom_nccl_unique_id (NULL when nranks == 1); rank in [0, nranks).
+ * Pins host arenas (12 B/param: fp32 master, m, v) and makes segment 1 resident.
+ * Errors: ATOM_E_INVALID, ATOM_E_CAPACITY, ATOM_E_OOM, ATOM_E_CUDA, ATOM_E_NCCL. */
+atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan, int32_t device, void* device_arena,
+                             int64_t arena_bytes, const float* init_params, uint64_t seed, const void* nccl_id,
+                             int32_t nranks, int32_t rank, atom_peer** out);
+
+/* One training step: swapped forward, backward and AdamW over C micro-batches.
+ *   tokens: HOST int32 [C*b, T+1] (inputs = [:, :T], targets = [:, 1:]), copied before return;
+ *   loss_out: mean token cross-entropy of the step (fp32).
+ * Returns once the loss is on the host; the tail of the backward keeps running on the device
+ * and overlaps the next step (P:307 locality).  Steps are ordered on the device. */
+atom_status atom_step(atom_peer* peer, const int32_t* tokens, float* loss_out);
+
+/* Same, with the tokens already resident in device memory (int32 [C*b, T+1]). */
+atom_status atom_step_device(atom_peer* peer, const int32_t* tokens_dev, float* loss_out);
+
+/* Peer averaging: p <- mean over all ranks' peers of p (fp32 master; m, v stay local).
+ * Collective over all ranks (each rank passes its local peers).  flush == 0 marks the next step as a
+ * sync step (the allreduce runs per sub-model inside that step's backward swap window, between AdamW
+ * and the swap-out, overlapped with the compute of the next sub-model); flush != 0 averages now
+ * (standalone pass over all sub-models).  Returns after enqueueing (flush == 0) or completion. */
+atom_status atom_sync(atom_peer* const* peers, int32_t n_local, int32_t flush);
+
+/* Copy the peer's fp32 master parameters and AdamW moments (canonical order, [N] each) to host
+ * buffers; NULL skips one.  Waits for all outstanding work of the peer. */
+atom_status atom_get_params(atom_peer* peer, float* master_out, float* m_out, float* v_out);
+
+/* Per-op trace of the last completed step: one line per issued op,
+ *   "<lane> <KIND> <seg> <mb|-> <slot|-> <t_start_us> <t_end_us>"
+ * (device timestamps from CUDA events, relative to the step start).  Same buffer rules as
+ * atom_plan_schedule. */
+atom_status atom_get_trace(atom_peer* peer, char* buf, int64_t cap, int64_t* len);
+
+/* Counters since creation (or the last reset) for measurement. */
+typedef struct {
+  int64_t steps;
+  int64_t kernel_launches;        /* kernels launched by the library                                   */
+  int64_t gemm_launches;          /* GEMM launches (the dominant kernel)                               */
+  double gemm_ms;                 /* summed CUDA-event duration of GEMM launches (when timing is on)   */
+  double gemm_flops;              /* algorithmic FLOPs of those launches                               */
+  double h2d_bytes, d2h_bytes;    /* bytes copied host<->device by the swap engine                     */
+  double copy_ms, copy_hidden_ms; /* summed copy time and the part overlapping compute (last step)    */
+  double step_ms;                 /* device time of the last step (first op start -> last op end)     */
+} atom_stats_t;
+atom_status atom_get_stats(atom_peer* peer, atom_stats_t* out);
+/* Reset counters; timing != 0 brackets every GEMM launch with CUDA events (GEMM-time roofline). */
+atom_status atom_reset_stats(atom_peer* peer, int32_t timing);
+
+/* Wait for all outstanding device work of the peer, release everything it owns. */
+atom_status atom_peer_destroy(atom_peer* peer);
+
+/* Thread-local message of the last failure on this thread. */
+const char* atom_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATOM_H */

@@ -1,0 +1,40 @@
+/*
+ * atom_kernels.h -- per-kernel C-ABI of libatom, for the GPU parity tests.
+ *
+ * Each entry runs one hand-written sm_100a kernel on caller-owned DEVICE buffers on the given
+ * CUDA stream (NULL = legacy default stream) and returns atom_status (see atom.h).  Nothing is
+ * synchronised; the caller synchronises before reading results.  Layouts are row-major.
+ */
+#ifndef ATOM_KERNELS_H
+#define ATOM_KERNELS_H
+
+#include "atom.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ATOM_IMPL_TC = 0, ATOM_IMPL_SIMT = 1 };
+/* GEMM epilogue modes (see csrc/epilogue.cuh) */
+enum { ATOM_EPI_STORE = 0, ATOM_EPI_BIAS = 1, ATOM_EPI_BIAS_RES = 2, ATOM_EPI_BIAS_GELU = 3, ATOM_EPI_DGELU = 4,
+       ATOM_EPI_ACC_F32 = 5 };
+
+/* D[m,n] = sum_k A[m,k] B[n,k] (fp32 accumulate), then the epilogue `mode`:
+ *   STORE out = D; BIAS out = D + bias[n]; BIAS_RES out = D + bias[n] + res[m,n];
+ *   BIAS_GELU out = u = D + bias[n], out2 = gelu_tanh(u); DGELU out = D * gelu_tanh'(aux[m,n]);
+ *   ACC_F32 out(fp32)[m,n] += D.       (nn.Linear of the minGPT block)
+ * A is [M, lda] (K-major) or, with a_mn, [K, lda] (M contiguous); B likewise with N.
+ * impl = ATOM_IMPL_TC: tcgen05/TMEM/TMA kernel, dtype must be ATOM_BF16, lda/ldb % 8 == 0;
+ * impl = ATOM_IMPL_SIMT: CUDA-core kernel, dtype ATOM_FP32 or ATOM_BF16.
+ * force_bn: 0 = automatic tile width, else 128 or 256 (TC only). */
+int atom_k_gemm(int impl, int dtype, int M, int N, int K, const void* A, long lda, int a_mn, const void* B, long ldb,
+                int b_mn, int mode, void* out, long ldo, void* out2, long ldo2, const void* bias, const void* res,
+                long ldr, const void* aux, long ldx, int force_bn, void* stream);
+
+/* Number of kernels libatom launched in this process. */
+unsigned long long atom_k_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATOM_KERNELS_H */

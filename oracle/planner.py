@@ -252,10 +252,14 @@ def hfin_bytes(c):
     return al256(wbytes(c) * c.micro_batch * c.seq_len * c.d_model)
 
 
-def stash_bytes(c: PlanCfg, C: int, nb_last: int) -> int:
+def stash_bytes(c: PlanCfg, C: int, nb_last: int, S: int) -> int:
+    """Block stashes (C micro-batches for blocks before the last segment, 1 for blocks of the
+    interleaved last segment) + [M, d] activation buffers at the last segment's boundary:
+    its input for all C micro-batches (S >= 2) and the final hidden state (when the last
+    segment has blocks; it is the input itself when the last segment is the head alone)."""
     L = c.n_layer
-    return (stash_blk_bytes(c) * (C * (L - nb_last) + nb_last)
-            + hfin_bytes(c) * (C if nb_last == 0 else 1))
+    nh = 1 if S == 1 else (C if nb_last == 0 else C + 1)
+    return stash_blk_bytes(c) * (C * (L - nb_last) + nb_last) + hfin_bytes(c) * nh
 
 
 RED_ROWS = 128   # rows per partial-sum chunk in the deterministic column reductions
@@ -345,15 +349,17 @@ class Evaluator:
 
     def mem_fixed(self, C, e1, il, S, Q):
         """device bytes for first segment [0..e1], last [il..n-1], S segments, max need Q."""
-        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1))
+        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1), S)
                 + work_bytes(self.c, C))
 
     def pair_ok(self, C, a, b, last):
         """a=(i,j), b=(j+1,k) adjacent segments; ``last``: b is the final segment.
 
         fwd:        C t_f(a) >= t_loadF(b); for a = segment 1 the prefetch of
-                    segment 2 also overlaps the previous step's backward of
-                    segment 1: C (t_f(a) + t_b(a)) >= t_loadF(b)
+                    segment 2 may start once the previous step's store of segment 2
+                    has landed (during the backward of segment 1), so it overlaps the
+                    rest of that backward and the forward of segment 1:
+                    C (t_f(a) + t_b(a)) >= t_store(b) + t_loadF(b)
         bwd store:  C t_b(a) >= t_store(b)
         bwd load:   C t_b(b) >= t_loadB(a) (no load when a is the resident segment 1);
                     for the final, interleaved segment b:
@@ -362,8 +368,10 @@ class Evaluator:
             return True
         (i, j), (j1, kk) = a, b
         first = i == 0
-        fwd_cover = self.s("tf", i, j) + (self.s("tb", i, j) if first else 0)
-        if C * fwd_cover < self.s("tlf", j1, kk):
+        if first:
+            if C * (self.s("tf", i, j) + self.s("tb", i, j)) < self.s("ts", j1, kk) + self.s("tlf", j1, kk):
+                return False
+        elif C * self.s("tf", i, j) < self.s("tlf", j1, kk):
             return False
         if C * self.s("tb", i, j) < self.s("ts", j1, kk):
             return False
@@ -404,7 +412,7 @@ class Evaluator:
         S = len(ends)
         Q = self.slot_need(ends)
         nb_last = self.nblocks(segs[-1][0], self.n - 1)
-        st = stash_bytes(c, C, nb_last)
+        st = stash_bytes(c, C, nb_last, S)
         wk = work_bytes(c, C)
         r1 = self.r1(ends[0])
         M = c.micro_batch * c.seq_len
@@ -471,7 +479,7 @@ def _dp_for_C(ev: Evaluator, C: int):
             # admissible last segments [il..n-1]
             term = [il for il in range(e1 + 2, n)
                     if ev.need(il, n - 1) <= Q
-                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1)) <= rem]
+                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1), 3) <= rem]
             if not term:
                 continue
             tset = set(term)

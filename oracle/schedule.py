@@ -21,7 +21,8 @@ the identical program.
 Canonical text: one op per line,
   ``<lane> <KIND> <seg> <mb|-> <slot|-> <waits|->``
 with waits a comma-separated list of cross-lane dependencies ``KIND:seg``
-(``PREV:s`` = the release of logical slot s in the previous step).
+(``PREV:s`` = the release of logical slot s in the previous step; ``HOST:k`` = the previous
+step's STORE of segment k, after which segment k's host arena holds the updated state).
 """
 from __future__ import annotations
 
@@ -61,12 +62,12 @@ def _emit(S: int, C: int, sync: bool):
             if mb == 0:
                 if k < S:
                     s, w = alloc(k + 1)
-                    op("h2d", "LOAD_F", k + 1, None, s, [w])
+                    op("h2d", "LOAD_F", k + 1, None, s, [w, f"HOST:{k + 1}"])
                 elif S >= 2:
-                    op("h2d", "LOAD_B", S, None, slot[S])          # AdamW moments of S only
+                    op("h2d", "LOAD_B", S, None, slot[S], [f"HOST:{S}"])   # AdamW moments of S only
                     if S - 1 >= 2:
                         s, w = alloc(S - 1)
-                        op("h2d", "LOAD_B", S - 1, None, s, [w])
+                        op("h2d", "LOAD_B", S - 1, None, s, [w, f"HOST:{S - 1}"])
             if k == S:
                 op("compute", "BWD", S, mb, slot.get(S))
         if 2 <= k < S:
@@ -95,7 +96,7 @@ def _emit(S: int, C: int, sync: bool):
             op("compute", "BWD", k, mb, slot.get(k))
             if mb == 0 and k - 1 >= 2:
                 s, w = alloc(k - 1)
-                op("h2d", "LOAD_B", k - 1, None, s, [w])
+                op("h2d", "LOAD_B", k - 1, None, s, [w, f"HOST:{k - 1}"])
         finish(k)
     return ops, list(q)
 
@@ -146,7 +147,7 @@ def simulate(ops, ev, plan):
             dur = 0
         start = lane_t[lane]
         for w in waits:
-            if not w.startswith("PREV"):
+            if not w.startswith(("PREV", "HOST")):
                 start = max(start, done[w])
         end = start + dur
         lane_t[lane] = end

@@ -1,0 +1,34 @@
+// C-ABI per-kernel entry points (include/atom_kernels.h): used by the GPU parity tests to
+// check each kernel against a plain fp32 reference on the same inputs.
+#include "../../include/atom_kernels.h"
+#include "kernels.h"
+#include <string.h>
+
+using namespace atom;
+
+extern "C" {
+
+int atom_k_gemm(int impl, int dtype, int M, int N, int K, const void* A, long lda, int a_mn, const void* B, long ldb,
+                int b_mn, int mode, void* out, long ldo, void* out2, long ldo2, const void* bias, const void* res,
+                long ldr, const void* aux, long ldx, int force_bn, void* stream) {
+  Epi e;
+  e.mode = mode;
+  e.out = out; e.ldo = ldo; e.out2 = out2; e.ldo2 = ldo2;
+  e.bias = bias; e.res = res; e.ldr = ldr; e.aux = aux; e.ldx = ldx;
+  cudaStream_t st = (cudaStream_t)stream;
+  bool ok;
+  if (impl == ATOM_IMPL_TC) {
+    if (dtype != ATOM_BF16) { set_error("tcgen05 GEMM is bf16 only"); return ATOM_E_INVALID; }
+    ok = gemm_tc(M, N, K, (const bf16*)A, lda, a_mn, (const bf16*)B, ldb, b_mn, e, st, force_bn);
+  } else if (dtype == ATOM_FP32) {
+    ok = gemm_simt<float>(M, N, K, (const float*)A, lda, a_mn, (const float*)B, ldb, b_mn, e, st);
+  } else {
+    ok = gemm_simt<bf16>(M, N, K, (const bf16*)A, lda, a_mn, (const bf16*)B, ldb, b_mn, e, st);
+  }
+  if (ok) return ATOM_OK;
+  return strncmp(last_error(), "CUDA", 4) == 0 ? ATOM_E_CUDA : ATOM_E_INVALID;
+}
+
+unsigned long long atom_k_launch_count(void) { return g_launch_count; }
+
+}  // extern "C"

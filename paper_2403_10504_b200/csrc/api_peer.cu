@@ -1,0 +1,205 @@
+// C-ABI: peer lifecycle, training step, peer averaging, inspection (include/atom.h).
+#include <string.h>
+
+#include <string>
+
+#include "peer.h"
+
+namespace atom {
+bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const void* nccl_id);
+bool peer_step(atom_peer* p, const int32_t* tokens, bool on_device, float* loss);
+bool peer_flush_average(atom_peer* p);
+bool peer_get_params(atom_peer* p, float* master, float* m, float* v);
+bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms);
+bool peer_stats(atom_peer* p, atom_stats_t* s);
+void peer_reset_stats(atom_peer* p, int timing);
+void peer_free(atom_peer* p);
+bool peer_stream_sync(atom_peer* p);
+}  // namespace atom
+
+using namespace atom;
+
+static atom_status fail(atom_peer* p, atom_status code) {
+  if (p && (code == ATOM_E_CUDA || code == ATOM_E_NCCL)) p->poisoned = true;
+  return code;
+}
+static atom_status cuda_or_nccl() {
+  return strncmp(last_error(), "nccl", 4) == 0 ? ATOM_E_NCCL : ATOM_E_CUDA;
+}
+
+extern "C" {
+
+atom_status atom_nccl_unique_id(void* out128) {
+  if (!out128) {
+    set_error("atom_nccl_unique_id: NULL");
+    return ATOM_E_INVALID;
+  }
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    set_error("ncclGetUniqueId failed: %s", ncclGetErrorString(r));
+    return ATOM_E_NCCL;
+  }
+  static_assert(sizeof(id) == 128, "nccl id size");
+  memcpy(out128, &id, 128);
+  return ATOM_OK;
+}
+
+atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan, int32_t device, void* device_arena,
+                             int64_t arena_bytes, const float* init_params, uint64_t seed, const void* nccl_id,
+                             int32_t nranks, int32_t rank, atom_peer** out) {
+  if (!cfg || !plan || !device_arena || !out) {
+    set_error("atom_peer_create: NULL argument");
+    return ATOM_E_INVALID;
+  }
+  *out = nullptr;
+  if (!check_plan(*cfg, *plan)) return ATOM_E_INVALID;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_id)) {
+    set_error("atom_peer_create: invalid nranks/rank/nccl_id");
+    return ATOM_E_INVALID;
+  }
+  if (arena_bytes < plan->device_bytes) {
+    set_error("device arena of %lld bytes < plan.device_bytes %lld", (long long)arena_bytes,
+              (long long)plan->device_bytes);
+    return ATOM_E_CAPACITY;
+  }
+  if ((uintptr_t)device_arena & 255) {
+    set_error("device arena must be 256-byte aligned");
+    return ATOM_E_INVALID;
+  }
+  atom_peer* p = new atom_peer();
+  p->cfg = *cfg;
+  p->cfg.cost_table = nullptr;
+  p->cfg.forced_ends = nullptr;
+  p->cfg.n_forced = 0;
+  p->plan = *plan;
+  make_dims(p->cfg, &p->dm);
+  const ModelDims& dm = p->dm;
+  if (dm.d / dm.h > 128 || dm.d > 6144 || (dm.dtype == ATOM_BF16 && dm.d % 8)) {
+    set_error("unsupported shape: head size <= 128, d_model <= 6144 (and a multiple of 8 for bf16) required");
+    delete p;
+    return ATOM_E_INVALID;
+  }
+  p->device = device;
+  p->arena = (uint8_t*)device_arena;
+  p->arena_bytes = arena_bytes;
+  p->S = plan->n_seg;
+  p->C = plan->C;
+  p->nranks = nranks;
+  p->rank = rank;
+  p->seg_of_node.assign(dm.n_nodes, 0);
+  int lo = 0;
+  for (int k = 1; k <= p->S; ++k) {
+    const int hi = plan->seg_end[k - 1];
+    p->seg_lo.push_back(lo);
+    p->seg_hi.push_back(hi);
+    int64_t P = 0;
+    for (int i = lo; i <= hi; ++i) {
+      P += dm.P[i];
+      p->seg_of_node[i] = k;
+    }
+    p->seg_P.push_back(P);
+    p->seg_off.push_back(dm.node_off[lo]);
+    lo = hi + 1;
+  }
+  for (int i = p->seg_lo[p->S - 1]; i <= p->seg_hi[p->S - 1]; ++i)
+    if (i >= 1 && i <= dm.L) {
+      if (p->l0_last < 0) p->l0_last = i - 1;
+      p->nb_last++;
+    }
+  if (!peer_create(p, init_params, seed, nccl_id)) {
+    atom_status code = strncmp(last_error(), "pinned", 6) == 0 ? ATOM_E_OOM : cuda_or_nccl();
+    std::string msg = last_error();
+    peer_free(p);
+    delete p;
+    set_error("%s", msg.c_str());
+    return code;
+  }
+  *out = p;
+  return ATOM_OK;
+}
+
+static atom_status do_step(atom_peer* p, const int32_t* tokens, bool dev, float* loss) {
+  if (!p || !tokens || !loss) {
+    set_error("atom_step: NULL argument");
+    return ATOM_E_INVALID;
+  }
+  if (p->poisoned) {
+    set_error("peer poisoned by an earlier CUDA/NCCL failure");
+    return ATOM_E_STATE;
+  }
+  if (!peer_step(p, tokens, dev, loss)) return fail(p, cuda_or_nccl());
+  return ATOM_OK;
+}
+
+atom_status atom_step(atom_peer* p, const int32_t* tokens, float* loss_out) { return do_step(p, tokens, false, loss_out); }
+atom_status atom_step_device(atom_peer* p, const int32_t* tokens_dev, float* loss_out) {
+  return do_step(p, tokens_dev, true, loss_out);
+}
+
+atom_status atom_sync(atom_peer* const* peers, int32_t n_local, int32_t flush) {
+  if (!peers || n_local < 1) {
+    set_error("atom_sync: no peers");
+    return ATOM_E_INVALID;
+  }
+  for (int i = 0; i < n_local; ++i) {
+    if (!peers[i]) { set_error("atom_sync: NULL peer"); return ATOM_E_INVALID; }
+    if (peers[i]->poisoned) { set_error("peer poisoned"); return ATOM_E_STATE; }
+  }
+  if (!flush) {
+    for (int i = 0; i < n_local; ++i) peers[i]->sync_next = true;
+    return ATOM_OK;
+  }
+  if (n_local > 1) ncclGroupStart();
+  for (int i = 0; i < n_local; ++i)
+    if (!peer_flush_average(peers[i])) {
+      if (n_local > 1) ncclGroupEnd();
+      return fail(peers[i], cuda_or_nccl());
+    }
+  if (n_local > 1) ncclGroupEnd();
+  return ATOM_OK;
+}
+
+atom_status atom_get_params(atom_peer* p, float* master, float* m, float* v) {
+  if (!p) { set_error("atom_get_params: NULL peer"); return ATOM_E_INVALID; }
+  if (p->poisoned) { set_error("peer poisoned"); return ATOM_E_STATE; }
+  if (!peer_get_params(p, master, m, v)) return fail(p, ATOM_E_CUDA);
+  return ATOM_OK;
+}
+
+atom_status atom_get_trace(atom_peer* p, char* buf, int64_t cap, int64_t* len) {
+  if (!p) { set_error("atom_get_trace: NULL peer"); return ATOM_E_INVALID; }
+  std::string s;
+  double a, b, c;
+  if (!peer_trace(p, &s, &a, &b, &c)) return fail(p, ATOM_E_CUDA);
+  if (len) *len = (int64_t)s.size();
+  if (!buf || cap < (int64_t)s.size() + 1) {
+    set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);
+    return ATOM_E_INVALID;
+  }
+  memcpy(buf, s.data(), s.size());
+  buf[s.size()] = 0;
+  return ATOM_OK;
+}
+
+atom_status atom_get_stats(atom_peer* p, atom_stats_t* out) {
+  if (!p || !out) { set_error("atom_get_stats: NULL"); return ATOM_E_INVALID; }
+  if (!peer_stats(p, out)) return fail(p, ATOM_E_CUDA);
+  return ATOM_OK;
+}
+
+atom_status atom_reset_stats(atom_peer* p, int32_t timing) {
+  if (!p) { set_error("atom_reset_stats: NULL"); return ATOM_E_INVALID; }
+  if (!peer_stream_sync(p)) return fail(p, ATOM_E_CUDA);
+  peer_reset_stats(p, timing);
+  return ATOM_OK;
+}
+
+atom_status atom_peer_destroy(atom_peer* p) {
+  if (!p) return ATOM_OK;
+  peer_free(p);
+  delete p;
+  return ATOM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,503 @@
+// HBM-bound kernels of the GPT-3 training step (activation dtype T in {float, bf16}):
+//   LayerNorm forward / re-apply / backward, column partial sums (bias, LN gain/shift grads),
+//   cross-entropy forward+backward over the vocabulary, embedding gather and its
+//   deterministic backward, GELU re-application, fused AdamW, casts, parameter init, loss sum.
+// Every reduction has a fixed order (no floating-point atomics): swapped and resident runs are
+// bit-identical (north star).
+#include "common.cuh"
+#include "kernels.h"
+#include "planner.h"
+
+namespace atom {
+
+constexpr float LN_EPS = 1e-5f;
+constexpr int LN_THREADS = 128;
+constexpr int LN_MAXE = 48;   // d <= 128 * 48 = 6144
+
+// block-wide sum over LN_THREADS threads, fixed order
+__device__ __forceinline__ float block_sum128(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = sh[0] + sh[1] + sh[2] + sh[3];
+  return t;
+}
+
+__device__ __forceinline__ float ln_out(float x, float mean, float rstd, float g, float b) {
+  return __fmaf_rn(__fmul_rn(__fsub_rn(x, mean), rstd), g, b);
+}
+
+// y = LN(x) * g + b; stats[row] = (mean, rstd)                       (minGPT nn.LayerNorm)
+template <typename T>
+__global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                            const T* __restrict__ b, T* __restrict__ y,
+                                                            float* __restrict__ stats, int d) {
+  __shared__ float sh[4];
+  const long row = blockIdx.x;
+  const T* xr = x + row * d;
+  float v[LN_MAXE];
+  float s = 0.f;
+  int n = 0;
+  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
+    v[n] = to_f(xr[j]);
+    s += v[n];
+  }
+  const float mean = block_sum128(s, sh) / (float)d;
+  float q = 0.f;
+  for (int i = 0; i < n; ++i) {
+    float t = v[i] - mean;
+    q = fmaf(t, t, q);
+  }
+  const float var = block_sum128(q, sh) / (float)d;
+  const float rstd = rsqrtf(var + LN_EPS);
+  T* yr = y + row * d;
+  n = 0;
+  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) yr[j] = from_f<T>(ln_out(v[n], mean, rstd, to_f(g[j]), to_f(b[j])));
+  if (threadIdx.x == 0) {
+    stats[2 * row] = mean;
+    stats[2 * row + 1] = rstd;
+  }
+}
+
+// y = LN(x) from stored stats (bit-identical to the forward's y)
+template <typename T>
+__global__ void ln_apply_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                                const float* __restrict__ stats, T* __restrict__ y, long rows, int d) {
+  const long n = rows * d;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const long r = i / d;
+    const int j = (int)(i - r * d);
+    y[i] = from_f<T>(ln_out(to_f(x[i]), stats[2 * r], stats[2 * r + 1], to_f(g[j]), to_f(b[j])));
+  }
+}
+
+// dx = dres + rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat))
+template <typename T>
+__global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                            const float* __restrict__ stats,
+                                                            const T* __restrict__ g, const T* __restrict__ dres,
+                                                            T* __restrict__ dx, int d) {
+  __shared__ float sh[4];
+  const long row = blockIdx.x;
+  const float mean = stats[2 * row], rstd = stats[2 * row + 1];
+  float xh[LN_MAXE], dg[LN_MAXE];
+  float s1 = 0.f, s2 = 0.f;
+  int n = 0;
+  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
+    xh[n] = (to_f(x[row * d + j]) - mean) * rstd;
+    dg[n] = to_f(dy[row * d + j]) * to_f(g[j]);
+    s1 += dg[n];
+    s2 = fmaf(dg[n], xh[n], s2);
+  }
+  const float m1 = block_sum128(s1, sh) / (float)d;
+  const float m2 = block_sum128(s2, sh) / (float)d;
+  n = 0;
+  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
+    float v = rstd * (dg[n] - m1 - xh[n] * m2);
+    if (dres) v += to_f(dres[row * d + j]);
+    dx[row * d + j] = from_f<T>(v);
+  }
+}
+
+// Column partial sums over chunks of RED_ROWS rows (fixed order):
+//   mode 0: part0[c][j] = sum_r a[r][j]                  (bias gradient: sum of dY over tokens)
+//   mode 1: part0[c][j] = sum_r a[r][j] * xhat[r][j], part1[c][j] = sum_r a[r][j]   (LN gain / shift)
+template <typename T>
+__global__ void col_partials_kernel(int mode, const T* __restrict__ a, long lda, const T* __restrict__ x,
+                                    const float* __restrict__ stats, long rows, int ncols, float* __restrict__ part0,
+                                    float* __restrict__ part1) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (j >= ncols) return;
+  const long r0 = (long)c * RED_ROWS, r1 = min(rows, r0 + RED_ROWS);
+  float s0 = 0.f, s1 = 0.f;
+  for (long r = r0; r < r1; ++r) {
+    const float v = to_f(a[r * lda + j]);
+    if (mode == 1) {
+      const float xh = (to_f(x[r * ncols + j]) - stats[2 * r]) * stats[2 * r + 1];
+      s0 = fmaf(v, xh, s0);
+      s1 += v;
+    } else {
+      s0 += v;
+    }
+  }
+  part0[(long)c * ncols + j] = s0;
+  if (mode == 1) part1[(long)c * ncols + j] = s1;
+}
+
+// out[j] += sum_c part[c][j], chunks in order
+__global__ void reduce_partials_kernel(const float* __restrict__ part, int nchunk, int ncols, float* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  float s = 0.f;
+  for (int c = 0; c < nchunk; ++c) s += part[(long)c * ncols + j];
+  out[j] += s;
+}
+
+// Cross-entropy over one row of logits ("softmax" layer):
+//   loss[row] = logsumexp(z) - z[y];  z <- (softmax(z) - onehot(y)) * scale   (in place)
+template <typename T>
+__global__ void __launch_bounds__(256) ce_kernel(T* __restrict__ logits, long ld, int V,
+                                                 const int32_t* __restrict__ targets, long tstride, int T_,
+                                                 float scale, float* __restrict__ loss) {
+  __shared__ float sh[8];
+  const long row = blockIdx.x;
+  T* z = logits + row * ld;
+  // pass 1: online max / sum-exp per thread
+  float mx = -INFINITY, se = 0.f;
+  for (int j = threadIdx.x; j < V; j += 256) {
+    const float v = to_f(z[j]);
+    if (v > mx) {
+      se = se * __expf(mx - v) + 1.f;
+      mx = v;
+    } else {
+      se += __expf(v - mx);
+    }
+  }
+  // combine (fixed order): max first
+  float m = warp_max(mx);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = m;
+  __syncthreads();
+  float gm = sh[0];
+  for (int i = 1; i < 8; ++i) gm = fmaxf(gm, sh[i]);
+  __syncthreads();
+  float part = (mx == -INFINITY) ? 0.f : se * __expf(mx - gm);
+  part = warp_sum(part);
+  if (l == 0) sh[w] = part;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < 8; ++i) tot += sh[i];
+  const float lse = gm + logf(tot);
+  const long b = row / T_, t = row - b * T_;
+  const int y = targets[b * tstride + t];
+  const float zy = to_f(z[y]);
+  __syncthreads();
+  if (threadIdx.x == 0) loss[row] = lse - zy;
+  const float inv = 1.f / tot;
+  for (int j = threadIdx.x; j < V; j += 256) {
+    float p = __expf(to_f(z[j]) - gm) * inv;
+    if (j == y) p -= 1.f;
+    z[j] = from_f<T>(p * scale);
+  }
+}
+
+// h0[row] = wte[x] + wpe[t]   (P:295, P:307 embedding in sub-model 1)
+template <typename T>
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, long tstride, int T_, const T* __restrict__ wte,
+                                 const T* __restrict__ wpe, T* __restrict__ h, int d) {
+  const long row = blockIdx.x;
+  const long b = row / T_, t = row - b * T_;
+  const int id = tok[b * tstride + t];
+  for (int j = threadIdx.x; j < d; j += blockDim.x)
+    h[row * d + j] = from_f<T>(to_f(wte[(long)id * d + j]) + to_f(wpe[t * d + j]));
+}
+
+// dwpe[t] += sum_b dh[b, t]   (b ascending)
+template <typename T>
+__global__ void embed_bwd_pos_kernel(const T* __restrict__ dh, int B, int T_, int d, float* __restrict__ dwpe) {
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i >= (long)T_ * d) return;
+  float s = 0.f;
+  for (int b = 0; b < B; ++b) s += to_f(dh[(long)b * T_ * d + i]);
+  dwpe[i] += s;
+}
+
+__global__ void tok_count_kernel(const int32_t* __restrict__ tok, long tstride, int T_, long M, int* __restrict__ cnt) {
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const long b = i / T_, t = i - b * T_;
+  atomicAdd(&cnt[tok[b * tstride + t]], 1);   // integer: order-independent
+}
+
+// exclusive scan of cnt[V] -> off[V+1] (one CTA of 1024 threads, fixed order)
+__global__ void __launch_bounds__(1024) scan_kernel(const int* __restrict__ cnt, int V, int* __restrict__ off) {
+  __shared__ int sh[1024];
+  const int per = (V + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(V, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += cnt[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    int v = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int base = threadIdx.x ? sh[threadIdx.x - 1] : 0;
+  for (int i = lo; i < hi; ++i) {
+    off[i] = base;
+    base += cnt[i];
+  }
+  if (threadIdx.x == 1023) off[V] = sh[1023];
+}
+
+__global__ void tok_fill_kernel(const int32_t* __restrict__ tok, long tstride, int T_, long M,
+                                const int* __restrict__ off, int* __restrict__ cur, int* __restrict__ perm) {
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const long b = i / T_, t = i - b * T_;
+  const int v = tok[b * tstride + t];
+  perm[off[v] + atomicAdd(&cur[v], 1)] = (int)i;
+}
+
+// sort each bucket ascending (insertion sort; buckets are token positions of one vocab id)
+__global__ void bucket_sort_kernel(const int* __restrict__ off, int V, int* __restrict__ perm) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int lo = off[v], hi = off[v + 1];
+  for (int i = lo + 1; i < hi; ++i) {
+    int key = perm[i], j = i - 1;
+    while (j >= lo && perm[j] > key) {
+      perm[j + 1] = perm[j];
+      --j;
+    }
+    perm[j + 1] = key;
+  }
+}
+
+// dwte[v] += sum over positions p with token v, ascending p, of dh[p]   (one warp per vocab row)
+template <typename T>
+__global__ void embed_bwd_tok_kernel(const T* __restrict__ dh, const int* __restrict__ off,
+                                     const int* __restrict__ perm, int V, int d, float* __restrict__ dwte) {
+  const int v = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (v >= V) return;
+  const int lo = off[v], hi = off[v + 1];
+  if (lo == hi) return;
+  for (int j = lane; j < d; j += 32) {
+    float s = 0.f;
+    for (int p = lo; p < hi; ++p) s += to_f(dh[(long)perm[p] * d + j]);
+    dwte[(long)v * d + j] += s;
+  }
+}
+
+template <typename T>
+__global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ g, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    g[i] = from_f<T>(gelu_f(to_f(u[i])));
+}
+
+// Fused AdamW on a swapped-in segment (torch AdamW semantics, R19):
+//   p <- p (1 - lr wd); m <- m + (1-b1)(g - m); v <- b2 v + (1-b2) g^2;
+//   p <- p - (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps);  w <- T(p) (optional)
+template <typename T>
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, T* __restrict__ w, long n, float lr, float b1, float b2, float eps,
+                             float wd, float bc1, float sbc2) {
+  const float decay = 1.f - lr * wd, step = lr / bc1;
+  const long n4 = n / 4;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    float4 pp = ((float4*)p)[i], gg = ((const float4*)g)[i], mm = ((float4*)m)[i], vv = ((float4*)v)[i];
+    float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float pk = pa[k] * decay;
+      ma[k] = fmaf(1.f - b1, ga[k] - ma[k], ma[k]);
+      va[k] = fmaf(b2, va[k], (1.f - b2) * ga[k] * ga[k]);
+      const float den = sqrtf(va[k]) / sbc2 + eps;
+      pa[k] = pk - step * ma[k] / den;
+    }
+    ((float4*)p)[i] = pp; ((float4*)m)[i] = mm; ((float4*)v)[i] = vv;
+    if (w) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[4 * i + k] = from_f<T>(pa[k]);
+    }
+  }
+  for (long i = 4 * n4 + blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    float pk = p[i] * decay;
+    m[i] = fmaf(1.f - b1, g[i] - m[i], m[i]);
+    v[i] = fmaf(b2, v[i], (1.f - b2) * g[i] * g[i]);
+    pk = pk - step * m[i] / (sqrtf(v[i]) / sbc2 + eps);
+    p[i] = pk;
+    if (w) w[i] = from_f<T>(pk);
+  }
+}
+
+template <typename T>
+__global__ void cast_kernel(const float* __restrict__ src, T* __restrict__ dst, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = from_f<T>(src[i]);
+}
+
+// minGPT init drawn on the device: normal(0, std) from a counter-based hash (splitmix64 +
+// Box-Muller), constant `fill` when std == 0.
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void init_normal_kernel(float* __restrict__ dst, long n, uint64_t seed, uint64_t base, float std,
+                                   float fill) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    if (std == 0.f) {
+      dst[i] = fill;
+      continue;
+    }
+    const uint64_t r = splitmix(seed * 0x2545F4914F6CDD1Dull + base + (uint64_t)i);
+    const float u1 = ((r >> 40) + 1) * (1.0f / 16777217.0f);
+    const float u2 = ((r & 0xFFFFFF)) * (1.0f / 16777216.0f);
+    dst[i] = std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+  }
+}
+
+// loss = sum(losses[0..n)) * scale, fixed order (one CTA)
+__global__ void __launch_bounds__(1024) loss_sum_kernel(const float* __restrict__ l, long n, float scale,
+                                                        float* __restrict__ out) {
+  __shared__ float sh[32];
+  float s = 0.f;
+  for (long i = threadIdx.x; i < n; i += 1024) s += l[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < 32; ++i) t += sh[i];
+    *out = t * scale;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static inline int grid_for(long n, int threads = 256) {
+  long g = (n + threads - 1) / threads;
+  return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+#define LAUNCH_OK()                      \
+  do {                                   \
+    count_launch();                      \
+    ATOM_CUDA_OK(cudaGetLastError());    \
+  } while (0)
+
+template <typename T>
+bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st) {
+  if (d > LN_THREADS * LN_MAXE) { set_error("LayerNorm: d too large"); return false; }
+  ln_fwd_kernel<T><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st) {
+  ln_apply_kernel<T><<<grid_for(rows * d), 256, 0, st>>>(x, g, b, stats, y, rows, d);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dres, T* dx, float* dg, float* db,
+            float* part, long rows, int d, cudaStream_t st) {
+  ln_bwd_kernel<T><<<rows, LN_THREADS, 0, st>>>(dy, x, stats, g, dres, dx, d);
+  LAUNCH_OK();
+  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
+  float* p0 = part;
+  float* p1 = part + (long)nch * d;
+  col_partials_kernel<T><<<dim3((d + 127) / 128, nch), 128, 0, st>>>(1, dy, d, x, stats, rows, d, p0, p1);
+  LAUNCH_OK();
+  reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p0, nch, d, dg);
+  LAUNCH_OK();
+  reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p1, nch, d, db);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, cudaStream_t st) {
+  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
+  col_partials_kernel<T><<<dim3((n + 127) / 128, nch), 128, 0, st>>>(0, dy, ld, nullptr, nullptr, rows, n, part,
+                                                                      nullptr);
+  LAUNCH_OK();
+  reduce_partials_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, nch, n, db);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool cross_entropy(T* logits, long ld, int V, const int32_t* targets, long tstride, int T_, long rows, float scale,
+                   float* loss, cudaStream_t st) {
+  ce_kernel<T><<<rows, 256, 0, st>>>(logits, ld, V, targets, tstride, T_, scale, loss);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool embed_fwd(const int32_t* tok, long tstride, int T_, long rows, const T* wte, const T* wpe, T* h, int d,
+               cudaStream_t st) {
+  embed_fwd_kernel<T><<<rows, 128, 0, st>>>(tok, tstride, T_, wte, wpe, h, d);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool embed_bwd(const int32_t* tok, long tstride, int T_, int B, const T* dh, int V, int d, float* dwte, float* dwpe,
+               int* scratch, cudaStream_t st) {
+  const long M = (long)B * T_;
+  int* cnt = scratch;
+  int* off = cnt + V;
+  int* cur = off + V + 1;
+  int* perm = cur + V;
+  ATOM_CUDA_OK(cudaMemsetAsync(cnt, 0, sizeof(int) * V, st));
+  ATOM_CUDA_OK(cudaMemsetAsync(cur, 0, sizeof(int) * V, st));
+  tok_count_kernel<<<(M + 255) / 256, 256, 0, st>>>(tok, tstride, T_, M, cnt);
+  LAUNCH_OK();
+  scan_kernel<<<1, 1024, 0, st>>>(cnt, V, off);
+  LAUNCH_OK();
+  tok_fill_kernel<<<(M + 255) / 256, 256, 0, st>>>(tok, tstride, T_, M, off, cur, perm);
+  LAUNCH_OK();
+  bucket_sort_kernel<<<(V + 255) / 256, 256, 0, st>>>(off, V, perm);
+  LAUNCH_OK();
+  embed_bwd_tok_kernel<T><<<(V + 7) / 8, 256, 0, st>>>(dh, off, perm, V, d, dwte);
+  LAUNCH_OK();
+  embed_bwd_pos_kernel<T><<<((long)T_ * d + 255) / 256, 256, 0, st>>>(dh, B, T_, d, dwpe);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool gelu_apply(const T* u, T* g, long n, cudaStream_t st) {
+  gelu_kernel<T><<<grid_for(n), 256, 0, st>>>(u, g, n);
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, float lr, float b1, float b2, float eps,
+           float wd, int t, cudaStream_t st) {
+  const double bc1 = 1.0 - pow((double)b1, t), bc2 = 1.0 - pow((double)b2, t);
+  adamw_kernel<T><<<grid_for(n / 4 + 1), 256, 0, st>>>(p, g, m, v, w, n, lr, b1, b2, eps, wd, (float)bc1,
+                                                       (float)sqrt(bc2));
+  LAUNCH_OK();
+  return true;
+}
+template <typename T>
+bool cast_params(const float* src, T* dst, long n, cudaStream_t st) {
+  cast_kernel<T><<<grid_for(n), 256, 0, st>>>(src, dst, n);
+  LAUNCH_OK();
+  return true;
+}
+bool init_normal(float* dst, long n, uint64_t seed, uint64_t base, float std, float fill, cudaStream_t st) {
+  init_normal_kernel<<<grid_for(n), 256, 0, st>>>(dst, n, seed, base, std, fill);
+  LAUNCH_OK();
+  return true;
+}
+bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) {
+  loss_sum_kernel<<<1, 1024, 0, st>>>(l, n, scale, out);
+  LAUNCH_OK();
+  return true;
+}
+
+#define INST(T)                                                                                                 \
+  template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t);                   \
+  template bool ln_apply<T>(const T*, const T*, const T*, const float*, T*, long, int, cudaStream_t);           \
+  template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, long, \
+                          int, cudaStream_t);                                                                   \
+  template bool bias_grad<T>(const T*, long, long, int, float*, float*, cudaStream_t);                          \
+  template bool cross_entropy<T>(T*, long, int, const int32_t*, long, int, long, float, float*, cudaStream_t);  \
+  template bool embed_fwd<T>(const int32_t*, long, int, long, const T*, const T*, T*, int, cudaStream_t);       \
+  template bool embed_bwd<T>(const int32_t*, long, int, int, const T*, int, int, float*, float*, int*,         \
+                             cudaStream_t);                                                                     \
+  template bool gelu_apply<T>(const T*, T*, long, cudaStream_t);                                                \
+  template bool adamw<T>(float*, const float*, float*, float*, T*, long, float, float, float, float, float, int, \
+                         cudaStream_t);                                                                         \
+  template bool cast_params<T>(const float*, T*, long, cudaStream_t);
+INST(float)
+INST(bf16)
+#undef INST
+
+}  // namespace atom

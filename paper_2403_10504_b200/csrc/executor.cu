@@ -1,0 +1,752 @@
+// The per-peer training step: swap engine + step-program interpreter + GPT-3 compute.
+//
+// PAPER.md §III-C/§IV: sub-models are swapped host -> device "immediately after the current
+// sub-model starts" on a prefetch stream, C mini-batches run through each sub-model, the last
+// forward sub-model is reused by the backward and sub-model 1 (with the embedding) stays on
+// the device.  Every op of the step program (planner.cpp emit_schedule) is
+// issued on its lane's CUDA stream with cross-lane waits on CUDA events:
+//   compute: CAST FWD BWD FREE ADAM RECAST     h2d: LOAD_F LOAD_B     d2h: STORE     comm: AVG
+// GPU AdamW updates each swapped-in segment (north star), NCCL averages masters on sync steps.
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "peer.h"
+
+using namespace atom;
+
+namespace atom {
+extern unsigned long long g_launch_count;
+}
+
+#define PEER_CUDA(expr)                                                                                      \
+  do {                                                                                                       \
+    cudaError_t _e = (expr);                                                                                 \
+    if (_e != cudaSuccess) {                                                                                 \
+      set_error("CUDA error %s at %s:%d: %s", cudaGetErrorString(_e), __FILE__, __LINE__, #expr);            \
+      return false;                                                                                          \
+    }                                                                                                        \
+  } while (0)
+#define PEER_OK(expr) \
+  do {                \
+    if (!(expr)) return false; \
+  } while (0)
+
+namespace {
+
+// ------------------------------------------------------------------ layout helpers
+struct SegView {
+  uint8_t* W;
+  float* grad;
+  float* master;
+  float* m;
+  float* v;
+};
+
+SegView seg_view(const atom_peer* p, int k, uint8_t* base) {
+  const int64_t P = p->seg_P[k - 1];
+  const int64_t wbytes = al256((int64_t)p->dm.wb * P), fbytes = al256(4 * P);
+  SegView s;
+  s.W = base;
+  s.grad = (float*)(base + wbytes);
+  s.master = (float*)(base + wbytes + fbytes);
+  s.m = (float*)(base + wbytes + 2 * fbytes);
+  s.v = (float*)(base + wbytes + 3 * fbytes);
+  return s;
+}
+
+// element offset of (node, tensor) inside its segment's sub-arrays
+int64_t toff(const atom_peer* p, int node, int tensor) {
+  const int k = p->seg_of_node[node];
+  return p->dm.node_off[node] - p->seg_off[k - 1] + p->dm.tensors[node][tensor].off;
+}
+
+struct StashView {
+  uint8_t *x, *qkv, *o, *x2, *u;
+  float *st1, *st2, *lse;
+};
+StashView stash_view(const atom_peer* p, int l, int mb) {
+  const ModelDims& dm = p->dm;
+  const int k = p->seg_of_node[l + 1];
+  const int64_t idx = p->stash_first[l] + (k == p->S ? 0 : mb);
+  uint8_t* b = p->stash + idx * stash_blk_bytes(dm);
+  const int64_t ab = dm.wb, M = dm.M, d = dm.d;
+  StashView s;
+  // the first block of the last segment reads its input from the C-deep boundary buffer
+  s.x = (p->S >= 2 && l == p->l0_last) ? p->hfin + (int64_t)mb * hfin_bytes(dm) : b;
+  b += al256(ab * M * d);
+  s.qkv = b; b += al256(ab * M * 3 * d);
+  s.o = b; b += al256(ab * M * d);
+  s.x2 = b; b += al256(ab * M * d);
+  s.u = b; b += al256(ab * M * 4 * d);
+  s.st1 = (float*)b; b += al256(8 * M);
+  s.st2 = (float*)b; b += al256(8 * M);
+  s.lse = (float*)b;
+  return s;
+}
+
+// input of the head for micro-batch mb: the single final-hidden buffer, or (head alone in the
+// last segment) the C-deep boundary buffer filled by the previous segment
+uint8_t* hfin_ptr(const atom_peer* p, int mb) {
+  const int64_t hb = hfin_bytes(p->dm);
+  if (p->S == 1) return p->hfin;
+  if (p->nb_last == 0) return p->hfin + (int64_t)mb * hb;
+  return p->hfin + (int64_t)p->C * hb;
+}
+
+// scratch sub-buffers (union of block scratch and head scratch; planner work_bytes)
+struct Scratch {
+  uint8_t *G, *A, *DA, *DX2, *DO;
+  float* Dsum;
+  uint8_t *logits, *z, *dz;
+  float* hst;
+};
+Scratch scratch_view(const atom_peer* p) {
+  const int64_t ab = p->dm.wb, M = p->dm.M, d = p->dm.d;
+  Scratch s;
+  uint8_t* b = p->scratch;
+  s.G = b; b += al256(ab * M * 4 * d);
+  s.A = b; b += al256(ab * M * d);
+  s.DA = b; b += al256(ab * M * d);
+  s.DX2 = b; b += al256(ab * M * d);
+  s.DO = b; b += al256(ab * M * d);
+  s.Dsum = (float*)b;
+  b = p->scratch;
+  s.logits = b; b += al256(ab * M * al(p->dm.V, 8));
+  s.z = b; b += al256(ab * M * d);
+  s.dz = b; b += al256(ab * M * d);
+  s.hst = (float*)b;
+  return s;
+}
+
+// ------------------------------------------------------------------ compute dispatch
+template <typename T>
+bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B, long ldb, bool b_mn,
+          const Epi& e) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing) {
+    while (p->gemm_ev.size() < 2 * (p->gemm_n + 1)) {
+      cudaEvent_t ev;
+      PEER_CUDA(cudaEventCreate(&ev));
+      p->gemm_ev.push_back(ev);
+    }
+    e0 = p->gemm_ev[2 * p->gemm_n];
+    e1 = p->gemm_ev[2 * p->gemm_n + 1];
+    PEER_CUDA(cudaEventRecord(e0, p->s_comp));
+  }
+  bool ok;
+  if constexpr (std::is_same<T, bf16>::value)
+    ok = gemm_tc(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, p->s_comp);
+  else
+    ok = gemm_simt<T>(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, p->s_comp);
+  if (!ok) return false;
+  p->gemm_launches++;
+  if (p->timing) {
+    PEER_CUDA(cudaEventRecord(e1, p->s_comp));
+    if (p->gemm_fl.size() < p->gemm_n + 1) p->gemm_fl.resize(p->gemm_n + 1);
+    p->gemm_fl[p->gemm_n] = 2.0 * M * N * (double)K;
+    p->gemm_n++;
+  }
+  return true;
+}
+
+template <typename T>
+bool attn_fwd(atom_peer* p, const T* qkv, T* o, float* lse) {
+  const ModelDims& dm = p->dm;
+  const int dh = dm.d / dm.h;
+  if constexpr (std::is_same<T, bf16>::value)
+    if (attn_fa_supported(dh)) return attn_fwd_fa(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
+  return attn_fwd_simt<T>(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
+}
+template <typename T>
+bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv) {
+  const ModelDims& dm = p->dm;
+  const int dh = dm.d / dm.h;
+  if constexpr (std::is_same<T, bf16>::value)
+    if (attn_fa_supported(dh)) return attn_bwd_fa(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
+  return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
+}
+
+Epi epi(int mode, void* out, long ldo) {
+  Epi e;
+  e.mode = mode;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+
+// forward of block l on micro-batch mb (minGPT Block)
+template <typename T>
+bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
+  const ModelDims& dm = p->dm;
+  const int node = l + 1;
+  const long M = dm.M, d = dm.d;
+  const T* W = (const T*)sv.W;
+  auto w = [&](int t) { return W + toff(p, node, t); };
+  StashView s = stash_view(p, l, mb);
+  Scratch sc = scratch_view(p);
+  T* x = (T*)s.x;
+  PEER_OK(ln_fwd<T>(x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
+  Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
+  e.bias = w(T_BQKV);
+  PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
+  PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
+  e = epi(EPI_BIAS_RES, s.x2, d);
+  e.bias = w(T_BO);
+  e.res = x;
+  e.ldr = d;
+  PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
+  PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp));
+  e = epi(EPI_BIAS_GELU, s.u, 4 * d);
+  e.bias = w(T_BFC);
+  e.out2 = sc.G;
+  e.ldo2 = 4 * d;
+  PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)sc.A, d, false, w(T_WFC), d, false, e));
+  void* out = (l + 1 < dm.L) ? (void*)stash_view(p, l + 1, mb).x : (void*)hfin_ptr(p, mb);
+  e = epi(EPI_BIAS_RES, out, d);
+  e.bias = w(T_BPR);
+  e.res = s.x2;
+  e.ldr = d;
+  PEER_OK(gemm<T>(p, M, d, 4 * d, (const T*)sc.G, 4 * d, false, w(T_WPR), 4 * d, false, e));
+  return true;
+}
+
+// backward of block l on micro-batch mb: dh[mb] (grad of the block output) -> dh[mb] (grad of its input)
+template <typename T>
+bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
+  const ModelDims& dm = p->dm;
+  const int node = l + 1;
+  const long M = dm.M, d = dm.d;
+  const T* W = (const T*)sv.W;
+  auto w = [&](int t) { return W + toff(p, node, t); };
+  auto g = [&](int t) { return sv.grad + toff(p, node, t); };
+  StashView s = stash_view(p, l, mb);
+  Scratch sc = scratch_view(p);
+  T* dy = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
+  T* G = (T*)sc.G;
+  // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
+  PEER_OK(gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
+  PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
+  PEER_OK(bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->s_comp));
+  Epi e = epi(EPI_DGELU, G, 4 * d);
+  e.aux = s.u;
+  e.ldx = 4 * d;
+  PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, e));
+  // MLP fc: u = LN2(x2) W_fc^T + b_fc
+  PEER_OK(ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, (T*)sc.A, M, d, p->s_comp));
+  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)sc.A, d, true, epi(EPI_ACC_F32, g(T_WFC), d)));
+  PEER_OK(bias_grad<T>(G, 4 * d, M, 4 * d, g(T_BFC), p->red, p->s_comp));
+  PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
+  PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
+                    M, d, p->s_comp));
+  // attention projection: x2 = x + o W_o^T + b_o
+  PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d)));
+  PEER_OK(bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->s_comp));
+  PEER_OK(gemm<T>(p, M, d, d, (const T*)sc.DX2, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
+  // attention
+  PEER_OK(attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
+  // QKV: qkv = LN1(x) W_qkv^T + b_qkv
+  PEER_OK(ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, (T*)sc.A, M, d, p->s_comp));
+  PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)sc.A, d, true, epi(EPI_ACC_F32, g(T_WQKV), d)));
+  PEER_OK(bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->s_comp));
+  PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
+  PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
+                    p->red, M, d, p->s_comp));
+  return true;
+}
+
+// head on micro-batch mb: ln_f, lm_head, cross-entropy and their backward (interleaved)
+template <typename T>
+bool head(atom_peer* p, int mb, const SegView& sv) {
+  const ModelDims& dm = p->dm;
+  const int node = dm.L + 1;
+  const long M = dm.M, d = dm.d, V = dm.V, Vp = al(dm.V, 8);
+  const T* W = (const T*)sv.W;
+  auto w = [&](int t) { return W + toff(p, node, t); };
+  auto g = [&](int t) { return sv.grad + toff(p, node, t); };
+  Scratch sc = scratch_view(p);
+  const T* h = (const T*)hfin_ptr(p, mb);
+  PEER_OK(ln_fwd<T>(h, w(T_LNFG), w(T_LNFB), (T*)sc.z, sc.hst, M, d, p->s_comp));
+  PEER_OK(gemm<T>(p, M, V, d, (const T*)sc.z, d, false, w(T_WLM), d, false, epi(EPI_STORE, sc.logits, Vp)));
+  const int32_t* tgt = p->tokens + (int64_t)mb * dm.b * (dm.T + 1) + 1;
+  PEER_OK(cross_entropy<T>((T*)sc.logits, Vp, V, tgt, dm.T + 1, dm.T, M, 1.f / (float)((double)p->C * M),
+                           p->losses + (int64_t)mb * M, p->s_comp));
+  PEER_OK(gemm<T>(p, M, d, V, (const T*)sc.logits, Vp, false, w(T_WLM), d, true, epi(EPI_STORE, sc.dz, d)));
+  PEER_OK(gemm<T>(p, V, d, M, (const T*)sc.logits, Vp, true, (const T*)sc.z, d, true, epi(EPI_ACC_F32, g(T_WLM), d)));
+  T* dout = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
+  PEER_OK(ln_bwd<T>((const T*)sc.dz, h, sc.hst, w(T_LNFG), nullptr, dout, g(T_LNFG), g(T_LNFB), p->red, M, d,
+                    p->s_comp));
+  return true;
+}
+
+template <typename T>
+bool embed_forward(atom_peer* p, int mb, const SegView& sv) {
+  const ModelDims& dm = p->dm;
+  const T* W = (const T*)sv.W;
+  const int32_t* tok = p->tokens + (int64_t)mb * dm.b * (dm.T + 1);
+  T* x0 = (T*)stash_view(p, 0, mb).x;
+  return embed_fwd<T>(tok, dm.T + 1, dm.T, dm.M, W + toff(p, 0, T_WTE), W + toff(p, 0, T_WPE), x0, dm.d, p->s_comp);
+}
+template <typename T>
+bool embed_backward(atom_peer* p, int mb, const SegView& sv) {
+  const ModelDims& dm = p->dm;
+  const int32_t* tok = p->tokens + (int64_t)mb * dm.b * (dm.T + 1);
+  const T* dh = (const T*)(p->dh + (int64_t)mb * dm.M * dm.d * dm.wb);
+  return embed_bwd<T>(tok, dm.T + 1, dm.T, dm.b, dh, dm.V, dm.d, sv.grad + toff(p, 0, T_WTE),
+                      sv.grad + toff(p, 0, T_WPE), p->emb, p->s_comp);
+}
+
+template <typename T>
+bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
+  if (k == p->S && mb == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  for (int node = p->seg_lo[k - 1]; node <= p->seg_hi[k - 1]; ++node) {
+    if (node == 0)
+      PEER_OK(embed_forward<T>(p, mb, sv));
+    else if (node <= p->dm.L)
+      PEER_OK(fwd_block<T>(p, node - 1, mb, sv));
+    else
+      PEER_OK(head<T>(p, mb, sv));
+  }
+  return true;
+}
+template <typename T>
+bool run_bwd(atom_peer* p, int k, int mb, const SegView& sv) {
+  if (k < p->S && mb == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  for (int node = p->seg_hi[k - 1]; node >= p->seg_lo[k - 1]; --node) {
+    if (node == 0)
+      PEER_OK(embed_backward<T>(p, mb, sv));
+    else if (node <= p->dm.L)
+      PEER_OK(bwd_block<T>(p, node - 1, mb, sv));
+    // the head's backward ran inside its forward op
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ op interpreter
+cudaStream_t lane_stream(atom_peer* p, int lane) {
+  switch (lane) {
+    case L_H2D: return p->s_h2d;
+    case L_D2H: return p->s_d2h;
+    case L_COMM: return p->s_comm;
+    default: return p->s_comp;
+  }
+}
+
+bool copy_seg(atom_peer* p, int k, float* dev, float* host, bool h2d) {
+  // one copy per layer (node) of the segment (P:263 layer loading; event per op)
+  for (int node = p->seg_lo[k - 1]; node <= p->seg_hi[k - 1]; ++node) {
+    const int64_t off = p->dm.node_off[node] - p->seg_off[k - 1];
+    const size_t bytes = 4 * (size_t)p->dm.P[node];
+    if (h2d) {
+      PEER_CUDA(cudaMemcpyAsync(dev + off, host + p->dm.node_off[node], bytes, cudaMemcpyHostToDevice, p->s_h2d));
+      p->h2d_bytes += bytes;
+    } else {
+      PEER_CUDA(cudaMemcpyAsync(host + p->dm.node_off[node], dev + off, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+      p->d2h_bytes += bytes;
+    }
+  }
+  return true;
+}
+
+template <typename T>
+bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
+  cudaStream_t st = lane_stream(p, o.lane);
+  for (auto& w : o.waits) {
+    if (w.kind == -1) {
+      auto it = p->rel_of.find(p->slot_phys[w.seg]);
+      if (it != p->rel_of.end() && it->second) PEER_CUDA(cudaStreamWaitEvent(st, it->second, 0));
+    } else if (w.kind == -2) {
+      // host arena of segment w.seg written by the previous step's STORE
+      if (p->t > 1) PEER_CUDA(cudaStreamWaitEvent(st, p->op_ev[{K_STORE, w.seg}], 0));
+    } else {
+      PEER_CUDA(cudaStreamWaitEvent(st, p->op_ev[{w.kind, w.seg}], 0));
+    }
+  }
+  PEER_CUDA(cudaEventRecord(p->trace_ev[2 * idx], st));
+  const int k = o.seg;
+  uint8_t* base = k == 1 ? p->r1 : (o.slot >= 0 ? p->slot_phys[o.slot] : nullptr);
+  SegView sv = base ? seg_view(p, k, base) : SegView{};
+  const int64_t P = p->seg_P[k - 1];
+  switch (o.kind) {
+    case K_CAST:
+      PEER_OK(cast_params<T>(sv.master, (T*)sv.W, P, st));
+      break;
+    case K_FWD:
+      PEER_OK(run_fwd<T>(p, k, o.mb, sv));
+      break;
+    case K_BWD:
+      PEER_OK(run_bwd<T>(p, k, o.mb, sv));
+      break;
+    case K_FREE:
+      break;
+    case K_ADAM: {
+      const float lr_t = p->cfg.warmup_steps > 0
+                             ? p->cfg.lr * (float)std::min(1.0, (double)p->t / (double)p->cfg.warmup_steps)
+                             : p->cfg.lr;
+      T* wout = (k == 1 && !sync) ? (T*)sv.W : nullptr;
+      PEER_OK(adamw<T>(sv.master, sv.grad, sv.m, sv.v, wout, P, lr_t, p->cfg.beta1, p->cfg.beta2, p->cfg.eps,
+                       p->cfg.weight_decay, (int)p->t, st));
+      break;
+    }
+    case K_AVG:
+      if (p->nranks > 1) {
+        ncclResult_t r = ncclAllReduce(sv.master, sv.master, (size_t)P, ncclFloat32, ncclAvg, p->comm, st);
+        if (r != ncclSuccess) {
+          set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
+          return false;
+        }
+      }
+      break;
+    case K_RECAST:
+      PEER_OK(cast_params<T>(sv.master, (T*)sv.W, P, st));
+      break;
+    case K_LOAD_F:
+      PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
+      break;
+    case K_LOAD_B:
+      if (!(k == p->S && p->S >= 2)) PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
+      PEER_OK(copy_seg(p, k, sv.m, p->h_m, true));
+      PEER_OK(copy_seg(p, k, sv.v, p->h_v, true));
+      break;
+    case K_STORE:
+      PEER_OK(copy_seg(p, k, sv.master, p->h_master, false));
+      PEER_OK(copy_seg(p, k, sv.m, p->h_m, false));
+      PEER_OK(copy_seg(p, k, sv.v, p->h_v, false));
+      break;
+  }
+  PEER_CUDA(cudaEventRecord(p->trace_ev[2 * idx + 1], st));
+  cudaEvent_t ev = p->op_ev[{o.kind, o.seg}];
+  PEER_CUDA(cudaEventRecord(ev, st));
+  if (o.kind == K_FREE || o.kind == K_STORE) p->rel_of[p->slot_phys[o.slot]] = ev;
+  // the step's loss is complete after the last micro-batch's head
+  if (o.kind == K_FWD && o.seg == p->S && o.mb == p->C - 1) {
+    PEER_OK(loss_sum(p->losses, (int64_t)p->C * p->dm.M, 1.f / (float)((double)p->C * p->dm.M), p->loss_dev, st));
+    PEER_CUDA(cudaMemcpyAsync(p->h_loss, p->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    PEER_CUDA(cudaEventRecord(p->ev_loss, st));
+  }
+  return true;
+}
+
+template <typename T>
+bool run_step(atom_peer* p, float* loss_out) {
+  p->t += 1;
+  bool sync = (p->cfg.sync_every > 0 && p->t % p->cfg.sync_every == 0) || p->sync_next;
+  p->sync_next = false;
+  if (p->nranks <= 1) sync = sync && false;
+  const std::vector<Op>& ops = sync ? p->ops_sync : p->ops;
+  const std::vector<int>& endq = sync ? p->endq_sync : p->endq;
+  if (p->trace_ev.size() < 2 * ops.size()) {
+    for (size_t i = p->trace_ev.size(); i < 2 * ops.size(); ++i) {
+      cudaEvent_t ev;
+      PEER_CUDA(cudaEventCreate(&ev));
+      p->trace_ev.push_back(ev);
+    }
+  }
+  for (size_t i = 0; i < ops.size(); ++i) PEER_OK(issue_op<T>(p, ops[i], sync, (int)i));
+  p->trace_ops = ops;
+  p->have_trace = true;
+  // relabel logical slots so that the next step starts from the queue [0 .. nslot-1]
+  std::vector<uint8_t*> nphys(p->slot_phys.size());
+  for (size_t i = 0; i < endq.size(); ++i) nphys[i] = p->slot_phys[endq[i]];
+  p->slot_phys = nphys;
+  p->steps++;
+  PEER_CUDA(cudaEventSynchronize(p->ev_loss));
+  *loss_out = *p->h_loss;
+  return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ creation
+namespace atom {
+
+bool peer_stream_sync(atom_peer* p) {
+  PEER_CUDA(cudaSetDevice(p->device));
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+    if (s) PEER_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+static float init_std(const atom_peer* p, int node, int t, float* fill) {
+  const ModelDims& dm = p->dm;
+  *fill = 0.f;
+  if (node == 0) return 0.02f;
+  if (node == dm.L + 1) {
+    if (t == T_LNFG) { *fill = 1.f; return 0.f; }
+    if (t == T_LNFB) return 0.f;
+    return 0.02f;
+  }
+  switch (t) {
+    case T_LN1G: case T_LN2G: *fill = 1.f; return 0.f;
+    case T_WQKV: case T_WFC: return 0.02f;
+    case T_WO: case T_WPR: return 0.02f / sqrtf(2.f * dm.L);
+    default: return 0.f;
+  }
+}
+
+bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const void* nccl_id) {
+  const ModelDims& dm = p->dm;
+  PEER_CUDA(cudaSetDevice(p->device));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
+  for (int kind = K_CAST; kind <= K_STORE; ++kind)
+    for (int k = 1; k <= p->S; ++k) {
+      cudaEvent_t ev;
+      PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      p->op_ev[{kind, k}] = ev;
+    }
+  PEER_CUDA(cudaEventCreateWithFlags(&p->ev_loss, cudaEventDisableTiming | cudaEventBlockingSync));
+  // host arenas
+  const size_t nb = 4 * (size_t)dm.N_pad;
+  if (cudaHostAlloc((void**)&p->h_master, nb, cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc((void**)&p->h_m, nb, cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc((void**)&p->h_v, nb, cudaHostAllocPortable) != cudaSuccess) {
+    set_error("pinned host allocation of %zu bytes x3 failed", nb);
+    return false;
+  }
+  memset(p->h_m, 0, nb);
+  memset(p->h_v, 0, nb);
+  PEER_CUDA(cudaHostAlloc((void**)&p->h_tokens, 4 * (size_t)p->C * dm.b * (dm.T + 1), cudaHostAllocPortable));
+  PEER_CUDA(cudaHostAlloc((void**)&p->h_loss, 64, cudaHostAllocPortable));
+  // carve the arena: r1 | slots | stash | hfin | work
+  uint8_t* a = p->arena;
+  p->r1 = a;
+  a += p->plan.r1_bytes;
+  for (int s = 0; s < p->plan.nslot; ++s) {
+    p->slot_phys.push_back(a);
+    a += p->plan.slot_bytes;
+  }
+  p->stash = a;
+  int64_t idx = 0;
+  for (int l = 0; l < dm.L; ++l) {
+    p->stash_first.push_back(idx);
+    idx += p->seg_of_node[l + 1] == p->S ? 1 : p->C;
+  }
+  a += idx * stash_blk_bytes(dm);
+  p->hfin = a;
+  a = p->stash + p->plan.stash_bytes;
+  const int64_t ab = dm.wb, M = dm.M, d = dm.d;
+  p->tokens = (int32_t*)a; a += al256(4LL * p->C * dm.b * (dm.T + 1));
+  p->dh = a; a += al256(ab * p->C * M * d);
+  p->losses = (float*)a; a += al256(4LL * p->C * M);
+  p->scratch = a;
+  a += std::max(al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T),
+                al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
+  p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);
+  p->emb = (int*)a; a += al256(4LL * (3 * dm.V + 1 + M));
+  p->loss_dev = (float*)a; a += 256;
+  if (a - p->arena != p->plan.device_bytes) {
+    set_error("internal: arena carve %lld != plan.device_bytes %lld", (long long)(a - p->arena),
+              (long long)p->plan.device_bytes);
+    return false;
+  }
+  // initial parameters -> host master (padded layout)
+  memset(p->h_master, 0, nb);
+  if (init_params) {
+    for (int node = 0; node < dm.n_nodes; ++node)
+      for (auto& ts : dm.tensors[node])
+        memcpy(p->h_master + dm.node_off[node] + ts.off, init_params + dm.node_canon[node] + ts.canon, 4 * ts.n);
+  } else {
+    // draw on the device node by node through R1's master region (R1 holds E, the largest node)
+    SegView r = seg_view(p, 1, p->r1);
+    for (int node = 0; node < dm.n_nodes; ++node) {
+      for (size_t t = 0; t < dm.tensors[node].size(); ++t) {
+        float fill;
+        const float sd = init_std(p, node, (int)t, &fill);
+        const TensorSlot& ts = dm.tensors[node][t];
+        PEER_OK(init_normal(r.master + ts.off, ts.n, seed, (uint64_t)(dm.node_canon[node] + ts.canon), sd, fill,
+                            p->s_comp));
+      }
+      PEER_CUDA(cudaMemcpyAsync(p->h_master + dm.node_off[node], r.master, 4 * (size_t)dm.P[node],
+                                cudaMemcpyDeviceToHost, p->s_comp));
+      PEER_CUDA(cudaStreamSynchronize(p->s_comp));
+      // padding stays zero: re-zero the padded gaps (init wrote only tensor ranges)
+    }
+  }
+  // segment 1 becomes resident: master, m, v, compute-dtype weights
+  {
+    SegView r = seg_view(p, 1, p->r1);
+    const int64_t P1 = p->seg_P[0];
+    PEER_CUDA(cudaMemcpyAsync(r.master, p->h_master, 4 * (size_t)P1, cudaMemcpyHostToDevice, p->s_comp));
+    PEER_CUDA(cudaMemsetAsync(r.m, 0, 4 * (size_t)P1, p->s_comp));
+    PEER_CUDA(cudaMemsetAsync(r.v, 0, 4 * (size_t)P1, p->s_comp));
+    if (dm.dtype == ATOM_BF16)
+      PEER_OK(cast_params<bf16>(r.master, (bf16*)r.W, P1, p->s_comp));
+    else
+      PEER_OK(cast_params<float>(r.master, (float*)r.W, P1, p->s_comp));
+    PEER_CUDA(cudaStreamSynchronize(p->s_comp));
+  }
+  if (p->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&p->comm, p->nranks, id, p->rank);
+    if (r != ncclSuccess) {
+      set_error("ncclCommInitRank failed: %s", ncclGetErrorString(r));
+      return false;
+    }
+  }
+  p->ops = emit_schedule(p->S, p->C, false, &p->endq);
+  p->ops_sync = emit_schedule(p->S, p->C, true, &p->endq_sync);
+  PEER_CUDA(cudaEventCreate(&p->step_start));
+  p->launch_base = g_launch_count;
+  return true;
+}
+
+bool peer_step(atom_peer* p, const int32_t* tokens, bool on_device, float* loss) {
+  PEER_CUDA(cudaSetDevice(p->device));
+  const size_t tb = 4 * (size_t)p->C * p->dm.b * (p->dm.T + 1);
+  if (on_device) {
+    PEER_CUDA(cudaMemcpyAsync(p->tokens, tokens, tb, cudaMemcpyDeviceToDevice, p->s_comp));
+  } else {
+    memcpy(p->h_tokens, tokens, tb);
+    PEER_CUDA(cudaMemcpyAsync(p->tokens, p->h_tokens, tb, cudaMemcpyHostToDevice, p->s_comp));
+  }
+  if (p->dm.dtype == ATOM_BF16) return run_step<bf16>(p, loss);
+  return run_step<float>(p, loss);
+}
+
+// standalone averaging pass (atom_sync flush=1): H2D master -> allreduce -> D2H per segment >= 2,
+// in place for the resident segment 1 (then re-derive its compute weights)
+bool peer_flush_average(atom_peer* p) {
+  PEER_OK(peer_stream_sync(p));
+  if (p->nranks <= 1) return true;
+  uint8_t* slot = p->slot_phys.empty() ? nullptr : p->slot_phys[0];
+  for (int k = 1; k <= p->S; ++k) {
+    SegView sv = seg_view(p, k, k == 1 ? p->r1 : slot);
+    const int64_t P = p->seg_P[k - 1];
+    if (k >= 2) PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
+    PEER_CUDA(cudaStreamSynchronize(p->s_h2d));
+    ncclResult_t r = ncclAllReduce(sv.master, sv.master, (size_t)P, ncclFloat32, ncclAvg, p->comm, p->s_comm);
+    if (r != ncclSuccess) {
+      set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
+      return false;
+    }
+    PEER_CUDA(cudaStreamSynchronize(p->s_comm));
+    if (k >= 2) {
+      PEER_OK(copy_seg(p, k, sv.master, p->h_master, false));
+      PEER_CUDA(cudaStreamSynchronize(p->s_d2h));
+    } else if (p->dm.dtype == ATOM_BF16) {
+      PEER_OK(cast_params<bf16>(sv.master, (bf16*)sv.W, P, p->s_comp));
+    } else {
+      PEER_OK(cast_params<float>(sv.master, (float*)sv.W, P, p->s_comp));
+    }
+  }
+  PEER_OK(peer_stream_sync(p));
+  return true;
+}
+
+bool peer_get_params(atom_peer* p, float* master, float* m, float* v) {
+  PEER_OK(peer_stream_sync(p));
+  const ModelDims& dm = p->dm;
+  // segment 1 lives on the device: refresh its host copy
+  SegView r = seg_view(p, 1, p->r1);
+  const size_t b1 = 4 * (size_t)p->seg_P[0];
+  PEER_CUDA(cudaMemcpy(p->h_master, r.master, b1, cudaMemcpyDeviceToHost));
+  PEER_CUDA(cudaMemcpy(p->h_m, r.m, b1, cudaMemcpyDeviceToHost));
+  PEER_CUDA(cudaMemcpy(p->h_v, r.v, b1, cudaMemcpyDeviceToHost));
+  float* outs[3] = {master, m, v};
+  float* srcs[3] = {p->h_master, p->h_m, p->h_v};
+  for (int a = 0; a < 3; ++a) {
+    if (!outs[a]) continue;
+    for (int node = 0; node < dm.n_nodes; ++node)
+      for (auto& ts : dm.tensors[node])
+        memcpy(outs[a] + dm.node_canon[node] + ts.canon, srcs[a] + dm.node_off[node] + ts.off, 4 * ts.n);
+  }
+  return true;
+}
+
+bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms) {
+  PEER_OK(peer_stream_sync(p));
+  out->clear();
+  *step_ms = *copy_ms = *hidden_ms = 0;
+  if (!p->have_trace) return true;
+  const auto& ops = p->trace_ops;
+  std::vector<float> t0(ops.size()), t1(ops.size());
+  float base = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    PEER_CUDA(cudaEventElapsedTime(&t0[i], p->trace_ev[0], p->trace_ev[2 * i]));
+    PEER_CUDA(cudaEventElapsedTime(&t1[i], p->trace_ev[0], p->trace_ev[2 * i + 1]));
+    base = std::min(base, t0[i]);
+  }
+  float lo = 1e30f, hi = -1e30f;
+  std::vector<std::pair<float, float>> comp, copies;
+  char buf[256];
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const Op& o = ops[i];
+    const float a = t0[i] - base, b = t1[i] - base;
+    lo = std::min(lo, a);
+    hi = std::max(hi, b);
+    char mb[16], sl[16];
+    if (o.mb < 0) strcpy(mb, "-"); else snprintf(mb, sizeof mb, "%d", o.mb);
+    if (o.slot < 0) strcpy(sl, "-"); else snprintf(sl, sizeof sl, "%d", o.slot);
+    snprintf(buf, sizeof buf, "%s %s %d %s %s %.1f %.1f\n", lane_name(o.lane), kind_name(o.kind), o.seg, mb, sl,
+             a * 1000.0, b * 1000.0);
+    *out += buf;
+    if (o.lane == L_COMPUTE && (o.kind == K_FWD || o.kind == K_BWD)) comp.push_back({a, b});
+    if ((o.lane == L_H2D || o.lane == L_D2H) && b > a) copies.push_back({a, b});
+  }
+  *step_ms = hi - lo;
+  for (auto& c : copies) {
+    *copy_ms += c.second - c.first;
+    for (auto& k : comp) {
+      float x = std::max(c.first, k.first), y = std::min(c.second, k.second);
+      if (y > x) *hidden_ms += y - x;
+    }
+  }
+  return true;
+}
+
+bool peer_stats(atom_peer* p, atom_stats_t* s) {
+  PEER_OK(peer_stream_sync(p));
+  for (size_t i = 0; i < p->gemm_n; ++i) {
+    float ms;
+    PEER_CUDA(cudaEventElapsedTime(&ms, p->gemm_ev[2 * i], p->gemm_ev[2 * i + 1]));
+    p->gemm_ms_acc += ms;
+    p->gemm_fl_acc += p->gemm_fl[i];
+  }
+  p->gemm_n = 0;
+  memset(s, 0, sizeof(*s));
+  s->steps = p->steps;
+  s->kernel_launches = (int64_t)(g_launch_count - p->launch_base);
+  s->gemm_launches = p->gemm_launches;
+  s->gemm_ms = p->gemm_ms_acc;
+  s->gemm_flops = p->gemm_fl_acc;
+  s->h2d_bytes = p->h2d_bytes;
+  s->d2h_bytes = p->d2h_bytes;
+  std::string tr;
+  PEER_OK(peer_trace(p, &tr, &s->step_ms, &s->copy_ms, &s->copy_hidden_ms));
+  return true;
+}
+
+void peer_reset_stats(atom_peer* p, int timing) {
+  p->steps = 0;
+  p->gemm_launches = 0;
+  p->gemm_ms_acc = p->gemm_fl_acc = 0;
+  p->gemm_n = 0;
+  p->h2d_bytes = p->d2h_bytes = 0;
+  p->launch_base = g_launch_count;
+  p->timing = timing;
+}
+
+void peer_free(atom_peer* p) {
+  cudaSetDevice(p->device);
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+    if (s) cudaStreamSynchronize(s);
+  if (p->comm) ncclCommDestroy(p->comm);
+  for (auto& kv : p->op_ev) cudaEventDestroy(kv.second);
+  for (auto ev : p->trace_ev) cudaEventDestroy(ev);
+  for (auto ev : p->gemm_ev) cudaEventDestroy(ev);
+  if (p->ev_loss) cudaEventDestroy(p->ev_loss);
+  if (p->step_start) cudaEventDestroy(p->step_start);
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+    if (s) cudaStreamDestroy(s);
+  for (float* h : {p->h_master, p->h_m, p->h_v, p->h_loss})
+    if (h) cudaFreeHost(h);
+  if (p->h_tokens) cudaFreeHost(p->h_tokens);
+}
+
+}  // namespace atom

@@ -1,0 +1,47 @@
+// Internal (C++) declarations of libatom's kernel launchers.  The C-ABI lives in
+// include/atom.h (training step) and include/atom_kernels.h (per-kernel test entry points).
+#pragma once
+#include "common.cuh"
+#include "epilogue.cuh"
+
+namespace atom {
+
+const char* last_error();
+
+// GEMM: D[m,n] = sum_k A[m,k] B[n,k] + epilogue.  *_mn = operand stored MN-major ([K][ld]).
+bool gemm_tc(int M, int N, int K, const bf16* A, long lda, bool a_mn, const bf16* B, long ldb, bool b_mn,
+             const Epi& e, cudaStream_t st, int force_bn = 0);
+template <typename T>
+bool gemm_simt(int M, int N, int K, const T* A, long lda, bool a_mn, const T* B, long ldb, bool b_mn, const Epi& e,
+               cudaStream_t st);
+
+// elementwise / reductions (elementwise.cu)
+template <typename T> bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st);
+template <typename T> bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st);
+template <typename T> bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dres, T* dx, float* dg,
+                                  float* db, float* part, long rows, int d, cudaStream_t st);
+template <typename T> bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, cudaStream_t st);
+template <typename T> bool cross_entropy(T* logits, long ld, int V, const int32_t* targets, long tstride, int T_, long rows,
+                                         float scale, float* loss, cudaStream_t st);
+template <typename T> bool embed_fwd(const int32_t* tok, long tstride, int T_, long rows, const T* wte, const T* wpe, T* h,
+                                     int d, cudaStream_t st);
+template <typename T> bool embed_bwd(const int32_t* tok, long tstride, int T_, int B, const T* dh, int V, int d, float* dwte,
+                                     float* dwpe, int* scratch, cudaStream_t st);
+template <typename T> bool gelu_apply(const T* u, T* g, long n, cudaStream_t st);
+template <typename T> bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, float lr, float b1, float b2,
+                                 float eps, float wd, int t, cudaStream_t st);
+template <typename T> bool cast_params(const float* src, T* dst, long n, cudaStream_t st);
+bool init_normal(float* dst, long n, uint64_t seed, uint64_t base, float std, float fill, cudaStream_t st);
+bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st);
+
+// attention (attn_simt.cu: fp32/bf16 CUDA cores; attn_fa.cu: bf16 tensor cores)
+// qkv [B*T, 3d] rows (b,t): [q | k | v], head j at columns j*dh; o [B*T, d]; lse [B, h, T]
+template <typename T> bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
+template <typename T> bool attn_bwd_simt(const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv,
+                                         int B, int T_, int h, int dh, cudaStream_t st);
+bool attn_fwd_fa(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
+bool attn_bwd_fa(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
+                 int T_, int h, int dh, cudaStream_t st);
+bool attn_fa_supported(int dh);
+
+}  // namespace atom

@@ -1,0 +1,80 @@
+// atom_peer: one whole-model replica on one B200 ("volunteer nodes ...
+// independently train a copy of the complete model").
+#pragma once
+#include <nccl.h>
+
+#include <map>
+#include <vector>
+
+#include "../../include/atom.h"
+#include "kernels.h"
+#include "planner.h"
+
+struct atom_peer {
+  atom_model_cfg cfg{};
+  atom_plan_t plan{};
+  atom::ModelDims dm;
+  int device = 0;
+  int S = 0, C = 0;
+  std::vector<int> seg_lo, seg_hi;      // node range of each segment (1-based index k -> [k-1])
+  std::vector<int64_t> seg_P, seg_off;  // padded params and padded offset of each segment
+  std::vector<int> seg_of_node;         // node -> segment index (1-based)
+  int nb_last = 0;                      // blocks in the last segment
+  int l0_last = -1;                     // first block (0-based) of the last segment, -1 if none
+
+  // ---- device arena (caller-owned) ----
+  uint8_t* arena = nullptr;
+  int64_t arena_bytes = 0;
+  uint8_t* r1 = nullptr;                // resident segment 1 state
+  std::vector<uint8_t*> slot_phys;      // physical slot base addresses, indexed by LOGICAL slot id
+  std::vector<cudaEvent_t> slot_rel;    // per physical slot address: event of its last release (or null)
+  std::map<uint8_t*, cudaEvent_t> rel_of;
+  uint8_t* stash = nullptr;
+  std::vector<int64_t> stash_first;     // per block: index of its first stash entry
+  uint8_t* hfin = nullptr;
+  // working set
+  int32_t* tokens = nullptr;
+  uint8_t* dh = nullptr;                // [C][M][d] boundary gradient
+  float* losses = nullptr;              // [C*M]
+  uint8_t* scratch = nullptr;
+  float* red = nullptr;
+  int* emb = nullptr;
+  float* loss_dev = nullptr;
+
+  // ---- host arenas (library-owned, pinned), padded canonical layout ----
+  float* h_master = nullptr;
+  float* h_m = nullptr;
+  float* h_v = nullptr;
+  int32_t* h_tokens = nullptr;          // pinned staging
+  float* h_loss = nullptr;
+
+  // ---- streams / events ----
+  cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_comm = nullptr;
+  std::map<std::pair<int, int>, cudaEvent_t> op_ev;  // (kind, seg) -> completion event
+  cudaEvent_t ev_loss = nullptr;
+
+  // ---- NCCL ----
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // ---- schedule ----
+  std::vector<atom::Op> ops, ops_sync;
+  std::vector<int> endq, endq_sync;
+  int64_t t = 0;                        // optimizer step count
+  bool sync_next = false;
+  bool poisoned = false;
+
+  // ---- trace / stats ----
+  std::vector<cudaEvent_t> trace_ev;    // 2 per op of the last step
+  std::vector<atom::Op> trace_ops;
+  cudaEvent_t step_start = nullptr, step_end = nullptr;
+  bool have_trace = false;
+  int timing = 0;
+  std::vector<cudaEvent_t> gemm_ev;
+  std::vector<double> gemm_fl;
+  size_t gemm_n = 0;
+  int64_t steps = 0, gemm_launches = 0;
+  unsigned long long launch_base = 0;
+  double h2d_bytes = 0, d2h_bytes = 0;
+  double gemm_ms_acc = 0, gemm_fl_acc = 0;
+};

@@ -97,7 +97,7 @@ def _compute_end(ops, ev, p):
         dur = {"FWD": ev.s("tf", i, j), "BWD": ev.s("tb", i, j), "LOAD_F": ev.s("tlf", i, j),
                "LOAD_B": ev.s("tmv", i, j) if (k == S and S >= 2) else ev.s("tlb", i, j),
                "STORE": ev.s("ts", i, j)}.get(kind, 0)
-        t0 = max([lane[ln]] + [done[w] for w in waits if not w.startswith("PREV")])
+        t0 = max([lane[ln]] + [done[w] for w in waits if not w.startswith(("PREV", "HOST"))])
         lane[ln] = t0 + dur
         done[f"{kind}:{k}"] = t0 + dur
     return lane["compute"]
