@@ -1,0 +1,288 @@
+"""Benchmark: swapped GPT-3 training step on B200 peers (Atom, arXiv 2403.10504).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config xl] [--impl atom|reference]
+
+One process per GPU (torchrun for N > 1).  Every rank is a peer holding a whole-model replica
+in pinned host memory; sub-models are swapped through a capped model-state budget (the paper's
+sub-model "GPU capacity") and peers average parameters every K_sync steps.
+Rank 0 prints ONE JSON line.  Timing: W warm-up steps, then K timed steps bracketed by a
+barrier + device synchronize, CUDA events, max over ranks.  Inputs: synthetic tokens
+(PCG64, uniform over the vocabulary); init drawn on the device (minGPT law).
+
+--impl reference times the CPU oracle (oracle/, fp64 numpy) as it stands on this host, on a
+bounded sample of the same workload (see cpu_sample()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "train tokens/s per B200 (swapped GPT-3), swap-hidden %, at 1/2/4/8 peers"
+UNIT = "tokens/s"
+# measured on this pool's B200 box (profiles/box_probe_r01.json): pinned copies, 1 GiB
+H2D_GBS, D2H_GBS, BIDIR_GBS = 55.5, 57.2, 49.7
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+WORKLOADS = {
+    # name: (config, model-state cap bytes, description)
+    "xl": ("xl", 10 * 2 ** 30, "GPT-3 XL 1.3B (24L, d=2048, 16x128 heads, T=2048, b=8), model state capped at 10 GiB"),
+    "2.7b": ("2.7b", 16 * 2 ** 30, "GPT-3 2.7B (32L, d=2560), model state capped at 16 GiB"),
+    "small": ("small", 0, "GPT-3 Small 125M (12L, d=768), per-layer sub-models"),
+    "tiny": ("tiny", 3 * 10 ** 6, "tiny GPT (4L, d=64, T=32, V=256)"),
+}
+
+
+def f_alg_per_token(g):
+    """Algorithmic FLOPs per token: 6(12 L d^2 + d V) + 6 L d (T+1) (causal half)."""
+    L, d, V, T = g.n_layer, g.d_model, g.vocab, g.seq_len
+    return 6 * (12 * L * d * d + d * V) + 6 * L * d * (T + 1)
+
+
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(g, seconds_hint=20.0):
+    """Time the fp64 oracle (fwd + hand bwd + AdamW) on one sequence of the workload through a
+    layer-reduced copy of the model (L = 1, same d, h, T, V) and extrapolate to the full depth by
+    algorithmic FLOPs.  Returns (tokens/s, sample description, cores)."""
+    from oracle import adamw as oadamw
+    from oracle import gpt as ogpt
+    g1 = synth.GPTConfig(g.name + "-L1", 1, g.d_model, g.n_head, g.seq_len, g.vocab, 1)
+    p = synth.init_params(g1, seed=1, dtype=np.float64)
+    toks = synth.tokens(g1, 1, 5)
+    h = oadamw.AdamWHyper()
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        loss, grad = ogpt.loss_and_grad(g1, p, toks)
+        p, m, v = oadamw.adamw_step(h, n + 1, p, grad, m, v)
+        n += 1
+        if time.perf_counter() - t0 > seconds_hint or n >= 3:
+            break
+    dt = (time.perf_counter() - t0) / n
+    rate_sample = g.seq_len / dt
+    rate = rate_sample * f_alg_per_token(g1) / f_alg_per_token(g)
+    desc = (f"oracle fp64 numpy fwd+bwd+AdamW on 1 sequence (T={g.seq_len}) of a 1-block copy of the model "
+            f"(d={g.d_model}, V={g.vocab}); {n} step(s), {dt:.1f} s each; tokens/s scaled to L={g.n_layer} by "
+            f"algorithmic FLOPs per token")
+    return rate, desc, os.cpu_count()
+
+
+def run_reference(args, g, wl_desc):
+    """--impl reference: the oracle timed on this host (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, desc, cores = cpu_sample(g, seconds_hint=0.0)
+        if i >= args.warmup:
+            rates.append(r)
+    val = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": g.seq_len / val * 1000.0,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl_desc, "model": g.name, "seq_len": g.seq_len, "sample_tokens_per_step": g.seq_len},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="xl", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="atom", choices=["atom", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--link-gbs", type=float, default=BIDIR_GBS)
+    args = ap.parse_args()
+    cfg_name, state_cap, wl_desc = WORKLOADS[args.config]
+    g = synth.CONFIGS[cfg_name]
+    if args.impl == "reference":
+        return run_reference(args, g, wl_desc)
+
+    import torch
+    from paper_2403_10504_b200 import atom
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pk = peaks()
+    free, total = torch.cuda.mem_get_info()
+    hbm_budget = int(free - 6 * 2 ** 30)
+    # peer averaging cadence from a global batch of 512 sequences (reading R17)
+    cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(pk["bf16_tflops"] * 1e12),
+                        state_budget=state_cap, lr=1e-4, warmup_steps=3000)
+    plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
+    tok_step = plan.C * g.micro_batch * g.seq_len
+    if world > 1:
+        cfg.sync_every = max(1, math.ceil(512 / (world * plan.C * g.micro_batch)))
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [atom.atom_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    peer = atom.Peer(cfg, plan, device=local, init_params=None, seed=1234, nccl_id=nccl_id, nranks=world, rank=rank)
+    n_seq = plan.C * g.micro_batch
+    host_batches = [synth.tokens(g, n_seq, synth.step_seed(rank, s)) for s in range(args.warmup + 2 * args.steps)]
+    dev_batches = [torch.tensor(b, device=f"cuda:{local}") for b in host_batches]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        peer.step_device(dev_batches[i])
+    barrier()
+
+    def timed(fn, batches):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        losses = [fn(b) for b in batches]
+        torch.cuda.synchronize()   # the step's tail runs on the library's streams: device-wide sync
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms, losses
+
+    # value: inputs resident in HBM; per-GEMM CUDA events on the library's compute stream
+    peer.reset_stats(timing=True)
+    with Clocks(local) as clk:
+        ms, losses = timed(peer.step_device, dev_batches[args.warmup:args.warmup + args.steps])
+    st = peer.stats()
+    # e2e: host tokens through atom_step (pinned staging + H2D in the step), loss read back
+    ms_e2e, _ = timed(peer.step, host_batches[args.warmup + args.steps:])
+    value = world * args.steps * tok_step / (ms / 1000.0)
+    e2e = world * args.steps * tok_step / (ms_e2e / 1000.0)
+
+    gemm_tf = st["gemm_flops"] / (st["gemm_ms"] / 1000.0) / 1e12 if st["gemm_ms"] > 0 else None
+    peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    ms_step = ms / args.steps
+    t_roof = max(tok_step * f_alg_per_token(g) / (pk["bf16_tflops"] * 1e12),
+                 14 * synth.n_params(g) / (H2D_GBS * 1e9), 12 * synth.n_params(g) / (D2H_GBS * 1e9))
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            r, desc, cores = cpu_sample(g)
+            cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": wl_desc, "model": g.name, "global_batch": world * n_seq, "seq_len": g.seq_len,
+                       "micro_batch": g.micro_batch, "C": plan.C, "sub_models": plan.ends(),
+                       "state_budget_bytes": state_cap, "device_arena_bytes": plan.device_bytes,
+                       "parallelism": f"peers{world}", "sync_every": cfg.sync_every,
+                       "l2": "inputs larger than L2 (weights/activations stream through HBM every step)"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 4 * n_seq * (g.seq_len + 1),
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": st["kernel_launches"],
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05)", "achieved": gemm_tf,
+                         "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                         "gemm_share_of_step": st["gemm_ms"] / ms if ms else None},
+            "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
+                              "flops_per_token": f_alg_per_token(g)},
+            "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
+            "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
+            "loss_first_last": [losses[0], losses[-1]],
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    peer.destroy()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -65,10 +65,11 @@ def step_seed(peer: int, step: int) -> int:
     return 1000 * peer + step
 
 
-def structured_tokens(cfg: GPTConfig, n_seq: int, seed: int, ngram: int = 64) -> np.ndarray:
-    """A random ``ngram``-long pattern repeated along every sequence (random phase)."""
+def structured_tokens(cfg: GPTConfig, n_seq: int, seed: int, ngram: int = 64, pattern_seed: int = 99) -> np.ndarray:
+    """One random ``ngram``-long pattern (fixed by ``pattern_seed``) repeated along every
+    sequence, each sequence at a random phase drawn from ``seed``."""
+    pat = np.random.Generator(np.random.PCG64(pattern_seed)).integers(0, cfg.vocab, size=ngram, dtype=np.int64)
     rng = np.random.Generator(np.random.PCG64(seed))
-    pat = rng.integers(0, cfg.vocab, size=ngram, dtype=np.int64)
     out = np.empty((n_seq, cfg.seq_len + 1), dtype=np.int32)
     for i in range(n_seq):
         ph = int(rng.integers(0, ngram))
