@@ -54,7 +54,10 @@ typedef enum {
 } atom_status;
 
 enum { ATOM_FP32 = 0, ATOM_BF16 = 1 };        /* compute dtype of weights and activations       */
-enum { ATOM_ACT_STASH = 1 };                  /* activation policy: stash every block's tensors  */
+/* activation policy: STASH keeps every block's forward tensors for all C micro-batches;
+ * RECOMPUTE keeps only each block's input and re-runs its forward inside the backward
+ * (sub-models before the interleaved last one); AUTO = STASH if any plan is feasible, else RECOMPUTE */
+enum { ATOM_ACT_AUTO = 0, ATOM_ACT_STASH = 1, ATOM_ACT_RECOMPUTE = 2 };
 #define ATOM_MAX_SEG 256
 
 /* Model and training configuration.  Caller-owned, read-only during every call. */
@@ -63,7 +66,7 @@ typedef struct {
   int32_t dtype;          /* ATOM_FP32 (parity path, SIMT kernels) | ATOM_BF16 (performance path, tcgen05)   */
   int32_t C;              /* micro-batches per step; 0 = planner picks the smallest feasible C       */
   int32_t max_C;          /* upper end of the C search (default 64)                                  */
-  int32_t act_policy;     /* ATOM_ACT_STASH                                                                 */
+  int32_t act_policy;     /* ATOM_ACT_AUTO | ATOM_ACT_STASH | ATOM_ACT_RECOMPUTE                            */
   int32_t overlap_check;  /* 1 = enforce the compute >= load constraints (Alg. 1 line 4); 0 = memory only    */
   int64_t peak_flops;     /* FLOP/s of the analytic cost model (e.g. measured bf16 GEMM peak)               */
   int64_t d2h_bw;         /* device->host bytes/s; 0 = same as link_bw                                       */
@@ -83,6 +86,7 @@ typedef struct {
   int32_t seg_end[ATOM_MAX_SEG];  /* last node index of each sub-model (nodes 0=E, 1..L blocks, L+1=H)  */
   int32_t C;                      /* micro-batches per step                                             */
   int32_t nslot;                  /* rotating device slots for sub-models 2..S (0, 2 or 3)              */
+  int32_t act_policy;             /* resolved activation policy (STASH or RECOMPUTE)                    */
   int64_t cut_bytes;              /* activation bytes crossing sub-model boundaries per micro-batch      */
   int64_t r1_bytes;               /* resident sub-model 1 (weights + grad + master + m + v)              */
   int64_t slot_bytes;             /* one slot: the largest swapped sub-model's state                    */

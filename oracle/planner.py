@@ -136,7 +136,7 @@ def determine_C(t_fwd_segs, t_load_segs, max_C=64):
 # 2. the B200 cost model
 # ----------------------------------------------------------------------------
 FP32, BF16 = 0, 1
-ACT_STASH = 1
+ACT_AUTO, ACT_STASH, ACT_RECOMPUTE = 0, 1, 2
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -170,7 +170,8 @@ class PlanCfg:
     peak_flops: int = 1606 * 10 ** 12
     d2h_bw: int = 0               # 0 = link_bw
     cost_table: Optional[List[int]] = None    # per node [t_f_ns, t_b_ns] flattened
-    state_budget: int = 0         # 0 = none; else cap on W1 + NSLOT*slot (model state on device)
+    state_budget: int = 0         # 0 = none; else cap on R1 + NSLOT*slot (model state on device)
+    act_policy: int = ACT_AUTO    # AUTO = stash if any plan is feasible, else recompute
     forced_ends: Optional[List[int]] = None
 
     @classmethod
@@ -197,6 +198,15 @@ def node_flops_fwd(c: PlanCfg):
     return [0] + [fB] * L + [fH]
 
 
+def node_flops_recompute(c: PlanCfg):
+    """Re-forward a block needs inside its backward under ACT_RECOMPUTE: the QKV, attention
+    projection and fc GEMMs (16 d^2 M) and the attention forward (the MLP projection's output is
+    not needed by the backward)."""
+    d, T, b, L = c.d_model, c.seq_len, c.micro_batch, c.n_layer
+    M = b * T
+    return [0] + [16 * d * d * M + 2 * d * T * (T + 1) * b] * L + [0]
+
+
 @dataclasses.dataclass
 class Costs:
     P: List[int]
@@ -207,24 +217,28 @@ class Costs:
     tmv: List[int]
     ts: List[int]
     ff: List[int]
+    tbr: List[int]      # backward time including the block re-forward (ACT_RECOMPUTE)
 
 
 def node_costs(c: PlanCfg, link_bw: int) -> Costs:
     P = node_params(c)
     n = len(P)
     ff = node_flops_fwd(c)
+    fr = node_flops_recompute(c)
     if c.cost_table is not None:
         tf = [c.cost_table[2 * i] for i in range(n)]
         tb = [c.cost_table[2 * i + 1] for i in range(n)]
+        tbr = [tb[i] + (tf[i] if 1 <= i <= c.n_layer else 0) for i in range(n)]
     else:
         tf = [ceil_div(f * 10 ** 9, c.peak_flops) for f in ff]
         tb = [ceil_div(2 * f * 10 ** 9, c.peak_flops) for f in ff]
+        tbr = [ceil_div((2 * f + r) * 10 ** 9, c.peak_flops) for f, r in zip(ff, fr)]
     d2h = c.d2h_bw if c.d2h_bw > 0 else link_bw
     tlf = [ceil_div(4 * p * 10 ** 9, link_bw) for p in P]
     tlb = [ceil_div(12 * p * 10 ** 9, link_bw) for p in P]
     tmv = [ceil_div(8 * p * 10 ** 9, link_bw) for p in P]
     ts = [ceil_div(12 * p * 10 ** 9, d2h) for p in P]
-    return Costs(P, tf, tb, tlf, tlb, tmv, ts, ff)
+    return Costs(P, tf, tb, tlf, tlb, tmv, ts, ff, tbr)
 
 
 def wbytes(c):
@@ -252,14 +266,20 @@ def hfin_bytes(c):
     return al256(wbytes(c) * c.micro_batch * c.seq_len * c.d_model)
 
 
-def stash_bytes(c: PlanCfg, C: int, nb_last: int, S: int) -> int:
+def stash_bytes(c: PlanCfg, C: int, nb_last: int, S: int, policy: int = 1) -> int:
     """Block stashes (C micro-batches for blocks before the last segment, 1 for blocks of the
     interleaved last segment) + [M, d] activation buffers at the last segment's boundary:
     its input for all C micro-batches (S >= 2) and the final hidden state (when the last
-    segment has blocks; it is the input itself when the last segment is the head alone)."""
+    segment has blocks; it is the input itself when the last segment is the head alone).
+    ACT_RECOMPUTE keeps only each earlier block's input (C copies) plus one full stash entry
+    that the backward re-forward fills block by block."""
     L = c.n_layer
     nh = 1 if S == 1 else (C if nb_last == 0 else C + 1)
-    return stash_blk_bytes(c) * (C * (L - nb_last) + nb_last) + hfin_bytes(c) * nh
+    nb_pre = L - nb_last
+    if policy == ACT_RECOMPUTE:
+        return (hfin_bytes(c) * C * nb_pre + stash_blk_bytes(c) * nb_last + hfin_bytes(c) * nh
+                + (stash_blk_bytes(c) if nb_pre > 0 else 0))
+    return stash_blk_bytes(c) * (C * nb_pre + nb_last) + hfin_bytes(c) * nh
 
 
 RED_ROWS = 128   # rows per partial-sum chunk in the deterministic column reductions
@@ -307,6 +327,7 @@ class Plan:
     pred_h2d_B: int
     pred_d2h_B: int
     pred_flops: int
+    act_policy: int = ACT_STASH
     pred_step_ns: int = 0
     pred_hidden_ppm: int = 0
 
@@ -319,17 +340,21 @@ def _seg_tables(c: PlanCfg, k: Costs):
         for x in v:
             s.append(s[-1] + x)
         return s
-    return {name: pre(getattr(k, name)) for name in ("P", "tf", "tb", "tlf", "tlb", "tmv", "ts")}, n
+    return {name: pre(getattr(k, name)) for name in ("P", "tf", "tb", "tbr", "tlf", "tlb", "tmv", "ts")}, n
 
 
 class Evaluator:
     """Feasibility of a partition under the cost model (memory + per-phase overlap)."""
 
-    def __init__(self, c: PlanCfg, budget: int, link_bw: int):
-        self.c, self.budget = c, budget
+    def __init__(self, c: PlanCfg, budget: int, link_bw: int, policy: int = ACT_STASH):
+        self.c, self.budget, self.policy = c, budget, policy
         self.k = node_costs(c, link_bw)
         self.pre, self.n = _seg_tables(c, self.k)
         self.L = c.n_layer
+
+    def tbn(self, i, j):
+        """backward time of a segment that is not the last one (re-forward under recompute)"""
+        return self.s("tbr" if self.policy == ACT_RECOMPUTE else "tb", i, j)
 
     def s(self, name, i, j):
         p = self.pre[name]
@@ -349,7 +374,7 @@ class Evaluator:
 
     def mem_fixed(self, C, e1, il, S, Q):
         """device bytes for first segment [0..e1], last [il..n-1], S segments, max need Q."""
-        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1), S)
+        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1), S, self.policy)
                 + work_bytes(self.c, C))
 
     def pair_ok(self, C, a, b, last):
@@ -369,16 +394,16 @@ class Evaluator:
         (i, j), (j1, kk) = a, b
         first = i == 0
         if first:
-            if C * (self.s("tf", i, j) + self.s("tb", i, j)) < self.s("ts", j1, kk) + self.s("tlf", j1, kk):
+            if C * (self.s("tf", i, j) + self.tbn(i, j)) < self.s("ts", j1, kk) + self.s("tlf", j1, kk):
                 return False
         elif C * self.s("tf", i, j) < self.s("tlf", j1, kk):
             return False
-        if C * self.s("tb", i, j) < self.s("ts", j1, kk):
+        if C * self.tbn(i, j) < self.s("ts", j1, kk):
             return False
         load_a = 0 if first else self.s("tlb", i, j)
         if last:
             return C * (self.s("tf", j1, kk) + self.s("tb", j1, kk)) >= self.s("tmv", j1, kk) + load_a
-        return C * self.s("tb", j1, kk) >= load_a
+        return C * self.tbn(j1, kk) >= load_a
 
     def segments(self, ends):
         starts = [0] + [e + 1 for e in ends[:-1]]
@@ -412,7 +437,7 @@ class Evaluator:
         S = len(ends)
         Q = self.slot_need(ends)
         nb_last = self.nblocks(segs[-1][0], self.n - 1)
-        st = stash_bytes(c, C, nb_last, S)
+        st = stash_bytes(c, C, nb_last, S, self.policy)
         wk = work_bytes(c, C)
         r1 = self.r1(ends[0])
         M = c.micro_batch * c.seq_len
@@ -422,20 +447,26 @@ class Evaluator:
         d2h = sum(12 * p for p in P[1:])
         return Plan(S, list(ends), C, nslot(S), (S - 1) * wbytes(c) * M * c.d_model, r1, al256(Q), st, wk,
                     r1 + nslot(S) * al256(Q) + st + wk, h2d, d2h,
-                    C * sum(3 * f for f in self.k.ff))
+                    C * sum(3 * f for f in self.k.ff), self.policy)
+
+
+def policies(c: PlanCfg):
+    """ACT_AUTO tries the full stash first and falls back to recompute (reading R28)."""
+    return [ACT_STASH, ACT_RECOMPUTE] if c.act_policy == ACT_AUTO else [c.act_policy]
 
 
 def brute_force_plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
     """Enumerate every contiguous partition x every C (SURVEY §8(c) c.5 pin)."""
-    ev = Evaluator(c, budget, link_bw)
-    Cs = [c.C] if c.C > 0 else range(1, c.max_C + 1)
-    for C in Cs:
-        feas = [e for e in all_partitions(ev.n) if ev.violation(C, list(e)) is None]
-        if c.forced_ends is not None:
-            feas = [e for e in feas if list(e) == list(c.forced_ends)]
-        if feas:
-            best = min(feas, key=lambda e: ((len(e) - 1) * wbytes(c), len(e), e))
-            return ev.make_plan(C, list(best))
+    for pol in policies(c):
+        ev = Evaluator(c, budget, link_bw, pol)
+        Cs = [c.C] if c.C > 0 else range(1, c.max_C + 1)
+        for C in Cs:
+            feas = [e for e in all_partitions(ev.n) if ev.violation(C, list(e)) is None]
+            if c.forced_ends is not None:
+                feas = [e for e in feas if list(e) == list(c.forced_ends)]
+            if feas:
+                best = min(feas, key=lambda e: ((len(e) - 1) * wbytes(c), len(e), e))
+                return ev.make_plan(C, list(best))
     return None
 
 
@@ -479,7 +510,7 @@ def _dp_for_C(ev: Evaluator, C: int):
             # admissible last segments [il..n-1]
             term = [il for il in range(e1 + 2, n)
                     if ev.need(il, n - 1) <= Q
-                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1), 3) <= rem]
+                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1), 3, ev.policy) <= rem]
             if not term:
                 continue
             tset = set(term)
@@ -527,16 +558,17 @@ def _dp_for_C(ev: Evaluator, C: int):
 
 
 def dp_plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
-    ev = Evaluator(c, budget, link_bw)
-    Cs = [c.C] if c.C > 0 else range(1, c.max_C + 1)
-    for C in Cs:
-        if c.forced_ends is not None:
-            if ev.violation(C, list(c.forced_ends)) is None:
-                return ev.make_plan(C, list(c.forced_ends))
-            continue
-        ends = _dp_for_C(ev, C)
-        if ends is not None:
-            return ev.make_plan(C, ends)
+    for pol in policies(c):
+        ev = Evaluator(c, budget, link_bw, pol)
+        Cs = [c.C] if c.C > 0 else range(1, c.max_C + 1)
+        for C in Cs:
+            if c.forced_ends is not None:
+                if ev.violation(C, list(c.forced_ends)) is None:
+                    return ev.make_plan(C, list(c.forced_ends))
+                continue
+            ends = _dp_for_C(ev, C)
+            if ends is not None:
+                return ev.make_plan(C, ends)
     return None
 
 
@@ -546,7 +578,7 @@ def plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
     p = dp_plan(c, budget, link_bw)
     if p is not None:
         from . import schedule
-        ev = Evaluator(c, budget, link_bw)
+        ev = Evaluator(c, budget, link_bw, p.act_policy)
         sim = schedule.simulate(schedule.emit(p.n_seg, p.C, False), ev, p)
         p.pred_step_ns, p.pred_hidden_ppm = sim["makespan"], sim["hidden_ppm"]
     return p

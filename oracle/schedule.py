@@ -136,7 +136,8 @@ def simulate(ops, ev, plan):
         if kind == "FWD":
             dur = seg("tf", k)
         elif kind == "BWD":
-            dur = seg("tb", k)
+            i, j = segs[k - 1]
+            dur = seg("tb", k) if k == S else ev.tbn(i, j)
         elif kind == "LOAD_F":
             dur = seg("tlf", k)
         elif kind == "LOAD_B":

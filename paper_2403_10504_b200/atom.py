@@ -22,7 +22,7 @@ lib = C.CDLL(LIB_PATH)
 ATOM_OK, ATOM_E_INVALID, ATOM_E_INFEASIBLE, ATOM_E_CAPACITY = 0, -1, -2, -3
 ATOM_E_CUDA, ATOM_E_NCCL, ATOM_E_OOM, ATOM_E_STATE = -4, -5, -6, -7
 FP32, BF16 = 0, 1
-ACT_STASH = 1
+ACT_AUTO, ACT_STASH, ACT_RECOMPUTE = 0, 1, 2
 MAX_SEG = 256
 IMPL_TC, IMPL_SIMT = 0, 1
 EPI_STORE, EPI_BIAS, EPI_BIAS_RES, EPI_BIAS_GELU, EPI_DGELU, EPI_ACC_F32 = range(6)
@@ -82,7 +82,7 @@ class ModelCfg(C.Structure):
 
 class Plan(C.Structure):
     _fields_ = [("n_seg", C.c_int32), ("seg_end", C.c_int32 * MAX_SEG), ("C", C.c_int32), ("nslot", C.c_int32),
-                ("cut_bytes", C.c_int64), ("r1_bytes", C.c_int64), ("slot_bytes", C.c_int64),
+                ("act_policy", C.c_int32), ("cut_bytes", C.c_int64), ("r1_bytes", C.c_int64), ("slot_bytes", C.c_int64),
                 ("stash_bytes", C.c_int64), ("work_bytes", C.c_int64), ("device_bytes", C.c_int64),
                 ("pred_step_ns", C.c_int64), ("pred_hidden_ppm", C.c_int64), ("pred_h2d_B", C.c_int64),
                 ("pred_d2h_B", C.c_int64), ("pred_flops", C.c_int64), ("hbm_budget", C.c_int64),
@@ -99,12 +99,12 @@ class Plan(C.Structure):
 
 def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 10 ** 12, d2h_bw=0,
              state_budget=0, cost_table=None, forced_ends=None, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8,
-             weight_decay=0.01, warmup_steps=3000, sync_every=0):
+             weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0):
     """atom_model_cfg from a synth.GPTConfig-like object (keeps ctypes arrays alive on the struct)."""
     c = ModelCfg()
     c.n_layer, c.d_model, c.n_head, c.seq_len, c.vocab, c.micro_batch = (
         g.n_layer, g.d_model, g.n_head, g.seq_len, g.vocab, g.micro_batch)
-    c.dtype, c.C, c.max_C, c.act_policy, c.overlap_check = dtype, C_, max_C, ACT_STASH, overlap_check
+    c.dtype, c.C, c.max_C, c.act_policy, c.overlap_check = dtype, C_, max_C, act_policy, overlap_check
     c.peak_flops, c.d2h_bw, c.state_budget = peak_flops, d2h_bw, state_budget
     if cost_table is not None:
         arr = (C.c_int64 * len(cost_table))(*cost_table)

@@ -86,6 +86,7 @@ atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan,
   p->S = plan->n_seg;
   p->C = plan->C;
   p->nranks = nranks;
+  p->policy = plan->act_policy;
   p->rank = rank;
   p->seg_of_node.assign(dm.n_nodes, 0);
   int lo = 0;

@@ -70,12 +70,20 @@ struct StashView {
 StashView stash_view(const atom_peer* p, int l, int mb) {
   const ModelDims& dm = p->dm;
   const int k = p->seg_of_node[l + 1];
-  const int64_t idx = p->stash_first[l] + (k == p->S ? 0 : mb);
-  uint8_t* b = p->stash + idx * stash_blk_bytes(dm);
   const int64_t ab = dm.wb, M = dm.M, d = dm.d;
   StashView s;
+  uint8_t* b;
+  if (p->blk_full[l]) {
+    b = p->stash + p->blk_off[l] + (k == p->S ? 0 : mb) * stash_blk_bytes(dm);
+    s.x = b;
+  } else {
+    // ACT_RECOMPUTE: the block's input checkpoint for this micro-batch; the rest of the entry
+    // is the shared one the backward re-forward fills
+    s.x = p->stash + p->blk_off[l] + (int64_t)mb * hfin_bytes(dm);
+    b = p->stash + p->rc_off;
+  }
   // the first block of the last segment reads its input from the C-deep boundary buffer
-  s.x = (p->S >= 2 && l == p->l0_last) ? p->hfin + (int64_t)mb * hfin_bytes(dm) : b;
+  if (p->S >= 2 && l == p->l0_last) s.x = p->hfin + (int64_t)mb * hfin_bytes(dm);
   b += al256(ab * M * d);
   s.qkv = b; b += al256(ab * M * 3 * d);
   s.o = b; b += al256(ab * M * d);
@@ -226,6 +234,25 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   Scratch sc = scratch_view(p);
   T* dy = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
   T* G = (T*)sc.G;
+  if (!p->blk_full[l]) {
+    // ACT_RECOMPUTE: re-run the block forward from its input checkpoint into the shared entry
+    // (same kernels and inputs as the forward: bit-identical tensors); the MLP projection's
+    // output is not needed by the backward and is skipped
+    PEER_OK(ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
+    Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
+    e.bias = w(T_BQKV);
+    PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
+    PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
+    e = epi(EPI_BIAS_RES, s.x2, d);
+    e.bias = w(T_BO);
+    e.res = s.x;
+    e.ldr = d;
+    PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
+    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp));
+    e = epi(EPI_BIAS, s.u, 4 * d);
+    e.bias = w(T_BFC);
+    PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)sc.A, d, false, w(T_WFC), d, false, e));
+  }
   // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
   PEER_OK(gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
@@ -520,14 +547,22 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
     p->slot_phys.push_back(a);
     a += p->plan.slot_bytes;
   }
+  // stash: per block either full entries (1 for the interleaved last segment, else C) or, under
+  // ACT_RECOMPUTE, C input checkpoints; then the re-forward entry; then the boundary buffers
   p->stash = a;
-  int64_t idx = 0;
+  int64_t off = 0;
+  const bool rc = p->policy == ATOM_ACT_RECOMPUTE;
   for (int l = 0; l < dm.L; ++l) {
-    p->stash_first.push_back(idx);
-    idx += p->seg_of_node[l + 1] == p->S ? 1 : p->C;
+    const bool last = p->seg_of_node[l + 1] == p->S;
+    p->blk_off.push_back(off);
+    p->blk_full.push_back(!rc || last);
+    off += (!rc || last) ? (last ? 1 : p->C) * stash_blk_bytes(dm) : (int64_t)p->C * hfin_bytes(dm);
   }
-  a += idx * stash_blk_bytes(dm);
-  p->hfin = a;
+  if (rc && dm.L > p->nb_last) {
+    p->rc_off = off;
+    off += stash_blk_bytes(dm);
+  }
+  p->hfin = p->stash + off;
   a = p->stash + p->plan.stash_bytes;
   const int64_t ab = dm.wb, M = dm.M, d = dm.d;
   p->tokens = (int32_t*)a; a += al256(4LL * p->C * dm.b * (dm.T + 1));

@@ -268,6 +268,225 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ 2-CTA variant
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with tcgen05.mma.cta_group::2:
+// each CTA stages its 128 rows of A and its 128 rows of B (half the operand bytes per SM of the
+// 1-CTA kernel), the leader CTA issues the M=256 MMAs, each CTA's TMEM holds its 128 x 256
+// accumulator half and its own epilogue drains it.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+struct Tc2Cfg {
+  static constexpr int BN = 256;         // cluster tile N (each CTA stages BN/2 rows of B)
+  static constexpr int HB = BN / 2;
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = BM * BK * 2;  // this CTA's 128 rows of A
+  static constexpr int B_BYTES = HB * BK * 2;  // this CTA's 128 rows of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, Epi epi) {
+  using Cfg = Tc2Cfg;
+  constexpr int BN = Cfg::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int num_m = (M + 2 * BM - 1) / (2 * BM);
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 2);   // leader arrive.expect_tx + peer's remote arrive
+      mbar_init(&empty[s], 1);  // one multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads (used in the leader)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        const int m0 = (tile % num_m) * 2 * BM + rank * BM;
+        const int n0 = (tile / num_m) * BN + rank * Cfg::HB;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          const uint32_t lbar = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader)
+            mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          else
+            mbar_arrive_cluster(lbar);
+          const int k0 = kb * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * 8192, &tmA, lbar, m0 + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(sa, &tmA, lbar, k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < Cfg::HB / 64; ++j) tma_load_2d_pair(sb + j * 8192, &tmB, lbar, n0 + 64 * j, k0);
+          } else {
+            tma_load_2d_pair(sb, &tmB, lbar, k0, n0);
+          }
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad =
+                  A_MN ? desc_sw128(sa + kk * 2048, 8192, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
+              const uint64_t bd =
+                  B_MN ? desc_sw128(sb + kk * 2048, 8192, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
+              tc_mma_pair(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            tc_commit_pair(&empty[stage]);
+            if (kb == num_kb - 1) tc_commit_pair(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (tile % num_m) * 2 * BM + rank * BM;
+      const int n0 = (tile / num_m) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const long m = m0 + 32 * q + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + c0, v);
+        const int nb = n0 + c0;
+        if (m < M && nb < N) {
+          if (nb + 32 <= N) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) epi_vec8_bf16(epi, m, nb + 8 * j, v + 8 * j);
+          } else {
+            for (int j = 0; j < 32 && nb + j < N; ++j) epi_scalar<bf16>(epi, m, nb + j, v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -337,8 +556,48 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
   return true;
 }
 
-// Tile width: the one with the better last-wave fill (BN = 256 preferred on ties).
+template <bool A_MN, bool B_MN>
+static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e,
+                       cudaStream_t st) {
+  auto kern = gemm_tc2_kernel<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    ATOM_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + Tc2Cfg::BN - 1) / Tc2Cfg::BN);
+  const int clusters = std::min(tiles, num_sms() / 2);
+  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, M, N, K, e);
+  count_launch();
+  ATOM_CUDA_OK(cudaGetLastError());
+  return true;
+}
+
+// Kernel choice by estimated time: waves x per-SM tile work / relative speed
+// (2-CTA 256x256 > 1-CTA 128x256 > 1-CTA 128x128 in per-SM efficiency).  Returns 512 for the
+// 2-CTA kernel, else the 1-CTA tile width.
+static bool g_allow_2cta = false;  // enabled once the 2-CTA kernel is validated on the GPU
 static int pick_bn(int M, int N) {
+  const int sms = num_sms();
+  struct V { int code; long tiles; int slots; double work, speed; };
+  V vs[3] = {{512, (long)((M + 255) / 256) * ((N + 255) / 256), sms / 2, 128.0 * 256, 1.0},
+             {256, (long)((M + 127) / 128) * ((N + 255) / 256), sms, 128.0 * 256, 0.85},
+             {128, (long)((M + 127) / 128) * ((N + 127) / 128), sms, 128.0 * 128, 0.78}};
+  double best = 1e300;
+  int code = 256;
+  for (auto& v : vs) {
+    if (v.code == 512 && (!g_allow_2cta || M < 256)) continue;
+    const double t = (double)((v.tiles + v.slots - 1) / v.slots) * v.work / v.speed;
+    if (t < best * 0.999) {
+      best = t;
+      code = v.code;
+    }
+  }
+  return code;
+}
+
+// (legacy chooser kept for reference by force_bn = 1)
+static int pick_bn_1cta(int M, int N) {
   const int sms = num_sms();
   double best = -1;
   int bn_best = 256;
@@ -365,8 +624,15 @@ bool gemm_tc(int M, int N, int K, const bf16* A, long lda, bool a_mn, const bf16
   CUtensorMap ta, tb;
   bool ok = a_mn ? make_map(&ta, A, M, K, lda, 64, 64) : make_map(&ta, A, K, M, lda, 64, BM);
   if (!ok) return false;
-  ok = b_mn ? make_map(&tb, B, N, K, ldb, 64, 64) : make_map(&tb, B, K, N, ldb, 64, bn);
+  // the 2-CTA kernel stages 128 rows of B per CTA
+  ok = b_mn ? make_map(&tb, B, N, K, ldb, 64, 64) : make_map(&tb, B, K, N, ldb, 64, bn == 512 ? 128 : bn);
   if (!ok) return false;
+  if (bn == 512) {
+    if (!a_mn && !b_mn) return launch_tc2<false, false>(ta, tb, M, N, K, e, st);
+    if (!a_mn && b_mn) return launch_tc2<false, true>(ta, tb, M, N, K, e, st);
+    if (a_mn && b_mn) return launch_tc2<true, true>(ta, tb, M, N, K, e, st);
+    return launch_tc2<true, false>(ta, tb, M, N, K, e, st);
+  }
 #define ATOM_TC_CASE(BN_, AM, BMN) \
   if (bn == BN_ && a_mn == AM && b_mn == BMN) return launch_tc<BN_, AM, BMN>(ta, tb, M, N, K, e, st);
   ATOM_TC_CASE(256, false, false)

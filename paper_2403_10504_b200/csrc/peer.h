@@ -30,7 +30,10 @@ struct atom_peer {
   std::vector<cudaEvent_t> slot_rel;    // per physical slot address: event of its last release (or null)
   std::map<uint8_t*, cudaEvent_t> rel_of;
   uint8_t* stash = nullptr;
-  std::vector<int64_t> stash_first;     // per block: index of its first stash entry
+  int policy = ATOM_ACT_STASH;          // resolved activation policy of the plan
+  std::vector<int64_t> blk_off;         // per block: byte offset (from stash) of its first stash entry
+  std::vector<char> blk_full;           // per block: full entries (1) or input checkpoints only (0)
+  int64_t rc_off = -1;                  // byte offset of the entry the backward re-forward fills
   uint8_t* hfin = nullptr;
   // working set
   int32_t* tokens = nullptr;

@@ -88,12 +88,17 @@ Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw) 
     if (i >= 1 && i <= dm.L) ff = 24 * d * d * M + 2 * d * T * (T + 1) * b;
     if (i == dm.L + 1) ff = 2 * d * V * M;
     k.ff.push_back((int64_t)ff);
+    const bool blk = i >= 1 && i <= dm.L;
     if (c.cost_table) {
       k.tf.push_back(c.cost_table[2 * i]);
       k.tb.push_back(c.cost_table[2 * i + 1]);
+      k.tbr.push_back(k.tb.back() + (blk ? k.tf.back() : 0));
     } else {
+      // re-forward inside the backward: QKV, proj and fc GEMMs + attention (not the MLP projection)
+      const i128 fr = blk ? 16 * d * d * M + 2 * d * T * (T + 1) * b : 0;
       k.tf.push_back(ceil_ns(ff, c.peak_flops));
       k.tb.push_back(ceil_ns(2 * ff, c.peak_flops));
+      k.tbr.push_back(ceil_ns(2 * ff + fr, c.peak_flops));
     }
     const i128 p = dm.P[i];
     k.P.push_back(dm.P[i]);
@@ -113,9 +118,13 @@ int64_t stash_blk_bytes(const ModelDims& dm) {
          al256(8 * M) + al256(8 * M) + al256(4LL * dm.b * dm.h * dm.T);
 }
 int64_t hfin_bytes(const ModelDims& dm) { return al256((int64_t)dm.wb * dm.M * dm.d); }
-int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S) {
+int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int policy) {
   const int64_t nh = S == 1 ? 1 : (nb_last == 0 ? C : C + 1);
-  return stash_blk_bytes(dm) * ((int64_t)C * (dm.L - nb_last) + nb_last) + hfin_bytes(dm) * nh;
+  const int64_t nb_pre = dm.L - nb_last;
+  if (policy == ATOM_ACT_RECOMPUTE)  // block inputs only + one entry the re-forward fills
+    return hfin_bytes(dm) * C * nb_pre + stash_blk_bytes(dm) * nb_last + hfin_bytes(dm) * nh +
+           (nb_pre > 0 ? stash_blk_bytes(dm) : 0);
+  return stash_blk_bytes(dm) * ((int64_t)C * nb_pre + nb_last) + hfin_bytes(dm) * nh;
 }
 int64_t work_bytes(const ModelDims& dm, int C) {
   const int64_t ab = dm.wb, d = dm.d, V = dm.V, T = dm.T, b = dm.b, h = dm.h, M = dm.M;
@@ -139,18 +148,22 @@ struct Eval {
   const atom_model_cfg& c;
   const ModelDims& dm;
   int64_t budget;
+  int policy;
   Costs k;
   int n;
-  std::vector<int64_t> pP, ptf, ptb, ptlf, ptlb, ptmv, pts;
-  Eval(const atom_model_cfg& c_, const ModelDims& dm_, int64_t budget_, int64_t link)
-      : c(c_), dm(dm_), budget(budget_), k(node_costs(c_, dm_, link)), n(dm_.n_nodes) {
+  std::vector<int64_t> pP, ptf, ptb, ptbr, ptlf, ptlb, ptmv, pts;
+  Eval(const atom_model_cfg& c_, const ModelDims& dm_, int64_t budget_, int64_t link, int policy_)
+      : c(c_), dm(dm_), budget(budget_), policy(policy_), k(node_costs(c_, dm_, link)), n(dm_.n_nodes) {
     auto pre = [&](const std::vector<int64_t>& v, std::vector<int64_t>& p) {
       p.assign(v.size() + 1, 0);
       for (size_t i = 0; i < v.size(); ++i) p[i + 1] = p[i] + v[i];
     };
-    pre(k.P, pP); pre(k.tf, ptf); pre(k.tb, ptb); pre(k.tlf, ptlf); pre(k.tlb, ptlb); pre(k.tmv, ptmv); pre(k.ts, pts);
+    pre(k.P, pP); pre(k.tf, ptf); pre(k.tb, ptb); pre(k.tbr, ptbr); pre(k.tlf, ptlf); pre(k.tlb, ptlb);
+    pre(k.tmv, ptmv); pre(k.ts, pts);
   }
   static int64_t s(const std::vector<int64_t>& p, int i, int j) { return p[j + 1] - p[i]; }
+  // backward time of a segment that is not the last one (re-forward under recompute)
+  int64_t tbn(int i, int j) const { return s(policy == ATOM_ACT_RECOMPUTE ? ptbr : ptb, i, j); }
   int64_t need(int i, int j) const { return seg_need(dm, s(pP, i, j)); }
   int nblocks(int i, int j) const {
     int lo = std::max(i, 1), hi = std::min(j, dm.L);
@@ -163,14 +176,14 @@ struct Eval {
     const int j1 = j + 1;
     const bool first = i == 0;
     if (first) {
-      if ((i128)C * (s(ptf, i, j) + s(ptb, i, j)) < (i128)s(pts, j1, kk) + s(ptlf, j1, kk)) return false;
+      if ((i128)C * (s(ptf, i, j) + tbn(i, j)) < (i128)s(pts, j1, kk) + s(ptlf, j1, kk)) return false;
     } else if ((i128)C * s(ptf, i, j) < s(ptlf, j1, kk)) {
       return false;
     }
-    if ((i128)C * s(ptb, i, j) < s(pts, j1, kk)) return false;
+    if ((i128)C * tbn(i, j) < s(pts, j1, kk)) return false;
     const i128 load_a = first ? 0 : s(ptlb, i, j);
     if (b_last) return (i128)C * (s(ptf, j1, kk) + s(ptb, j1, kk)) >= s(ptmv, j1, kk) + load_a;
-    return (i128)C * s(ptb, j1, kk) >= load_a;
+    return (i128)C * tbn(j1, kk) >= load_a;
   }
   int64_t slot_need(const std::vector<int>& ends) const {
     int64_t q = 0;
@@ -180,7 +193,7 @@ struct Eval {
   int64_t device_bytes(int C, const std::vector<int>& ends) const {
     const int S = (int)ends.size();
     const int il = S == 1 ? 0 : ends[S - 2] + 1;
-    return r1(ends[0]) + nslot_for(S) * al256(slot_need(ends)) + stash_bytes(dm, C, nblocks(il, n - 1), S) +
+    return r1(ends[0]) + nslot_for(S) * al256(slot_need(ends)) + stash_bytes(dm, C, nblocks(il, n - 1), S, policy) +
            work_bytes(dm, C);
   }
   // nullptr if feasible, else the first violated constraint
@@ -231,7 +244,7 @@ bool dp_for_C(const Eval& ev, int C, std::vector<int>* best_out) {
       std::vector<char> term(n, 0);
       bool any = false;
       for (int il = e1 + 2; il < n; ++il)
-        if (ev.need(il, n - 1) <= Q && stash_bytes(ev.dm, C, ev.nblocks(il, n - 1), 3) <= rem) {
+        if (ev.need(il, n - 1) <= Q && stash_bytes(ev.dm, C, ev.nblocks(il, n - 1), 3, ev.policy) <= rem) {
           term[il] = 1;
           any = true;
         }
@@ -404,7 +417,7 @@ static void simulate(const Eval& ev, const std::vector<int>& ends, const std::ve
     int64_t dur = 0;
     switch (o.kind) {
       case K_FWD: dur = seg(ev.ptf, o.seg); break;
-      case K_BWD: dur = seg(ev.ptb, o.seg); break;
+      case K_BWD: dur = o.seg == S ? seg(ev.ptb, o.seg) : seg(ev.ptbr.empty() || ev.policy != ATOM_ACT_RECOMPUTE ? ev.ptb : ev.ptbr, o.seg); break;
       case K_LOAD_F: dur = seg(ev.ptlf, o.seg); break;
       case K_LOAD_B: dur = (o.seg == S && S >= 2) ? seg(ev.ptmv, o.seg) : seg(ev.ptlb, o.seg); break;
       case K_STORE: dur = seg(ev.pts, o.seg); break;
@@ -442,7 +455,8 @@ static void fill_plan(const Eval& ev, int C, const std::vector<int>& ends, int64
   p->cut_bytes = (int64_t)(S - 1) * dm.wb * dm.M * dm.d;
   p->r1_bytes = ev.r1(ends[0]);
   p->slot_bytes = al256(ev.slot_need(ends));
-  p->stash_bytes = stash_bytes(dm, C, ev.nblocks(il, ev.n - 1), S);
+  p->stash_bytes = stash_bytes(dm, C, ev.nblocks(il, ev.n - 1), S, ev.policy);
+  p->act_policy = ev.policy;
   p->work_bytes = work_bytes(dm, C);
   p->device_bytes = p->r1_bytes + p->nslot * p->slot_bytes + p->stash_bytes + p->work_bytes;
   std::vector<int64_t> P;
@@ -480,11 +494,15 @@ bool check_plan(const atom_model_cfg& c, const atom_plan_t& p) {
       set_error("invalid plan: segment ends must ascend");
       return false;
     }
-  Eval ev(c, dm, p.hbm_budget > 0 ? p.hbm_budget : 1, p.link_bw > 0 ? p.link_bw : 1);
+  if (p.act_policy != ATOM_ACT_STASH && p.act_policy != ATOM_ACT_RECOMPUTE) {
+    set_error("invalid plan: act_policy");
+    return false;
+  }
+  Eval ev(c, dm, p.hbm_budget > 0 ? p.hbm_budget : 1, p.link_bw > 0 ? p.link_bw : 1, p.act_policy);
   const int S = p.n_seg;
   const int il = S == 1 ? 0 : ends[S - 2] + 1;
   if (ev.r1(ends[0]) != p.r1_bytes || al256(ev.slot_need(ends)) != p.slot_bytes || nslot_for(S) != p.nslot ||
-      stash_bytes(dm, p.C, ev.nblocks(il, n - 1), S) != p.stash_bytes || work_bytes(dm, p.C) != p.work_bytes ||
+      stash_bytes(dm, p.C, ev.nblocks(il, n - 1), S, p.act_policy) != p.stash_bytes || work_bytes(dm, p.C) != p.work_bytes ||
       p.r1_bytes + p.nslot * p.slot_bytes + p.stash_bytes + p.work_bytes != p.device_bytes) {
     set_error("invalid plan: arena sizes do not match this configuration (plan made for another cfg?)");
     return false;
@@ -504,8 +522,8 @@ bool make_plan(const atom_model_cfg& c, int64_t budget, int64_t link, atom_plan_
     set_error("invalid config: C / max_C out of range");
     return false;
   }
-  if (c.act_policy != 0 && c.act_policy != ATOM_ACT_STASH) {
-    set_error("invalid config: act_policy (only ATOM_ACT_STASH is implemented)");
+  if (c.act_policy != ATOM_ACT_AUTO && c.act_policy != ATOM_ACT_STASH && c.act_policy != ATOM_ACT_RECOMPUTE) {
+    set_error("invalid config: act_policy");
     return false;
   }
   std::vector<int> forced;
@@ -519,32 +537,38 @@ bool make_plan(const atom_model_cfg& c, int64_t budget, int64_t link, atom_plan_
       return false;
     }
   }
-  Eval ev(c, dm, budget, link);
   const int c_lo = c.C > 0 ? c.C : 1, c_hi = c.C > 0 ? c.C : maxC;
   const char* first_violation = nullptr;
   int bad_pair = 0;
-  for (int C = c_lo; C <= c_hi; ++C) {
-    std::vector<int> ends;
-    if (!forced.empty()) {
-      int bp = 0;
-      const char* v = ev.violation(C, forced, &bp);
-      if (!v) {
-        if ((int)forced.size() > ATOM_MAX_SEG) break;
-        fill_plan(ev, C, forced, link, out);
+  // ACT_AUTO: the full stash if any plan is feasible, else re-forward inside the backward
+  std::vector<int> pols;
+  if (c.act_policy == ATOM_ACT_AUTO) pols = {ATOM_ACT_STASH, ATOM_ACT_RECOMPUTE};
+  else pols = {c.act_policy};
+  for (int pol : pols) {
+    Eval ev(c, dm, budget, link, pol);
+    for (int C = c_lo; C <= c_hi; ++C) {
+      std::vector<int> ends;
+      if (!forced.empty()) {
+        int bp = 0;
+        const char* v = ev.violation(C, forced, &bp);
+        if (!v) {
+          fill_plan(ev, C, forced, link, out);
+          return true;
+        }
+        if (!first_violation) { first_violation = v; bad_pair = bp; }
+        continue;
+      }
+      if (dp_for_C(ev, C, &ends)) {
+        if ((int)ends.size() > ATOM_MAX_SEG) {
+          set_error("plan needs %d sub-models (> %d)", (int)ends.size(), ATOM_MAX_SEG);
+          return false;
+        }
+        fill_plan(ev, C, ends, link, out);
         return true;
       }
-      if (!first_violation) { first_violation = v; bad_pair = bp; }
-      continue;
-    }
-    if (dp_for_C(ev, C, &ends)) {
-      if ((int)ends.size() > ATOM_MAX_SEG) {
-        set_error("plan needs %d sub-models (> %d)", (int)ends.size(), ATOM_MAX_SEG);
-        return false;
-      }
-      fill_plan(ev, C, ends, link, out);
-      return true;
     }
   }
+  Eval ev(c, dm, budget, link, pols[0]);
   if (first_violation)
     set_error("no feasible C in [%d, %d] for the forced partition: first violation at C=%d: %s%s", c_lo, c_hi, c_lo,
               first_violation, bad_pair ? " (sub-models around the first failing boundary)" : "");

@@ -44,6 +44,7 @@ bool make_dims(const atom_model_cfg& c, ModelDims* out);
 
 struct Costs {
   std::vector<int64_t> P, tf, tb, tlf, tlb, tmv, ts;
+  std::vector<int64_t> tbr;  // backward incl. the block re-forward (ATOM_ACT_RECOMPUTE)
   std::vector<int64_t> ff;  // forward FLOPs per micro-batch
 };
 Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw);
@@ -52,7 +53,7 @@ Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw);
 int64_t seg_need(const ModelDims& dm, int64_t P_seg);
 int64_t stash_blk_bytes(const ModelDims& dm);
 int64_t hfin_bytes(const ModelDims& dm);
-int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S);
+int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int policy);
 int64_t work_bytes(const ModelDims& dm, int C);
 int nslot_for(int S);
 

@@ -86,7 +86,7 @@ MAJORS = [(False, False), (False, True), (True, True), (True, False)]
 
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("majors", MAJORS)
-@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("bn", [128, 256, 512], ids=["1cta-128", "1cta-256", "2cta-256x256"])
 def test_tc_gemm_store(shape, majors, bn):
     M, N, K = shape
     ref, got = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, atom.EPI_STORE, bn)
@@ -96,9 +96,10 @@ def test_tc_gemm_store(shape, majors, bn):
 @pytest.mark.parametrize("mode", [atom.EPI_BIAS, atom.EPI_BIAS_RES, atom.EPI_BIAS_GELU, atom.EPI_DGELU,
                                   atom.EPI_ACC_F32])
 @pytest.mark.parametrize("majors", [(False, False), (False, True), (True, True)])
-def test_tc_gemm_epilogues(mode, majors):
+@pytest.mark.parametrize("bn", [0, 512], ids=["auto", "2cta"])
+def test_tc_gemm_epilogues(mode, majors, bn):
     M, N, K = 384, 520, 256
-    ref, got = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, mode)
+    ref, got = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, mode, bn)
     _close(ref, got, torch.bfloat16, K)
 
 

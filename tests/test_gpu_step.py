@@ -23,13 +23,15 @@ MINI = synth.GPTConfig("mini", n_layer=3, d_model=128, n_head=2, seq_len=128, vo
 HYPER = oadamw.AdamWHyper(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, warmup_steps=0)
 
 
-def make_peer(g, dtype, C, ends=None, init=None, seed=0, sync_every=0):
+def make_peer(g, dtype, C, ends=None, init=None, seed=0, sync_every=0, policy=0):
     cfg = atom.make_cfg(g, dtype=dtype, C_=C, overlap_check=0, forced_ends=ends, lr=HYPER.lr, beta1=HYPER.beta1,
                         beta2=HYPER.beta2, eps=HYPER.eps, weight_decay=HYPER.weight_decay, warmup_steps=0,
-                        sync_every=sync_every)
+                        sync_every=sync_every, act_policy=policy)
     plan = atom.atom_plan(cfg, 10 ** 11, 10 ** 10)
     if ends is not None:
         assert plan.ends() == list(ends)
+    if policy:
+        assert plan.act_policy == policy
     return atom.Peer(cfg, plan, init_params=init, seed=seed)
 
 
@@ -49,13 +51,14 @@ def per_tensor_rel(a, b, g):
     return out
 
 
-@pytest.mark.parametrize("g,ends", [(TINY, None), (TINY, [2, 5]), (TINY, [1, 2, 3, 4, 5]), (MINI, [1, 2, 4])],
-                         ids=["tiny-resident", "tiny-2seg", "tiny-5seg", "mini-3seg"])
-def test_fp32_step_matches_oracle(g, ends):
+@pytest.mark.parametrize("g,ends,pol", [(TINY, None, 0), (TINY, [2, 5], 0), (TINY, [1, 2, 3, 4, 5], 0),
+                                         (MINI, [1, 2, 4], 0), (MINI, [0, 2, 4], 2)],
+                         ids=["tiny-resident", "tiny-2seg", "tiny-5seg", "mini-3seg", "mini-3seg-recompute"])
+def test_fp32_step_matches_oracle(g, ends, pol):
     C = 2
     init = synth.init_params(g, seed=1234, perturb=True)
     toks = batches(g, C, 2)
-    peer = make_peer(g, atom.FP32, C, ends, init)
+    peer = make_peer(g, atom.FP32, C, ends, init, policy=pol)
     ref = opeers.Peer(g, init.astype(np.float64), HYPER)
     for s in range(2):
         loss = peer.step(toks[s])
@@ -83,13 +86,14 @@ def test_swapped_equals_resident_bit_exact(dtype, g, plans):
     base_losses = [res.step(t) for t in toks]
     base = res.params()
     res.destroy()
-    for ends in plans:
-        p = make_peer(g, dt, C, ends, init)
+    # every plan with the full stash, and with block re-forward in the backward (ACT_RECOMPUTE)
+    for ends, pol in [(e, atom.ACT_STASH) for e in plans] + [(e, atom.ACT_RECOMPUTE) for e in plans]:
+        p = make_peer(g, dt, C, ends, init, policy=pol)
         losses = [p.step(t) for t in toks]
         got = p.params()
-        assert losses == base_losses, (ends, losses, base_losses)
+        assert losses == base_losses, (ends, pol, losses, base_losses)
         for k in ("master", "m", "v"):
-            assert np.array_equal(got[k], base[k]), (ends, k)
+            assert np.array_equal(got[k], base[k]), (ends, pol, k)
         p.destroy()
 
 

@@ -139,6 +139,7 @@ def _rand_plan_cfg(rng):
                    max_C=rng.randint(1, 6), overlap_check=rng.choice([0, 1, 1, 1]))
     if rng.random() < 0.4:
         c.state_budget = rng.randint(10 ** 4, 10 ** 7)
+    c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE])
     if rng.random() < 0.7:
         tf = [0] + [rng.randint(1, 400) for _ in range(n - 1)]
         c.cost_table = sum(([t, 2 * t + rng.randint(0, 50)] for t in tf), [])
@@ -220,5 +221,13 @@ def test_full_stash_2p7b_needs_more_link_than_pcie():
     ~3*P/W tokens per step; at 50 GB/s the full activation stash of 2.7B does not fit
     next to a 16 GiB model-state cap in 178 GB of HBM (recompute is required)."""
     g = synth.CONFIGS["2.7b"]
-    c = pl.PlanCfg.from_gpt(g, max_C=16, state_budget=16 * 2 ** 30)
+    c = pl.PlanCfg.from_gpt(g, max_C=16, state_budget=16 * 2 ** 30, act_policy=pl.ACT_STASH)
     assert pl.dp_plan(c, 178 * 10 ** 9, 50 * 10 ** 9) is None
+    # ACT_AUTO falls back to re-forwarding blocks inside the backward (reading R28)
+    c.act_policy = pl.ACT_AUTO
+    p = pl.dp_plan(c, 178 * 10 ** 9, 50 * 10 ** 9)
+    assert p is not None and p.act_policy == pl.ACT_RECOMPUTE and p.n_seg >= 3
+    ev = pl.Evaluator(c, 178 * 10 ** 9, 50 * 10 ** 9, pl.ACT_RECOMPUTE)
+    assert ev.violation(p.C, p.seg_end) is None
+    # the stash keeps block inputs only: far below the full stash at the same C
+    assert p.stash_bytes < pl.stash_bytes(c, p.C, 0, p.n_seg, pl.ACT_STASH) / 4
