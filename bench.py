@@ -176,6 +176,7 @@ def main():
 
     import torch
     from paper_2403_10504_b200 import atom
+    from paper_2403_10504_b200 import dist as adist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -192,14 +193,8 @@ def main():
                         state_budget=state_cap, lr=1e-4, warmup_steps=3000)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
     tok_step = plan.C * g.micro_batch * g.seq_len
-    if world > 1:
-        cfg.sync_every = max(1, math.ceil(512 / (world * plan.C * g.micro_batch)))
-    nccl_id = None
-    if world > 1:
-        import torch.distributed as dist
-        obj = [atom.atom_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    cfg.sync_every = adist.sync_every(world, plan.C, g.micro_batch)     # global batch 512
+    nccl_id = adist.bootstrap_nccl_id(atom.atom_nccl_unique_id) if world > 1 else None
     peer = atom.Peer(cfg, plan, device=local, init_params=None, seed=1234, nccl_id=nccl_id, nranks=world, rank=rank)
     n_seq = plan.C * g.micro_batch
     host_batches = [synth.tokens(g, n_seq, synth.step_seed(rank, s)) for s in range(args.warmup + 2 * args.steps)]
@@ -224,12 +219,7 @@ def main():
         torch.cuda.synchronize()   # the step's tail runs on the library's streams: device-wide sync
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([ms], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
+        ms = adist.max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
         return ms, losses
 
     # value: inputs resident in HBM; per-GEMM CUDA events on the library's compute stream

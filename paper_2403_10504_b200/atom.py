@@ -256,3 +256,20 @@ class Peer:
 def atom_sync(peers, flush=False):
     arr = (_P * len(peers))(*[p.h for p in peers])
     check(lib.atom_sync(arr, len(peers), int(flush)))
+
+
+ATTN_TC, ATTN_MMA, ATTN_SIMT = 0, 1, 2
+lib.atom_k_attn_fwd.restype = C.c_int
+lib.atom_k_attn_fwd.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                C.c_int, C.c_void_p]
+lib.atom_k_attn_bwd.restype = C.c_int
+lib.atom_k_attn_bwd.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+
+
+def k_attn_fwd(impl, dtype, qkv, o, lse, B, T, h, dh, stream=0):
+    return check(lib.atom_k_attn_fwd(impl, dtype, qkv, o, lse, B, T, h, dh, stream or None))
+
+
+def k_attn_bwd(impl, dtype, qkv, o, dout, lse, dsum, dqkv, B, T, h, dh, stream=0):
+    return check(lib.atom_k_attn_bwd(impl, dtype, qkv, o, dout, lse, dsum, dqkv, B, T, h, dh, stream or None))

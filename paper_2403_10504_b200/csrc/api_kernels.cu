@@ -29,6 +29,41 @@ int atom_k_gemm(int impl, int dtype, int M, int N, int K, const void* A, long ld
   return strncmp(last_error(), "CUDA", 4) == 0 ? ATOM_E_CUDA : ATOM_E_INVALID;
 }
 
+int atom_k_attn_fwd(int impl, int dtype, const void* qkv, void* o, float* lse, int B, int T, int h, int dh,
+                    void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  bool ok;
+  if (dtype == ATOM_FP32) {
+    ok = attn_fwd_simt<float>((const float*)qkv, (float*)o, lse, B, T, h, dh, st);
+  } else if (impl == ATOM_ATTN_TC) {
+    ok = attn_fwd_tc((const bf16*)qkv, (bf16*)o, lse, B, T, h, dh, st);
+  } else if (impl == ATOM_ATTN_MMA) {
+    ok = attn_fwd_fa((const bf16*)qkv, (bf16*)o, lse, B, T, h, dh, st);
+  } else {
+    ok = attn_fwd_simt<bf16>((const bf16*)qkv, (bf16*)o, lse, B, T, h, dh, st);
+  }
+  if (ok) return ATOM_OK;
+  return strncmp(last_error(), "CUDA", 4) == 0 ? ATOM_E_CUDA : ATOM_E_INVALID;
+}
+
+int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
+                    float* dsum, void* dqkv, int B, int T, int h, int dh, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  bool ok;
+  if (dtype == ATOM_FP32)
+    ok = attn_bwd_simt<float>((const float*)qkv, (const float*)o, (const float*)dout, lse, dsum, (float*)dqkv, B, T,
+                              h, dh, st);
+  else if (impl == ATOM_ATTN_TC)
+    ok = attn_bwd_tc((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);
+  else if (impl == ATOM_ATTN_MMA)
+    ok = attn_bwd_fa((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);
+  else
+    ok = attn_bwd_simt<bf16>((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h,
+                             dh, st);
+  if (ok) return ATOM_OK;
+  return strncmp(last_error(), "CUDA", 4) == 0 ? ATOM_E_CUDA : ATOM_E_INVALID;
+}
+
 unsigned long long atom_k_launch_count(void) { return g_launch_count; }
 
 }  // extern "C"

@@ -1,0 +1,861 @@
+// Causal attention forward on 5th-gen tensor cores (tcgen05 / TMEM / TMA), flash style.
+// minGPT CausalSelfAttention: o_t = sum_{s<=t} softmax_s(q_t.k_s/sqrt(dh)) v_s,
+// LSE stashed for the backward.  One CTA per (b, h, 128-query block):
+//   warp 0     TMA: Q once, then K_j / V_j (two stages) from the qkv activation [tokens, 3d]
+//   warp 1     MMA issuer: S_j = Q K_j^T into TMEM (two S buffers), O += P_j V_j into TMEM
+//   warp 2     TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4-7  softmax: thread i owns query row i = TMEM lane i; reads its S row with tcgen05.ld,
+//              online softmax in the log2 domain with lazy O rescaling (only when the running
+//              max grows by more than 2^8), writes P (bf16) into a 128B-swizzled K-major smem
+//              tile that is the A operand of the P V MMA; finally O / l -> bf16, LSE.
+// K and V tiles are loaded with the same TMA box ([128 keys, 64 features] panels); V is read by
+// the MMA as an MN-major B operand (features contiguous), so no transpose is materialised.
+// Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace atom {
+namespace atc {
+
+constexpr int BQ = 128, BKV = 128;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_THRESHOLD = 8.f;   // log2 units
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int DH>
+struct Cfg {
+  static constexpr int NP = (DH + 63) / 64;        // 64-feature panels per row
+  static constexpr int PANEL = 128 * 128;          // bytes: 128 rows x 128 B
+  static constexpr int Q_BYTES = NP * PANEL;
+  static constexpr int KV_BYTES = 2 * NP * PANEL;  // K and V of one stage
+  static constexpr int P_BYTES = 2 * PANEL;        // 128 queries x 128 keys bf16
+  static constexpr int SMEM = Q_BYTES + 2 * KV_BYTES + P_BYTES + 1024 + 256;
+  static constexpr int S_COL0 = 0, O_COL = 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, float* __restrict__ lse, int T_,
+                       int h) {
+  using C = Cfg<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;
+  uint8_t* sKV = sQ + C::Q_BYTES;  // stage s: K at sKV + s*KV_BYTES, V at + NP*PANEL
+  uint8_t* sP = sKV + 2 * C::KV_BYTES;
+  uint64_t* bars = (uint64_t*)(sP + C::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_done = bars + 8;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (T_ + BQ - 1) / BQ;
+  const int qb = nqb - 1 - blockIdx.x;     // heavy (late) query blocks first
+  const int bh = blockIdx.y;
+  const int b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int q0 = qb * BQ;
+  const int nkb = min(qb + 1, (T_ + BKV - 1) / BKV);
+  const int row0 = b * T_;   // token row of this sequence in qkv
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+      mbar_expect_tx(q_full, C::Q_BYTES);
+      for (int p = 0; p < C::NP; ++p) tma_load(sQ + p * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + q0);
+      for (int j = 0; j < nkb; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        uint8_t* k = sKV + s * C::KV_BYTES;
+        uint8_t* v = k + C::NP * C::PANEL;
+        mbar_expect_tx(&kv_full[s], C::KV_BYTES);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(k + p * C::PANEL, &tm, &kv_full[s], d + hh * DH + 64 * p, row0 + j * BKV);
+          tma_load(v + p * C::PANEL, &tm, &kv_full[s], 2 * d + hh * DH + 64 * p, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t id_s = idesc_bf16(128, BKV, false, false);  // S = Q K^T   (both K-major)
+    constexpr uint32_t id_o = idesc_bf16(128, DH, false, true);    // O += P V    (V MN-major)
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int s = j & 1;
+      mbar_wait(&kv_full[s], (j >> 1) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t q = smem_u32(sQ), k = smem_u32(sKV + s * C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::PANEL + (kk & 3) * 32;
+          mma(tbase + C::S_COL0 + s * BKV, desc_sw128(q + off, 16, 1024), desc_sw128(k + off, 16, 1024), id_s,
+              kk > 0);
+        }
+        commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkb; ++j) {
+      if (j + 1 < nkb) issue_s(j + 1);
+      mbar_wait(p_full, j & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t p = smem_u32(sP), v = smem_u32(sKV + (j & 1) * C::KV_BYTES + C::NP * C::PANEL);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * C::PANEL + (kk & 3) * 32;
+          mma(tbase + C::O_COL, desc_sw128(p + aoff, 16, 1024), desc_sw128(v + kk * 2048, C::PANEL, 1024), id_o,
+              (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        commit(o_done);
+        commit(&kv_empty[j & 1]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int qw = warp & 3;
+    const int r = 32 * qw + lane;  // query row within the block = TMEM lane
+    const int qi = q0 + r;
+    const uint32_t lane_addr = tbase + ((uint32_t)(32 * qw) << 16);
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
+      fence_after();
+      uint32_t raw[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV; c += 32) tmem_ld32(lane_addr + C::S_COL0 + s * BKV + c, raw + c);
+      tmem_wait_ld();
+      const bool diag = j == qb;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BKV; ++c) {
+        const int kj = j * BKV + c;
+        float v = __uint_as_float(raw[c]) * sc;
+        if ((diag && kj > qi) || kj >= T_) v = -INFINITY;
+        raw[c] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      // lazy rescale: move the reference max only when it grows by more than 2^8
+      const bool need = mx > m_ref + RESCALE_THRESHOLD;
+      const float new_ref = need ? mx : m_ref;
+      const float alpha = (m_ref == -INFINITY) ? 0.f : exp2f(m_ref - new_ref);
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable and P buffer free
+      if (__any_sync(0xffffffffu, need) && j > 0) {
+        fence_after();
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {
+          uint32_t ov[16];
+          tmem_ld16(lane_addr + C::O_COL + c, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st16(lane_addr + C::O_COL + c, ov);
+        }
+        tmem_wait_st();
+      }
+      l *= alpha;
+      m_ref = new_ref;
+      // P = exp2(S - m_ref) -> bf16, 128B-swizzled K-major rows (2 panels of 64 keys)
+      float rs = 0.f;
+      uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < BKV / 8; ++c8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float p0 = exp2f(__uint_as_float(raw[c8 * 8 + 2 * i]) - m_ref);
+          const float p1 = exp2f(__uint_as_float(raw[c8 * 8 + 2 * i + 1]) - m_ref);
+          rs += p0 + p1;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+          pk[i] = *(uint32_t*)&v2;
+        }
+        const int panel = c8 >> 3, ch = c8 & 7;
+        *(uint4*)(prow + panel * C::PANEL + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l += rs;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16, LSE (natural log)
+    mbar_wait(o_done, (nkb - 1) & 1);
+    fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = o + ((long)b * T_ + qi) * d + hh * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t ov[16];
+      tmem_ld16(lane_addr + C::O_COL + c, ov);
+      tmem_wait_ld();
+      if (qi < T_) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 v2 =
+              __floats2bfloat162_rn(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+          pk[i] = *(uint32_t*)&v2;
+        }
+        *(uint4*)(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+    if (qi < T_) lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+// ======================================================================================
+// Backward (deterministic, no atomics), P and dS recomputed from the stashed LSE:
+//   dK/dV kernel, one CTA per (b, h, 128-key block), loops over 64-query blocks i >= it:
+//     S^T = K Q_i^T, dP^T = V dO_i^T (TMEM); thread = key row: P^T = exp(S^T/sqrt(dh) - lse_q),
+//     dS^T = P^T (dP^T - D_q) -> bf16 swizzled smem; dV += P^T dO_i, dK += dS^T Q_i (TMEM)
+//   dQ kernel, one CTA per (b, h, 128-query block), loops over 64-key blocks j <= it:
+//     S = Q K_j^T, dP = dO V_j^T; thread = query row: dS = P (dP - D); dQ += dS K_j
+// D = rowsum(dO * O) comes from fa::dsum_kernel.
+// ======================================================================================
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+template <int DH>
+struct BCfg {
+  static constexpr int NP = (DH + 63) / 64;
+  static constexpr int P128 = 128 * 128;   // panel of 128 rows x 128 B
+  static constexpr int P64 = 64 * 128;     // panel of 64 rows x 128 B
+  // dK/dV kernel
+  static constexpr int KV_BYTES = 2 * NP * P128;          // K and V of the key block
+  static constexpr int QD_BYTES = 2 * NP * P64;           // Q_i and dO_i of one stage
+  static constexpr int PD_BYTES = 2 * P64 * 2;            // P^T and dS^T: 128 rows x 64 queries each
+  static constexpr int SMEM_KV = KV_BYTES + 2 * QD_BYTES + PD_BYTES + 2 * 2 * 64 * 4 + 1024 + 256;
+  // dQ kernel
+  static constexpr int QO_BYTES = 2 * NP * P128;          // Q and dO of the query block
+  static constexpr int KVS_BYTES = 2 * NP * P64;          // K_j and V_j of one stage
+  static constexpr int DS_BYTES = 128 * 128;              // dS: 128 rows x 64 keys bf16
+  static constexpr int SMEM_Q = QO_BYTES + 2 * KVS_BYTES + DS_BYTES + 1024 + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                           const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                           const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
+  using C = BCfg<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + C::NP * C::P128;
+  uint8_t* sQD = sm + C::KV_BYTES;                 // stage s: Q at + s*QD_BYTES, dO at + NP*P64
+  uint8_t* sPT = sQD + 2 * C::QD_BYTES;
+  uint8_t* sdST = sPT + 128 * 128;
+  float* sL = (float*)(sdST + 128 * 128);          // [2][64]
+  float* sD = sL + 128;                            // [2][64]
+  uint64_t* bars = (uint64_t*)(sD + 128);
+  uint64_t* kv_full = bars;
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* pd_full = bars + 6;
+  uint64_t* pd_empty = bars + 7;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;       // key block 0 has the most work: scheduled first
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int k0 = kb * 128;
+  const int nq = (T_ + 63) / 64;
+  const int i0 = k0 / 64;          // first query block that sees these keys
+  const int nblk = nq - i0;
+  const int row0 = b * T_;
+  constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + ((DH + 15) / 16) * 16;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qd_full[s], 1);
+      mbar_init(&qd_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(pd_full, 128);
+    mbar_init(pd_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, C::KV_BYTES);
+      for (int p = 0; p < C::NP; ++p) {
+        tma_load(sK + p * C::P128, &tm_kv, kv_full, d + hh * DH + 64 * p, row0 + k0);
+        tma_load(sV + p * C::P128, &tm_kv, kv_full, 2 * d + hh * DH + 64 * p, row0 + k0);
+      }
+      for (int it = 0; it < nblk; ++it) {
+        const int s = it & 1, q0 = (i0 + it) * 64;
+        mbar_wait(&qd_empty[s], ((it >> 1) & 1) ^ 1);
+        uint8_t* q = sQD + s * C::QD_BYTES;
+        uint8_t* g = q + C::NP * C::P64;
+        mbar_expect_tx(&qd_full[s], C::QD_BYTES);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(q + p * C::P64, &tm_q, &qd_full[s], hh * DH + 64 * p, row0 + q0);
+          tma_load(g + p * C::P64, &tm_do, &qd_full[s], hh * DH + 64 * p, row0 + q0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
+    constexpr uint32_t id_g = idesc_bf16(128, DH, false, true);    // dV += P^T dO, dK += dS^T Q
+    mbar_wait(kv_full, 0);
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it & 1;
+      mbar_wait(&qd_full[s], (it >> 1) & 1);
+      fence_after();
+      const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
+      if (lane == 0) {
+        const uint32_t k = smem_u32(sK), v = smem_u32(sV);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
+          mma(tbase + ST_COL, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + DPT_COL, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s, kk > 0);
+        }
+        commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(pd_full, it & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t pt = smem_u32(sPT), dst = smem_u32(sdST);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          mma(tbase + DV_COL, desc_sw128(pt + kk * 32, 16, 1024), desc_sw128(g + kk * 2048, C::P64, 1024), id_g,
+              acc);
+          mma(tbase + DK_COL, desc_sw128(dst + kk * 32, 16, 1024), desc_sw128(q + kk * 2048, C::P64, 1024), id_g,
+              acc);
+        }
+        commit(pd_empty);
+        commit(&qd_empty[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int r = 32 * qw + lane, kj = k0 + r;
+    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    const float* lrow = lse + ((long)b * h + hh) * T_;
+    const float* drow = Dsum + ((long)b * h + hh) * T_;
+    const int t = threadIdx.x - 128;
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it & 1, q0 = (i0 + it) * 64;
+      if (t < 64) {
+        const int qi = q0 + t;
+        sL[s * 64 + t] = qi < T_ ? lrow[qi] * LOG2E : INFINITY;
+      } else {
+        const int qi = q0 + t - 64;
+        sD[s * 64 + t - 64] = qi < T_ ? drow[qi] : 0.f;
+      }
+      named_sync(1, 128);
+      mbar_wait(s_full, it & 1);
+      fence_after();
+      uint32_t sv[64], dv[64];
+      tmem_ld32(la + ST_COL, sv);
+      tmem_ld32(la + ST_COL + 32, sv + 32);
+      tmem_ld32(la + DPT_COL, dv);
+      tmem_ld32(la + DPT_COL + 32, dv + 32);
+      tmem_wait_ld();
+      if (it > 0) mbar_wait(pd_empty, (it - 1) & 1);
+      uint8_t* prow = sPT + (r >> 3) * 1024 + (r & 7) * 128;
+      uint8_t* drw = sdST + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t pk[4], dk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float pp[2], dd[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c = c8 * 8 + 2 * e + u, qi = q0 + c;
+            float p = exp2f(__uint_as_float(sv[c]) * sc - sL[s * 64 + c]);
+            if (qi < kj || kj >= T_) p = 0.f;
+            pp[u] = p;
+            dd[u] = p * (__uint_as_float(dv[c]) - sD[s * 64 + c]);
+          }
+          __nv_bfloat162 a2 = __floats2bfloat162_rn(pp[0], pp[1]), b2 = __floats2bfloat162_rn(dd[0], dd[1]);
+          pk[e] = *(uint32_t*)&a2;
+          dk[e] = *(uint32_t*)&b2;
+        }
+        const int sw = (c8 ^ (r & 7)) << 4;
+        *(uint4*)(prow + sw) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(drw + sw) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      mbar_arrive(pd_full);
+    }
+    mbar_wait(pd_empty, (nblk - 1) & 1);
+    fence_after();
+    const float isq = rsqrtf((float)DH);
+    bf16* row = dqkv + ((long)row0 + kj) * 3 * d + hh * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t gk[16], gv[16];
+      tmem_ld16(la + DK_COL + c, gk);
+      tmem_ld16(la + DV_COL + c, gv);
+      tmem_wait_ld();
+      if (kj < T_) {
+        uint32_t pk[8], pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 k2 = __floats2bfloat162_rn(__uint_as_float(gk[2 * i]) * isq, __uint_as_float(gk[2 * i + 1]) * isq);
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(gv[2 * i]), __uint_as_float(gv[2 * i + 1]));
+          pk[i] = *(uint32_t*)&k2;
+          pv[i] = *(uint32_t*)&v2;
+        }
+        *(uint4*)(row + d + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(row + d + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        *(uint4*)(row + 2 * d + c) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+        *(uint4*)(row + 2 * d + c + 8) = make_uint4(pv[4], pv[5], pv[6], pv[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_kv, const float* __restrict__ lse,
+                          const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
+  using C = BCfg<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;
+  uint8_t* sO = sQ + C::NP * C::P128;
+  uint8_t* sKV = sm + C::QO_BYTES;    // stage s: K at + s*KVS_BYTES, V at + NP*P64
+  uint8_t* sdS = sKV + 2 * C::KVS_BYTES;
+  uint64_t* bars = (uint64_t*)(sdS + C::DS_BYTES);
+  uint64_t* qo_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* ds_empty = bars + 7;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (T_ + 127) / 128;
+  const int qb = nqb - 1 - blockIdx.x;
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int q0 = qb * 128;
+  const int nblk = min((q0 + 127) / 64 + 1, (T_ + 63) / 64);
+  const int row0 = b * T_;
+  constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qo_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 128);
+    mbar_init(ds_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qo_full, C::QO_BYTES);
+      for (int p = 0; p < C::NP; ++p) {
+        tma_load(sQ + p * C::P128, &tm_q, qo_full, hh * DH + 64 * p, row0 + q0);
+        tma_load(sO + p * C::P128, &tm_do, qo_full, hh * DH + 64 * p, row0 + q0);
+      }
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        uint8_t* k = sKV + s * C::KVS_BYTES;
+        uint8_t* v = k + C::NP * C::P64;
+        mbar_expect_tx(&kv_full[s], C::KVS_BYTES);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(k + p * C::P64, &tm_kv, &kv_full[s], d + hh * DH + 64 * p, row0 + j * 64);
+          tma_load(v + p * C::P64, &tm_kv, &kv_full[s], 2 * d + hh * DH + 64 * p, row0 + j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S = Q K^T, dP = dO V^T
+    constexpr uint32_t id_q = idesc_bf16(128, DH, false, true);    // dQ += dS K
+    mbar_wait(qo_full, 0);
+    for (int j = 0; j < nblk; ++j) {
+      const int s = j & 1;
+      mbar_wait(&kv_full[s], (j >> 1) & 1);
+      fence_after();
+      const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES), v = k + C::NP * C::P64;
+      if (lane == 0) {
+        const uint32_t q = smem_u32(sQ), g = smem_u32(sO);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
+          mma(tbase + S_COL, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + DP_COL, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s, kk > 0);
+        }
+        commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(ds_full, j & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t ds = smem_u32(sdS);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma(tbase + DQ_COL, desc_sw128(ds + kk * 32, 16, 1024), desc_sw128(k + kk * 2048, C::P64, 1024), id_q,
+              (j > 0 || kk > 0) ? 1u : 0u);
+        commit(ds_empty);
+        commit(&kv_empty[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int r = 32 * qw + lane, qi = q0 + r;
+    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    const float L = qi < T_ ? lse[((long)b * h + hh) * T_ + qi] * LOG2E : INFINITY;
+    const float Dr = qi < T_ ? Dsum[((long)b * h + hh) * T_ + qi] : 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(s_full, j & 1);
+      fence_after();
+      uint32_t sv[64], dv[64];
+      tmem_ld32(la + S_COL, sv);
+      tmem_ld32(la + S_COL + 32, sv + 32);
+      tmem_ld32(la + DP_COL, dv);
+      tmem_ld32(la + DP_COL + 32, dv + 32);
+      tmem_wait_ld();
+      if (j > 0) mbar_wait(ds_empty, (j - 1) & 1);
+      uint8_t* drw = sdS + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint32_t dk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float dd[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c = c8 * 8 + 2 * e + u, kj = j * 64 + c;
+            float p = exp2f(__uint_as_float(sv[c]) * sc - L);
+            if (kj > qi || kj >= T_) p = 0.f;
+            dd[u] = p * (__uint_as_float(dv[c]) - Dr);
+          }
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(dd[0], dd[1]);
+          dk[e] = *(uint32_t*)&b2;
+        }
+        *(uint4*)(drw + ((c8 ^ (r & 7)) << 4)) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(ds_empty, (nblk - 1) & 1);
+    fence_after();
+    const float isq = rsqrtf((float)DH);
+    bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t gq[16];
+      tmem_ld16(la + DQ_COL + c, gq);
+      tmem_wait_ld();
+      if (qi < T_) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 q2 = __floats2bfloat162_rn(__uint_as_float(gq[2 * i]) * isq, __uint_as_float(gq[2 * i + 1]) * isq);
+          pk[i] = *(uint32_t*)&q2;
+        }
+        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
+  }
+}
+
+__global__ void dsum_tc_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ Dsum,
+                               int B, int T_, int h, int dh) {
+  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  if (gw >= (long)B * h * T_) return;
+  const int lane = threadIdx.x & 31;
+  const int t = (int)(gw % T_);
+  const int hh = (int)((gw / T_) % h);
+  const int b = (int)(gw / ((long)T_ * h));
+  const long off = ((long)b * T_ + t) * h * dh + hh * dh;
+  float s = 0.f;
+  for (int j = lane; j < dh; j += 32) s = fmaf(__bfloat162float(o[off + j]), __bfloat162float(dout[off + j]), s);
+  s = warp_sum(s);
+  if (lane == 0) Dsum[((long)b * h + hh) * T_ + t] = s;
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+template <int DH>
+bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_t st) {
+  using C = Cfg<DH>;
+  PFN_encodeTiled enc = encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  CUtensorMap tm;
+  const long d = (long)h * DH;
+  cuuint64_t dims[2] = {(cuuint64_t)(3 * d), (cuuint64_t)B * T_};
+  cuuint64_t strides[1] = {(cuuint64_t)(3 * d) * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(qkv), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("attention: tensor map encode failed");
+    return false;
+  }
+  static bool once = false;
+  if (!once) {
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    once = true;
+  }
+  dim3 grid((T_ + BQ - 1) / BQ, B * h);
+  attn_fwd_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tm, o, lse, T_, h);
+  count_launch();
+  ATOM_CUDA_OK(cudaGetLastError());
+  return true;
+}
+
+static bool make_map2d(CUtensorMap* m, const bf16* base, long cols, long rows, int box_rows) {
+  PFN_encodeTiled enc = encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("attention: tensor map encode failed");
+    return false;
+  }
+  return true;
+}
+
+template <int DH>
+bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B, int T_,
+         int h, cudaStream_t st) {
+  using C = BCfg<DH>;
+  const long d = (long)h * DH, rows = (long)B * T_;
+  CUtensorMap qkv64, qkv128, do64, do128;
+  if (!make_map2d(&qkv64, qkv, 3 * d, rows, 64) || !make_map2d(&qkv128, qkv, 3 * d, rows, 128) ||
+      !make_map2d(&do64, dout, d, rows, 64) || !make_map2d(&do128, dout, d, rows, 128))
+    return false;
+  static bool once = false;
+  if (!once) {
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::SMEM_KV));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::SMEM_Q));
+    once = true;
+  }
+  const long warps = rows * h;
+  dsum_tc_kernel<<<(warps + 7) / 8, 256, 0, st>>>(o, dout, Dsum, B, T_, h, DH);
+  count_launch();
+  dim3 grid((T_ + 127) / 128, B * h);
+  attn_bwd_dkv_tc_kernel<DH><<<grid, 256, C::SMEM_KV, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
+  count_launch();
+  attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
+  count_launch();
+  ATOM_CUDA_OK(cudaGetLastError());
+  return true;
+}
+
+}  // namespace atc
+
+bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 80 || dh == 128) && ((3 * d) % 8 == 0); }
+
+bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
+                 int T_, int h, int dh, cudaStream_t st) {
+  switch (dh) {
+    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
+    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
+    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
+  }
+  set_error("tcgen05 attention: unsupported head size %d", dh);
+  return false;
+}
+
+bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st) {
+  switch (dh) {
+    case 64: return atc::fwd<64>(qkv, o, lse, B, T_, h, st);
+    case 80: return atc::fwd<80>(qkv, o, lse, B, T_, h, st);
+    case 128: return atc::fwd<128>(qkv, o, lse, B, T_, h, st);
+  }
+  set_error("tcgen05 attention: unsupported head size %d", dh);
+  return false;
+}
+
+}  // namespace atom

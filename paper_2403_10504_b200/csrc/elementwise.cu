@@ -29,47 +29,97 @@ __device__ __forceinline__ float ln_out(float x, float mean, float rstd, float g
   return __fmaf_rn(__fmul_rn(__fsub_rn(x, mean), rstd), g, b);
 }
 
+// 16-byte vectors of T (8 bf16 / 4 fp32); a row of d elements is d / VW chunks, chunk c of a row
+// handled by thread c % 128 (coalesced), at most LN_MAXC chunks per thread kept in registers.
+template <typename T> struct Vec { static constexpr int N = 16 / sizeof(T); };
+constexpr int LN_MAXC = 6;   // 6 x 128 x 8 = 6144 bf16 (3072 fp32) elements per row
+
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* p, float* f) {
+  uint4 u = *(const uint4*)p;
+  const T* e = (const T*)&u;
+#pragma unroll
+  for (int i = 0; i < Vec<T>::N; ++i) f[i] = to_f(e[i]);
+}
+template <typename T>
+__device__ __forceinline__ void store_vec(T* p, const float* f) {
+  uint4 u;
+  T* e = (T*)&u;
+#pragma unroll
+  for (int i = 0; i < Vec<T>::N; ++i) e[i] = from_f<T>(f[i]);
+  *(uint4*)p = u;
+}
+
 // y = LN(x) * g + b; stats[row] = (mean, rstd)                       (minGPT nn.LayerNorm)
 template <typename T>
 __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                             const T* __restrict__ b, T* __restrict__ y,
                                                             float* __restrict__ stats, int d) {
+  constexpr int VW = Vec<T>::N;
   __shared__ float sh[4];
   const long row = blockIdx.x;
+  const int nch = d / VW;
   const T* xr = x + row * d;
-  float v[LN_MAXE];
+  float v[LN_MAXC][VW];
   float s = 0.f;
-  int n = 0;
-  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
-    v[n] = to_f(xr[j]);
-    s += v[n];
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch) {
+      load_vec<T>(xr + ch * VW, v[c]);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) s += v[c][i];
+    }
   }
   const float mean = block_sum128(s, sh) / (float)d;
   float q = 0.f;
-  for (int i = 0; i < n; ++i) {
-    float t = v[i] - mean;
-    q = fmaf(t, t, q);
-  }
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c)
+    if (c * LN_THREADS + threadIdx.x < nch)
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        const float t = v[c][i] - mean;
+        q = fmaf(t, t, q);
+      }
   const float var = block_sum128(q, sh) / (float)d;
   const float rstd = rsqrtf(var + LN_EPS);
   T* yr = y + row * d;
-  n = 0;
-  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) yr[j] = from_f<T>(ln_out(v[n], mean, rstd, to_f(g[j]), to_f(b[j])));
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch) {
+      float gg[VW], bb[VW], o[VW];
+      load_vec<T>(g + ch * VW, gg);
+      load_vec<T>(b + ch * VW, bb);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) o[i] = ln_out(v[c][i], mean, rstd, gg[i], bb[i]);
+      store_vec<T>(yr + ch * VW, o);
+    }
+  }
   if (threadIdx.x == 0) {
     stats[2 * row] = mean;
     stats[2 * row + 1] = rstd;
   }
 }
 
-// y = LN(x) from stored stats (bit-identical to the forward's y)
+// y = LN(x) from stored stats (bit-identical to the forward's y); one 16-byte chunk per thread
 template <typename T>
 __global__ void ln_apply_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
                                 const float* __restrict__ stats, T* __restrict__ y, long rows, int d) {
-  const long n = rows * d;
+  constexpr int VW = Vec<T>::N;
+  const int nch = d / VW;
+  const long n = rows * nch;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const long r = i / d;
-    const int j = (int)(i - r * d);
-    y[i] = from_f<T>(ln_out(to_f(x[i]), stats[2 * r], stats[2 * r + 1], to_f(g[j]), to_f(b[j])));
+    const long r = i / nch;
+    const int ch = (int)(i - r * nch);
+    float xv[VW], gg[VW], bb[VW], o[VW];
+    load_vec<T>(x + i * VW, xv);
+    load_vec<T>(g + ch * VW, gg);
+    load_vec<T>(b + ch * VW, bb);
+    const float mean = stats[2 * r], rstd = stats[2 * r + 1];
+#pragma unroll
+    for (int k = 0; k < VW; ++k) o[k] = ln_out(xv[k], mean, rstd, gg[k], bb[k]);
+    store_vec<T>(y + i * VW, o);
   }
 }
 
@@ -79,25 +129,45 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
                                                             const float* __restrict__ stats,
                                                             const T* __restrict__ g, const T* __restrict__ dres,
                                                             T* __restrict__ dx, int d) {
+  constexpr int VW = Vec<T>::N;
   __shared__ float sh[4];
   const long row = blockIdx.x;
+  const int nch = d / VW;
   const float mean = stats[2 * row], rstd = stats[2 * row + 1];
-  float xh[LN_MAXE], dg[LN_MAXE];
+  float xh[LN_MAXC][VW], dg[LN_MAXC][VW];
   float s1 = 0.f, s2 = 0.f;
-  int n = 0;
-  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
-    xh[n] = (to_f(x[row * d + j]) - mean) * rstd;
-    dg[n] = to_f(dy[row * d + j]) * to_f(g[j]);
-    s1 += dg[n];
-    s2 = fmaf(dg[n], xh[n], s2);
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch) {
+      float gg[VW];
+      load_vec<T>(x + row * d + ch * VW, xh[c]);
+      load_vec<T>(dy + row * d + ch * VW, dg[c]);
+      load_vec<T>(g + ch * VW, gg);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        xh[c][i] = (xh[c][i] - mean) * rstd;
+        dg[c][i] *= gg[i];
+        s1 += dg[c][i];
+        s2 = fmaf(dg[c][i], xh[c][i], s2);
+      }
+    }
   }
   const float m1 = block_sum128(s1, sh) / (float)d;
   const float m2 = block_sum128(s2, sh) / (float)d;
-  n = 0;
-  for (int j = threadIdx.x; j < d; j += LN_THREADS, ++n) {
-    float v = rstd * (dg[n] - m1 - xh[n] * m2);
-    if (dres) v += to_f(dres[row * d + j]);
-    dx[row * d + j] = from_f<T>(v);
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch) {
+      float o[VW], r[VW];
+      if (dres) load_vec<T>(dres + row * d + ch * VW, r);
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        o[i] = rstd * (dg[c][i] - m1 - xh[c][i] * m2);
+        if (dres) o[i] += r[i];
+      }
+      store_vec<T>(dx + row * d + ch * VW, o);
+    }
   }
 }
 
@@ -375,14 +445,17 @@ static inline int grid_for(long n, int threads = 256) {
 
 template <typename T>
 bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st) {
-  if (d > LN_THREADS * LN_MAXE) { set_error("LayerNorm: d too large"); return false; }
+  if (d % Vec<T>::N || d > LN_THREADS * LN_MAXC * Vec<T>::N) {
+    set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
+    return false;
+  }
   ln_fwd_kernel<T><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d);
   LAUNCH_OK();
   return true;
 }
 template <typename T>
 bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st) {
-  ln_apply_kernel<T><<<grid_for(rows * d), 256, 0, st>>>(x, g, b, stats, y, rows, d);
+  ln_apply_kernel<T><<<grid_for(rows * d / Vec<T>::N), 256, 0, st>>>(x, g, b, stats, y, rows, d);
   LAUNCH_OK();
   return true;
 }

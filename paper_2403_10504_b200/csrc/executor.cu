@@ -164,16 +164,20 @@ template <typename T>
 bool attn_fwd(atom_peer* p, const T* qkv, T* o, float* lse) {
   const ModelDims& dm = p->dm;
   const int dh = dm.d / dm.h;
-  if constexpr (std::is_same<T, bf16>::value)
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (attn_tc_supported(dh, dm.d)) return attn_fwd_tc(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
     if (attn_fa_supported(dh)) return attn_fwd_fa(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
+  }
   return attn_fwd_simt<T>(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
 }
 template <typename T>
 bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv) {
   const ModelDims& dm = p->dm;
   const int dh = dm.d / dm.h;
-  if constexpr (std::is_same<T, bf16>::value)
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (attn_tc_supported(dh, dm.d)) return attn_bwd_tc(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
     if (attn_fa_supported(dh)) return attn_bwd_fa(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
+  }
   return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
 }
 

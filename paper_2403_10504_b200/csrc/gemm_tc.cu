@@ -109,6 +109,20 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool 
 constexpr int BM = 128;
 constexpr int BK = 64;
 
+// Grouped raster: consecutive tiles walk GROUP_M m-blocks down before moving right, so the
+// ~148 tiles in flight cover a GROUP_M x (148 / GROUP_M) block of the output and re-read A and
+// B from L2 instead of DRAM.
+constexpr int GROUP_M = 16;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int* mb, int* nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = tile / per_group;
+  const int first = g * GROUP_M;
+  const int gsz = min(num_m - first, GROUP_M);
+  const int r = tile - g * per_group;
+  *mb = first + r % gsz;
+  *nb = r / gsz;
+}
+
 template <int BN>
 struct TcCfg {
   static constexpr int STAGES = BN == 256 ? 4 : 6;
@@ -170,8 +184,10 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % num_m) * BM;
-        const int n0 = (tile / num_m) * BN;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, &mb, &nb);
+        const int m0 = mb * BM;
+        const int n0 = nb * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -238,8 +254,10 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * BM;
-      const int n0 = (tile / num_m) * BN;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, &mb, &nb);
+      const int m0 = mb * BM;
+      const int n0 = nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const long m = m0 + 32 * q + lane;
@@ -286,8 +304,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// remote arrive on a peer CTA's mbarrier.  Default (CTA-scope) release: an explicit
+// .release.cluster compiles to MEMBAR.ALL.GPU, which made every arrive wait for the thread's
+// outstanding global stores (profiles/r01: 2-CTA GEMM at 34% tensor-pipe activity).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
                                                  int c1) {
@@ -356,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 256);  // both CTAs' epilogue threads (used in the leader)
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp of both CTAs (used in the leader)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -380,8 +401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const int m0 = (tile % num_m) * 2 * BM + rank * BM;
-        const int n0 = (tile / num_m) * BN + rank * Cfg::HB;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, &mb, &nb);
+        const int m0 = mb * 2 * BM + rank * BM;
+        const int n0 = nb * BN + rank * Cfg::HB;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -456,8 +479,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * 2 * BM + rank * BM;
-      const int n0 = (tile / num_m) * BN;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, &mb, &nb);
+      const int m0 = mb * 2 * BM + rank * BM;
+      const int n0 = nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const long m = m0 + 32 * q + lane;
@@ -476,7 +501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
     }
   }
   tc_fence_before();
@@ -576,13 +602,14 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
 // Kernel choice by estimated time: waves x per-SM tile work / relative speed
 // (2-CTA 256x256 > 1-CTA 128x256 > 1-CTA 128x128 in per-SM efficiency).  Returns 512 for the
 // 2-CTA kernel, else the 1-CTA tile width.
-static bool g_allow_2cta = false;  // enabled once the 2-CTA kernel is validated on the GPU
+static bool g_allow_2cta = true;
 static int pick_bn(int M, int N) {
   const int sms = num_sms();
   struct V { int code; long tiles; int slots; double work, speed; };
+  // relative per-SM speeds measured on B200 (tools/gemm_perf.py): 128-wide tiles ~0.6x of 256-wide
   V vs[3] = {{512, (long)((M + 255) / 256) * ((N + 255) / 256), sms / 2, 128.0 * 256, 1.0},
-             {256, (long)((M + 127) / 128) * ((N + 255) / 256), sms, 128.0 * 256, 0.85},
-             {128, (long)((M + 127) / 128) * ((N + 127) / 128), sms, 128.0 * 128, 0.78}};
+             {256, (long)((M + 127) / 128) * ((N + 255) / 256), sms, 128.0 * 256, 0.9},
+             {128, (long)((M + 127) / 128) * ((N + 127) / 128), sms, 128.0 * 128, 0.6}};
   double best = 1e300;
   int code = 256;
   for (auto& v : vs) {

@@ -43,5 +43,10 @@ bool attn_fwd_fa(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int
 bool attn_bwd_fa(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
                  int T_, int h, int dh, cudaStream_t st);
 bool attn_fa_supported(int dh);
+// tcgen05 / TMEM forward (attn_tc.cu)
+bool attn_tc_supported(int dh, int d);
+bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
+bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
+                 int T_, int h, int dh, cudaStream_t st);
 
 }  // namespace atom

@@ -1,0 +1,87 @@
+"""Attention kernels (tcgen05 forward, mma.sync flash attention, SIMT) vs a plain PyTorch fp32 reference."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2403_10504_b200 import atom  # noqa: E402
+
+
+def ref_attention(qkv, B, T, h, dh):
+    x = qkv.float().view(B, T, 3, h, dh)
+    q, k, v = (x[:, :, i].transpose(1, 2) for i in range(3))        # [B, h, T, dh]
+    s = q @ k.transpose(-1, -2) / math.sqrt(dh)
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool, device=qkv.device), 1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ v
+    return o.transpose(1, 2).reshape(B * T, h * dh), lse
+
+
+CASES = [(2, 128, 2, 64), (1, 300, 3, 64), (2, 256, 2, 128), (1, 384, 2, 128), (1, 200, 2, 80), (2, 256, 4, 80),
+         (1, 2048, 2, 128)]
+
+
+@pytest.mark.parametrize("impl", [atom.ATTN_TC, atom.ATTN_MMA], ids=["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("case", CASES, ids=[f"B{b}T{t}h{h}d{d}" for b, t, h, d in CASES])
+def test_attention_forward(impl, case):
+    B, T, h, dh = case
+    g = torch.Generator(device="cuda").manual_seed(1)
+    qkv = (torch.randn(B * T, 3 * h * dh, generator=g, device="cuda") * 1.5).bfloat16()
+    o = torch.zeros(B * T, h * dh, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(B, h, T, device="cuda")
+    atom.k_attn_fwd(impl, atom.BF16, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, h, dh)
+    torch.cuda.synchronize()
+    ro, rl = ref_attention(qkv, B, T, h, dh)
+    assert (o.float() - ro).abs().max().item() < 2e-2 * max(1.0, ro.abs().max().item())
+    assert (lse - rl).abs().max().item() < 2e-2
+
+
+BWD_CASES = [(2, 256, 2, 64), (1, 200, 2, 80), (1, 384, 2, 128), (1, 300, 3, 64), (1, 2048, 1, 128),
+             (2, 130, 2, 80)]
+
+
+@pytest.mark.parametrize("impl", [atom.ATTN_TC, atom.ATTN_MMA], ids=["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("case", BWD_CASES, ids=[f"B{b}T{t}h{h}d{d}" for b, t, h, d in BWD_CASES])
+def test_attention_backward(impl, case):
+    B, T, h, dh = case
+    g = torch.Generator(device="cuda").manual_seed(2)
+    qkv = (torch.randn(B * T, 3 * h * dh, generator=g, device="cuda")).bfloat16()
+    dout = torch.randn(B * T, h * dh, generator=g, device="cuda").bfloat16()
+    o = torch.zeros(B * T, h * dh, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(B, h, T, device="cuda")
+    dsum = torch.zeros(B, h, T, device="cuda")
+    dqkv = torch.zeros(B * T, 3 * h * dh, device="cuda", dtype=torch.bfloat16)
+    atom.k_attn_fwd(atom.ATTN_TC if dh != 16 else atom.ATTN_MMA, atom.BF16, qkv.data_ptr(), o.data_ptr(),
+                    lse.data_ptr(), B, T, h, dh)
+    atom.k_attn_bwd(impl, atom.BF16, qkv.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                    dsum.data_ptr(), dqkv.data_ptr(), B, T, h, dh)
+    torch.cuda.synchronize()
+    x = qkv.float().requires_grad_(True)
+    ro, _ = ref_attention(x, B, T, h, dh)
+    ro.backward(dout.float())
+    ref = x.grad
+    err = (dqkv.float() - ref).abs().max().item()
+    assert err < 3e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_attention_tc_deterministic():
+    B, T, h, dh = 1, 512, 2, 128
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn(B * T, 3 * h * dh, generator=g, device="cuda").bfloat16()
+    dout = torch.randn(B * T, h * dh, generator=g, device="cuda").bfloat16()
+    outs = []
+    for _ in range(2):
+        o = torch.zeros(B * T, h * dh, device="cuda", dtype=torch.bfloat16)
+        lse = torch.zeros(B, h, T, device="cuda")
+        dsum = torch.zeros(B, h, T, device="cuda")
+        dq = torch.zeros(B * T, 3 * h * dh, device="cuda", dtype=torch.bfloat16)
+        atom.k_attn_fwd(atom.ATTN_TC, atom.BF16, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, h, dh)
+        atom.k_attn_bwd(atom.ATTN_TC, atom.BF16, qkv.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                        dsum.data_ptr(), dq.data_ptr(), B, T, h, dh)
+        outs.append((o, lse, dq))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

@@ -18,7 +18,7 @@ shapes = [("qkv", 16384, 7680, 2560, 0, 0), ("proj", 16384, 2560, 2560, 0, 0), (
           ("lm_wgrad", 50257, 2560, 16384, 1, 1), ("xl_qkv", 16384, 6144, 2048, 0, 0), ("xl_proj", 16384, 2048, 2048, 0, 0),
           ("sq8192", 8192, 8192, 8192, 0, 0)]
 for name, M, N, K, amn, bmn in shapes:
-    lda = (M + 7) // 8 * 8 if amn else K
+    lda = (M + 7) // 8 * 8 if amn else (K + 7) // 8 * 8
     ldb = (N + 7) // 8 * 8 if bmn else (K + 7) // 8 * 8
     A = torch.randn((K, lda) if amn else (M, lda), device="cuda").bfloat16()
     B = torch.randn((K, ldb) if bmn else (N, ldb), device="cuda").bfloat16()
