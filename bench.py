@@ -47,7 +47,8 @@ def peaks():
 WORKLOADS = {
     # name: (config, model-state cap bytes, description)
     "xl": ("xl", 10 * 2 ** 30, "GPT-3 XL 1.3B (24L, d=2048, 16x128 heads, T=2048, b=8), model state capped at 10 GiB"),
-    "2.7b": ("2.7b", 16 * 2 ** 30, "GPT-3 2.7B (32L, d=2560), model state capped at 16 GiB"),
+    "2.7b": ("2.7b", 20 * 2 ** 30, "GPT-3 2.7B (32L, d=2560, 32x80 heads, T=2048, b=8), model state capped at "
+             "20 GiB (resident would need 50 GB), block re-forward in the backward (full stash does not fit)"),
     "small": ("small", 0, "GPT-3 Small 125M (12L, d=768), per-layer sub-models"),
     "tiny": ("tiny", 3 * 10 ** 6, "tiny GPT (4L, d=64, T=32, V=256)"),
 }
@@ -164,7 +165,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="xl", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="2.7b", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="atom", choices=["atom", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--link-gbs", type=float, default=BIDIR_GBS)

@@ -102,6 +102,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// single MUFU.EX2 (exp2f adds denormal range fix-ups around it); ex2(-inf) = 0
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int DH>
@@ -237,20 +243,30 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int c = 0; c < BKV; c += 32) tmem_ld32(lane_addr + C::S_COL0 + s * BKV + c, raw + c);
       tmem_wait_ld();
-      const bool diag = j == qb;
+      // masking only on the diagonal block and the ragged last block
+      const bool masked = j == qb || (j + 1) * BKV > T_;
       float mx = -INFINITY;
+      if (masked) {
 #pragma unroll
-      for (int c = 0; c < BKV; ++c) {
-        const int kj = j * BKV + c;
-        float v = __uint_as_float(raw[c]) * sc;
-        if ((diag && kj > qi) || kj >= T_) v = -INFINITY;
-        raw[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        for (int c = 0; c < BKV; ++c) {
+          const int kj = j * BKV + c;
+          float v = __uint_as_float(raw[c]) * sc;
+          if (kj > qi || kj >= T_) v = -INFINITY;
+          raw[c] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          const float v = __uint_as_float(raw[c]) * sc;
+          raw[c] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
       }
       // lazy rescale: move the reference max only when it grows by more than 2^8
       const bool need = mx > m_ref + RESCALE_THRESHOLD;
       const float new_ref = need ? mx : m_ref;
-      const float alpha = (m_ref == -INFINITY) ? 0.f : exp2f(m_ref - new_ref);
+      const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable and P buffer free
       if (__any_sync(0xffffffffu, need) && j > 0) {
         fence_after();
@@ -275,8 +291,8 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t pk[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float p0 = exp2f(__uint_as_float(raw[c8 * 8 + 2 * i]) - m_ref);
-          const float p1 = exp2f(__uint_as_float(raw[c8 * 8 + 2 * i + 1]) - m_ref);
+          const float p0 = fast_exp2(__uint_as_float(raw[c8 * 8 + 2 * i]) - m_ref);
+          const float p1 = fast_exp2(__uint_as_float(raw[c8 * 8 + 2 * i + 1]) - m_ref);
           rs += p0 + p1;
           __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
           pk[i] = *(uint32_t*)&v2;
@@ -499,7 +515,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int c = c8 * 8 + 2 * e + u, qi = q0 + c;
-            float p = exp2f(__uint_as_float(sv[c]) * sc - sL[s * 64 + c]);
+            float p = fast_exp2(__uint_as_float(sv[c]) * sc - sL[s * 64 + c]);
             if (qi < kj || kj >= T_) p = 0.f;
             pp[u] = p;
             dd[u] = p * (__uint_as_float(dv[c]) - sD[s * 64 + c]);
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int c = c8 * 8 + 2 * e + u, kj = j * 64 + c;
-            float p = exp2f(__uint_as_float(sv[c]) * sc - L);
+            float p = fast_exp2(__uint_as_float(sv[c]) * sc - L);
             if (kj > qi || kj >= T_) p = 0.f;
             dd[u] = p * (__uint_as_float(dv[c]) - Dr);
           }

@@ -174,27 +174,41 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
 // Column partial sums over chunks of RED_ROWS rows (fixed order):
 //   mode 0: part0[c][j] = sum_r a[r][j]                  (bias gradient: sum of dY over tokens)
 //   mode 1: part0[c][j] = sum_r a[r][j] * xhat[r][j], part1[c][j] = sum_r a[r][j]   (LN gain / shift)
+// Each thread owns one 16-byte vector of columns (8 bf16 / 4 fp32); ncols % VW == 0.
 template <typename T>
 __global__ void col_partials_kernel(int mode, const T* __restrict__ a, long lda, const T* __restrict__ x,
                                     const float* __restrict__ stats, long rows, int ncols, float* __restrict__ part0,
                                     float* __restrict__ part1) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int VW = Vec<T>::N;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * VW;
   const int c = blockIdx.y;
   if (j >= ncols) return;
   const long r0 = (long)c * RED_ROWS, r1 = min(rows, r0 + RED_ROWS);
-  float s0 = 0.f, s1 = 0.f;
+  float s0[VW], s1[VW];
+#pragma unroll
+  for (int i = 0; i < VW; ++i) s0[i] = s1[i] = 0.f;
   for (long r = r0; r < r1; ++r) {
-    const float v = to_f(a[r * lda + j]);
+    float v[VW];
+    load_vec<T>(a + r * lda + j, v);
     if (mode == 1) {
-      const float xh = (to_f(x[r * ncols + j]) - stats[2 * r]) * stats[2 * r + 1];
-      s0 = fmaf(v, xh, s0);
-      s1 += v;
+      float xv[VW];
+      load_vec<T>(x + r * ncols + j, xv);
+      const float mean = stats[2 * r], rstd = stats[2 * r + 1];
+#pragma unroll
+      for (int i = 0; i < VW; ++i) {
+        s0[i] = fmaf(v[i], (xv[i] - mean) * rstd, s0[i]);
+        s1[i] += v[i];
+      }
     } else {
-      s0 += v;
+#pragma unroll
+      for (int i = 0; i < VW; ++i) s0[i] += v[i];
     }
   }
-  part0[(long)c * ncols + j] = s0;
-  if (mode == 1) part1[(long)c * ncols + j] = s1;
+#pragma unroll
+  for (int i = 0; i < VW; ++i) {
+    part0[(long)c * ncols + j + i] = s0[i];
+    if (mode == 1) part1[(long)c * ncols + j + i] = s1[i];
+  }
 }
 
 // out[j] += sum_c part[c][j], chunks in order
@@ -345,10 +359,17 @@ __global__ void embed_bwd_tok_kernel(const T* __restrict__ dh, const int* __rest
   }
 }
 
+// n % VW == 0 (rows of 4d elements); 16-byte vectors
 template <typename T>
 __global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ g, long n) {
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
-    g[i] = from_f<T>(gelu_f(to_f(u[i])));
+  constexpr int VW = Vec<T>::N;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n / VW; i += (long)gridDim.x * blockDim.x) {
+    float v[VW];
+    load_vec<T>(u + i * VW, v);
+#pragma unroll
+    for (int k = 0; k < VW; ++k) v[k] = gelu_f(v[k]);
+    store_vec<T>(g + i * VW, v);
+  }
 }
 
 // Fused AdamW on a swapped-in segment (torch AdamW semantics, R19):
@@ -467,7 +488,8 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   float* p0 = part;
   float* p1 = part + (long)nch * d;
-  col_partials_kernel<T><<<dim3((d + 127) / 128, nch), 128, 0, st>>>(1, dy, d, x, stats, rows, d, p0, p1);
+  constexpr int VW = Vec<T>::N;
+  col_partials_kernel<T><<<dim3((d / VW + 127) / 128, nch), 128, 0, st>>>(1, dy, d, x, stats, rows, d, p0, p1);
   LAUNCH_OK();
   reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p0, nch, d, dg);
   LAUNCH_OK();
@@ -478,8 +500,13 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
 template <typename T>
 bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, cudaStream_t st) {
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
-  col_partials_kernel<T><<<dim3((n + 127) / 128, nch), 128, 0, st>>>(0, dy, ld, nullptr, nullptr, rows, n, part,
-                                                                      nullptr);
+  constexpr int VW = Vec<T>::N;
+  if (n % VW || ld % VW) {
+    set_error("bias_grad: columns and pitch must be multiples of %d", VW);
+    return false;
+  }
+  col_partials_kernel<T><<<dim3((n / VW + 127) / 128, nch), 128, 0, st>>>(0, dy, ld, nullptr, nullptr, rows, n,
+                                                                           part, nullptr);
   LAUNCH_OK();
   reduce_partials_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, nch, n, db);
   LAUNCH_OK();
@@ -525,7 +552,11 @@ bool embed_bwd(const int32_t* tok, long tstride, int T_, int B, const T* dh, int
 }
 template <typename T>
 bool gelu_apply(const T* u, T* g, long n, cudaStream_t st) {
-  gelu_kernel<T><<<grid_for(n), 256, 0, st>>>(u, g, n);
+  if (n % Vec<T>::N) {
+    set_error("gelu: length must be a multiple of %d", Vec<T>::N);
+    return false;
+  }
+  gelu_kernel<T><<<grid_for(n / Vec<T>::N), 256, 0, st>>>(u, g, n);
   LAUNCH_OK();
   return true;
 }
