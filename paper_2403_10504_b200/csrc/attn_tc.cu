@@ -356,13 +356,15 @@ struct BCfg {
   // dK/dV kernel
   static constexpr int KV_BYTES = 2 * NP * P128;          // K and V of the key block
   static constexpr int QD_BYTES = 2 * NP * P64;           // Q_i and dO_i of one stage
-  static constexpr int PD_BYTES = 2 * P64 * 2;            // P^T and dS^T: 128 rows x 64 queries each
-  static constexpr int SMEM_KV = KV_BYTES + 2 * QD_BYTES + PD_BYTES + 2 * 2 * 64 * 4 + 1024 + 256;
+  static constexpr int PD_BYTES = 2 * 128 * 128;          // P^T and dS^T: 128 rows x 64 queries each
+  // two P^T/dS^T buffers and two S^T/dP^T TMEM buffers: the MMAs of block i+1 overlap the
+  // thread math of block i
+  static constexpr int SMEM_KV = KV_BYTES + 2 * QD_BYTES + 2 * PD_BYTES + 2 * 2 * 64 * 4 + 1024 + 256;
   // dQ kernel
   static constexpr int QO_BYTES = 2 * NP * P128;          // Q and dO of the query block
   static constexpr int KVS_BYTES = 2 * NP * P64;          // K_j and V_j of one stage
-  static constexpr int DS_BYTES = 128 * 128;              // dS: 128 rows x 64 keys bf16
-  static constexpr int SMEM_Q = QO_BYTES + 2 * KVS_BYTES + DS_BYTES + 1024 + 256;
+  static constexpr int DS_BYTES = 128 * 128;              // dS: 128 rows x 64 keys bf16 (x2 buffers)
+  static constexpr int SMEM_Q = QO_BYTES + 2 * KVS_BYTES + 2 * DS_BYTES + 1024 + 256;
 };
 
 template <int DH>
@@ -376,18 +378,17 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
   uint8_t* sQD = sm + C::KV_BYTES;                 // stage s: Q at + s*QD_BYTES, dO at + NP*P64
-  uint8_t* sPT = sQD + 2 * C::QD_BYTES;
-  uint8_t* sdST = sPT + 128 * 128;
-  float* sL = (float*)(sdST + 128 * 128);          // [2][64]
+  uint8_t* sPD = sQD + 2 * C::QD_BYTES;            // buffer u: P^T at + u*PD_BYTES, dS^T at + 128*128
+  float* sL = (float*)(sPD + 2 * C::PD_BYTES);     // [2][64]
   float* sD = sL + 128;                            // [2][64]
   uint64_t* bars = (uint64_t*)(sD + 128);
   uint64_t* kv_full = bars;
   uint64_t* qd_full = bars + 1;   // [2]
   uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* pd_full = bars + 6;
-  uint64_t* pd_empty = bars + 7;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 8);
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* pd_full = bars + 7;   // [2]
+  uint64_t* pd_empty = bars + 9;  // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;       // key block 0 has the most work: scheduled first
@@ -398,17 +399,18 @@ __global__ void __launch_bounds__(256, 1)
   const int i0 = k0 / 64;          // first query block that sees these keys
   const int nblk = nq - i0;
   const int row0 = b * T_;
-  constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + ((DH + 15) / 16) * 16;
+  // TMEM: buffer u holds S^T at 128u and dP^T at 128u + 64; dV, dK accumulators after them
+  constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 256, DK_COL = 256 + ((DH + 15) / 16) * 16;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&pd_full[s], 128);
+      mbar_init(&pd_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(pd_full, 128);
-    mbar_init(pd_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -444,26 +446,34 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
     constexpr uint32_t id_g = idesc_bf16(128, DH, false, true);    // dV += P^T dO, dK += dS^T Q
     mbar_wait(kv_full, 0);
-    for (int it = 0; it < nblk; ++it) {
+    // S^T / dP^T of block it into TMEM buffer it&1 (free: its previous user, block it-2, was
+    // consumed by the threads before they arrived on pd_full[it&1], which precedes dV/dK(it-2))
+    auto issue_s = [&](int it) {
       const int s = it & 1;
       mbar_wait(&qd_full[s], (it >> 1) & 1);
       fence_after();
-      const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
       if (lane == 0) {
+        const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
         const uint32_t k = smem_u32(sK), v = smem_u32(sV);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + ST_COL, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + DPT_COL, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + ST_COL + 128 * s, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + DPT_COL + 128 * s, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s, kk > 0);
         }
-        commit(s_full);
+        commit(&s_full[s]);
       }
       __syncwarp();
-      mbar_wait(pd_full, it & 1);
+    };
+    issue_s(0);
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it & 1;
+      if (it + 1 < nblk) issue_s(it + 1);
+      mbar_wait(&pd_full[s], (it >> 1) & 1);
       fence_after();
       if (lane == 0) {
-        const uint32_t pt = smem_u32(sPT), dst = smem_u32(sdST);
+        const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
+        const uint32_t pt = smem_u32(sPD + s * C::PD_BYTES), dst = pt + 128 * 128;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
           const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
@@ -472,7 +482,7 @@ __global__ void __launch_bounds__(256, 1)
           mma(tbase + DK_COL, desc_sw128(dst + kk * 32, 16, 1024), desc_sw128(q + kk * 2048, C::P64, 1024), id_g,
               acc);
         }
-        commit(pd_empty);
+        commit(&pd_empty[s]);
         commit(&qd_empty[s]);
       }
       __syncwarp();
@@ -495,17 +505,17 @@ __global__ void __launch_bounds__(256, 1)
         sD[s * 64 + t - 64] = qi < T_ ? drow[qi] : 0.f;
       }
       named_sync(1, 128);
-      mbar_wait(s_full, it & 1);
+      mbar_wait(&s_full[s], (it >> 1) & 1);
       fence_after();
       uint32_t sv[64], dv[64];
-      tmem_ld32(la + ST_COL, sv);
-      tmem_ld32(la + ST_COL + 32, sv + 32);
-      tmem_ld32(la + DPT_COL, dv);
-      tmem_ld32(la + DPT_COL + 32, dv + 32);
+      tmem_ld32(la + ST_COL + 128 * s, sv);
+      tmem_ld32(la + ST_COL + 128 * s + 32, sv + 32);
+      tmem_ld32(la + DPT_COL + 128 * s, dv);
+      tmem_ld32(la + DPT_COL + 128 * s + 32, dv + 32);
       tmem_wait_ld();
-      if (it > 0) mbar_wait(pd_empty, (it - 1) & 1);
-      uint8_t* prow = sPT + (r >> 3) * 1024 + (r & 7) * 128;
-      uint8_t* drw = sdST + (r >> 3) * 1024 + (r & 7) * 128;
+      if (it >= 2) mbar_wait(&pd_empty[s], ((it >> 1) & 1) ^ 1);   // dV/dK of block it-2 read this buffer
+      uint8_t* prow = sPD + s * C::PD_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
+      uint8_t* drw = prow + 128 * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t pk[4], dk[4];
@@ -530,9 +540,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       fence_before();
-      mbar_arrive(pd_full);
+      mbar_arrive(&pd_full[s]);
     }
-    mbar_wait(pd_empty, (nblk - 1) & 1);
+    mbar_wait(&pd_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);   // last dV/dK MMAs (commit tracks all)
     fence_after();
     const float isq = rsqrtf((float)DH);
     bf16* row = dqkv + ((long)row0 + kj) * 3 * d + hh * DH;
@@ -577,15 +587,15 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sQ = sm;
   uint8_t* sO = sQ + C::NP * C::P128;
   uint8_t* sKV = sm + C::QO_BYTES;    // stage s: K at + s*KVS_BYTES, V at + NP*P64
-  uint8_t* sdS = sKV + 2 * C::KVS_BYTES;
-  uint64_t* bars = (uint64_t*)(sdS + C::DS_BYTES);
+  uint8_t* sdS = sKV + 2 * C::KVS_BYTES;   // buffer u at + u*DS_BYTES
+  uint64_t* bars = (uint64_t*)(sdS + 2 * C::DS_BYTES);
   uint64_t* qo_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* ds_empty = bars + 7;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 8);
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* ds_full = bars + 7;   // [2]
+  uint64_t* ds_empty = bars + 9;  // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (T_ + 127) / 128;
@@ -595,22 +605,23 @@ __global__ void __launch_bounds__(256, 1)
   const int q0 = qb * 128;
   const int nblk = min((q0 + 127) / 64 + 1, (T_ + 63) / 64);
   const int row0 = b * T_;
-  constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128;
+  // TMEM: buffer u holds S at 128u and dP at 128u + 64; the dQ accumulator at 256
+  constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 256;
 
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&ds_full[s], 128);
+      mbar_init(&ds_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(ds_full, 128);
-    mbar_init(ds_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
@@ -641,31 +652,37 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S = Q K^T, dP = dO V^T
     constexpr uint32_t id_q = idesc_bf16(128, DH, false, true);    // dQ += dS K
     mbar_wait(qo_full, 0);
-    for (int j = 0; j < nblk; ++j) {
+    auto issue_s = [&](int j) {
       const int s = j & 1;
       mbar_wait(&kv_full[s], (j >> 1) & 1);
       fence_after();
-      const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES), v = k + C::NP * C::P64;
       if (lane == 0) {
+        const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES), v = k + C::NP * C::P64;
         const uint32_t q = smem_u32(sQ), g = smem_u32(sO);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + S_COL, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + DP_COL, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + S_COL + 128 * s, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + DP_COL + 128 * s, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s, kk > 0);
         }
-        commit(s_full);
+        commit(&s_full[s]);
       }
       __syncwarp();
-      mbar_wait(ds_full, j & 1);
+    };
+    issue_s(0);
+    for (int j = 0; j < nblk; ++j) {
+      const int s = j & 1;
+      if (j + 1 < nblk) issue_s(j + 1);
+      mbar_wait(&ds_full[s], (j >> 1) & 1);
       fence_after();
       if (lane == 0) {
-        const uint32_t ds = smem_u32(sdS);
+        const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES);
+        const uint32_t ds = smem_u32(sdS + s * C::DS_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma(tbase + DQ_COL, desc_sw128(ds + kk * 32, 16, 1024), desc_sw128(k + kk * 2048, C::P64, 1024), id_q,
               (j > 0 || kk > 0) ? 1u : 0u);
-        commit(ds_empty);
+        commit(&ds_empty[s]);
         commit(&kv_empty[s]);
       }
       __syncwarp();
@@ -678,16 +695,17 @@ __global__ void __launch_bounds__(256, 1)
     const float L = qi < T_ ? lse[((long)b * h + hh) * T_ + qi] * LOG2E : INFINITY;
     const float Dr = qi < T_ ? Dsum[((long)b * h + hh) * T_ + qi] : 0.f;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(s_full, j & 1);
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
       fence_after();
       uint32_t sv[64], dv[64];
-      tmem_ld32(la + S_COL, sv);
-      tmem_ld32(la + S_COL + 32, sv + 32);
-      tmem_ld32(la + DP_COL, dv);
-      tmem_ld32(la + DP_COL + 32, dv + 32);
+      tmem_ld32(la + S_COL + 128 * s, sv);
+      tmem_ld32(la + S_COL + 128 * s + 32, sv + 32);
+      tmem_ld32(la + DP_COL + 128 * s, dv);
+      tmem_ld32(la + DP_COL + 128 * s + 32, dv + 32);
       tmem_wait_ld();
-      if (j > 0) mbar_wait(ds_empty, (j - 1) & 1);
-      uint8_t* drw = sdS + (r >> 3) * 1024 + (r & 7) * 128;
+      if (j >= 2) mbar_wait(&ds_empty[s], ((j >> 1) & 1) ^ 1);   // dQ MMA of block j-2 read this buffer
+      uint8_t* drw = sdS + s * C::DS_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
       for (int c8 = 0; c8 < 8; ++c8) {
         uint32_t dk[4];
@@ -708,9 +726,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       fence_before();
-      mbar_arrive(ds_full);
+      mbar_arrive(&ds_full[s]);
     }
-    mbar_wait(ds_empty, (nblk - 1) & 1);
+    mbar_wait(&ds_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     fence_after();
     const float isq = rsqrtf((float)DH);
     bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
@@ -735,7 +753,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
   }
 }
 
