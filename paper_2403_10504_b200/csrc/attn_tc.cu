@@ -12,6 +12,7 @@
 // the MMA as an MN-major B operand (features contiguous), so no transpose is materialised.
 // Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -109,6 +110,36 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+// D[tmem] (+)= A[tmem] * B[smem]: A is M x 16 bf16 at lanes 0..M-1, 8 columns (two bf16 per
+// 32-bit column, even k in the low half) -- the "TS" form of tcgen05.mma.
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+// 2^x on the FMA pipe (x <= 0 finite): round-to-nearest split x = n + f, f in [-1/2, 1/2],
+// minimax cubic for 2^f (max relative error 7.5e-5, below bf16's 2^-9), n added to the exponent
+// field. Used for a fraction of the softmax exponentials so MUFU.EX2 is not the bottleneck.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;   // 1.5 * 2^23: n sits in the low mantissa bits of t
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.05517132f, f, 0.24261054f);
+  p = fmaf(p, f, 0.69326097f);
+  p = fmaf(p, f, 0.99992812f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 template <int DH>
 struct Cfg {
@@ -328,6 +359,281 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     if (qi < T_) lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+// ======================================================================================
+// Forward v2: two 128-query tiles per CTA, ping-pong between two softmax warpgroups so the
+// tensor core works on one tile while the other tile's exponentials run.
+//   warp 0      TMA producer: Q0, Q1 once; then K_j, V_j through a ring of NSLOT tile slots
+//   warp 1      MMA issuer, per key block j:  PV0(j-1)... in the order
+//                 S0(0) S1(0) | PV0(0) S0(1) PV1(0) S1(1) | PV0(1) S0(2) PV1(1) S1(2) | ...
+//   warp 2      TMEM allocator (512 columns: S0/P0 | S1/P1 | O0 | O1)
+//   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1 (thread = query row = TMEM lane)
+// P is written back into TMEM over its own S columns (bf16 pairs) and is the A operand of the
+// O += P V MMA (tcgen05 "TS" form): no shared-memory round trip for P. The MMAs of one tile
+// execute in issue order, so S_t(j+1) overwrites P_t(j) only after PV_t(j) has read it, and
+// the commit that publishes S_t(j+1) also certifies that PV_t(j) finished (O_t is stable for
+// the lazy rescale).
+// ======================================================================================
+template <int DH>
+struct Cfg2 {
+  static constexpr int NP = (DH + 63) / 64;
+  static constexpr int PANEL = 128 * 128;
+  static constexpr int SLOT = NP * PANEL;             // one K or V tile of 128 keys
+  static constexpr int Q_BYTES = 2 * NP * PANEL;      // two query tiles
+  static constexpr int NSLOT_FIT = (232448 - Q_BYTES - 2048) / SLOT;
+  static constexpr int NSLOT = NSLOT_FIT > 8 ? 8 : NSLOT_FIT;
+  static constexpr int SMEM = Q_BYTES + NSLOT * SLOT + 1024 + 512;
+  static constexpr uint32_t S_COL = 0, O_COL = 256;  // tile t: S/P at 128t, O at 256 + 128t
+};
+
+template <int DH>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, float* __restrict__ lse, int T_,
+                        int h) {
+  using C = Cfg2<DH>;
+  constexpr int NS = C::NSLOT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;                        // tile t at + t * NP * PANEL
+  uint8_t* sR = sQ + C::Q_BYTES;           // ring slot s at + s * SLOT
+  uint64_t* bars = (uint64_t*)(sR + NS * C::SLOT);
+  uint64_t* q_full = bars;                 // [1]
+  uint64_t* r_full = bars + 1;             // [NS]
+  uint64_t* r_empty = bars + 1 + NS;       // [NS]
+  uint64_t* s_full = bars + 1 + 2 * NS;    // [2]
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* o_full = p_full + 2;           // [2]
+  uint32_t* tmem_slot = (uint32_t*)(o_full + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npair = (T_ + 2 * BQ - 1) / (2 * BQ);
+  const int qp = npair - 1 - blockIdx.x;   // heavy (late) query pairs first
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int nkb_all = (T_ + BKV - 1) / BKV;
+  // tile t covers queries [128 (2 qp + t), +128); it sees key blocks 0 .. 2 qp + t
+  const int qb0 = 2 * qp, qb1 = 2 * qp + 1;
+  const int nkb0 = min(qb0 + 1, nkb_all);
+  const int nkb1 = qb1 * BQ < T_ ? min(qb1 + 1, nkb_all) : 0;
+  const int nkb = max(nkb0, nkb1);
+  const int row0 = b * T_;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_full[t], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+      const int ntile = nkb1 > 0 ? 2 : 1;
+      mbar_expect_tx(q_full, ntile * C::NP * C::PANEL);
+      for (int t = 0; t < ntile; ++t)
+        for (int p = 0; p < C::NP; ++p)
+          tma_load(sQ + (t * C::NP + p) * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + (qb0 + t) * BQ);
+      // ring positions: K_j at 2j, V_j at 2j + 1
+      for (int pos = 0; pos < 2 * nkb; ++pos) {
+        const int s = pos % NS, use = pos / NS, j = pos >> 1;
+        mbar_wait(&r_empty[s], (use & 1) ^ 1);
+        uint8_t* dst = sR + s * C::SLOT;
+        mbar_expect_tx(&r_full[s], C::SLOT);
+        const int col = ((pos & 1) ? 2 * d : d) + hh * DH;
+        for (int p = 0; p < C::NP; ++p) tma_load(dst + p * C::PANEL, &tm, &r_full[s], col + 64 * p, row0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t id_s = idesc_bf16(128, BKV, false, false);  // S = Q K^T (both K-major)
+    constexpr uint32_t id_o = idesc_bf16(128, DH, false, true);    // O += P V (P in TMEM, V MN-major)
+    auto wait_pos = [&](int pos) {
+      mbar_wait(&r_full[pos % NS], (pos / NS) & 1);
+      fence_after();
+    };
+    auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T; K_j resident
+      if (lane == 0) {
+        const uint32_t q = smem_u32(sQ + t * C::NP * C::PANEL), k = smem_u32(sR + ((2 * j) % NS) * C::SLOT);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::PANEL + (kk & 3) * 32;
+          mma(tbase + C::S_COL + 128 * t, desc_sw128(q + off, 16, 1024), desc_sw128(k + off, 16, 1024), id_s,
+              kk > 0);
+        }
+        commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {   // O_t += P_t(j) V_j
+      mbar_wait(&p_full[t], j & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t v = smem_u32(sR + ((2 * j + 1) % NS) * C::SLOT);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tbase + C::O_COL + 128 * t, tbase + C::S_COL + 128 * t + 8 * kk,
+                 desc_sw128(v + kk * 2048, C::PANEL, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    auto release = [&](int pos) {
+      if (lane == 0) commit(&r_empty[pos % NS]);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    wait_pos(0);
+    if (nkb0 > 0) issue_s(0, 0);
+    if (nkb1 > 0) issue_s(1, 0);
+    release(0);
+    for (int j = 0; j < nkb; ++j) {
+      wait_pos(2 * j + 1);   // V_j
+      const bool more = j + 1 < nkb;
+      if (more) wait_pos(2 * j + 2);   // K_{j+1}
+      if (j < nkb0) {
+        issue_pv(0, j);
+        if (j + 1 < nkb0) issue_s(0, j + 1);
+        else if (lane == 0) commit(&o_full[0]);
+      }
+      if (j < nkb1) {
+        issue_pv(1, j);
+        if (j + 1 < nkb1) issue_s(1, j + 1);
+        else if (lane == 0) commit(&o_full[1]);
+      }
+      __syncwarp();
+      release(2 * j + 1);
+      if (more) release(2 * j + 2);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax, tile t
+    const int t = (warp - 4) >> 2;
+    const int qw = warp & 3;
+    const int r = 32 * qw + lane;
+    const int qb = qb0 + t;
+    const int qi = qb * BQ + r;
+    const int my_nkb = t ? nkb1 : nkb0;
+    const uint32_t lane_addr = tbase + ((uint32_t)(32 * qw) << 16);
+    const uint32_t s_addr = lane_addr + C::S_COL + 128 * t, o_addr = lane_addr + C::O_COL + 128 * t;
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < my_nkb; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      fence_after();
+      uint32_t raw[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV; c += 32) tmem_ld32(s_addr + c, raw + c);
+      tmem_wait_ld();
+      const bool masked = j == qb || (j + 1) * BKV > T_;
+      float mx = -INFINITY;
+      if (masked) {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          const int kj = j * BKV + c;
+          float v = __uint_as_float(raw[c]) * sc;
+          if (kj > qi || kj >= T_) v = -INFINITY;
+          raw[c] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BKV; ++c) {
+          const float v = __uint_as_float(raw[c]) * sc;
+          raw[c] = __float_as_uint(v);
+          mx = fmaxf(mx, v);
+        }
+      }
+      const bool need = mx > m_ref + RESCALE_THRESHOLD;
+      const float new_ref = need ? mx : m_ref;
+      const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
+      // PV_t(j-1) completed before s_full[t] fired for S_t(j): O_t is stable here
+      if (__any_sync(0xffffffffu, need) && j > 0) {
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {
+          uint32_t ov[16];
+          tmem_ld16(o_addr + c, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st16(o_addr + c, ov);
+        }
+      }
+      l *= alpha;
+      m_ref = new_ref;
+      // P = 2^(S - m_ref) -> bf16 pairs into TMEM over S (16 columns = 32 keys at a time)
+      float rs = 0.f;
+#pragma unroll
+      for (int c16 = 0; c16 < BKV / 32; ++c16) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = c16 * 32 + 2 * i;
+          const float x0 = __uint_as_float(raw[c]) - m_ref, x1 = __uint_as_float(raw[c + 1]) - m_ref;
+          float p0, p1;
+          if (!masked && (i & 3) == 0) {   // 1 pair in 4 on the FMA pipe
+            p0 = exp2_poly(x0);
+            p1 = exp2_poly(x1);
+          } else {
+            p0 = fast_exp2(x0);
+            p1 = fast_exp2(x1);
+          }
+          rs += p0 + p1;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+          pk[i] = *(uint32_t*)&v2;
+        }
+        tmem_st16(s_addr + 16 * c16, pk);
+      }
+      l += rs;
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    if (my_nkb > 0) {
+      mbar_wait(&o_full[t], 0);
+      fence_after();
+      const float inv = 1.f / l;
+      bf16* orow = o + ((long)b * T_ + qi) * d + hh * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 16) {
+        uint32_t ov[16];
+        tmem_ld16(o_addr + c, ov);
+        tmem_wait_ld();
+        if (qi < T_) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat162 v2 =
+                __floats2bfloat162_rn(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+            pk[i] = *(uint32_t*)&v2;
+          }
+          *(uint4*)(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *(uint4*)(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      if (qi < T_) lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
+    }
   }
   fence_before();
   __syncthreads();
@@ -757,19 +1063,442 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ======================================================================================
+// Backward v2. Same math and block shapes as above, re-organised for the tensor core:
+//   * P^T / dS^T (dK/dV kernel) and dS (dQ kernel) go back into TMEM over the S / dP columns
+//     they were computed from and feed the next MMAs as TMEM A operands (no smem round trip);
+//   * 4-stage TMA rings for the streamed tiles (a 2-stage ring left TMA latency exposed);
+//   * two elementwise warpgroups, each on half of the 64 columns of a block (warps w and w+4
+//     share TMEM lanes; a 64-thread named barrier per lane quarter orders their loads before
+//     the in-place stores);
+//   * the streamed per-query LSE / D values are staged by the producer warp with the tiles;
+//   * the causal mask is applied only on the blocks that straddle the diagonal.
+// Key rows beyond T_ (dK/dV kernel) and query rows beyond T_ (dQ kernel) produce values that
+// are never stored; every result row depends only on its own TMEM lane.
+// ======================================================================================
+constexpr int BW_NST = 4;   // ring stages
+
+template <int DH>
+struct BCfg2 {
+  static constexpr int NP = (DH + 63) / 64;
+  static constexpr int P128 = 128 * 128, P64 = 64 * 128;
+  static constexpr int FIX = 2 * NP * P128;          // K,V (dK/dV kernel) or Q,dO (dQ kernel)
+  static constexpr int STG = 2 * NP * P64;           // Q_i,dO_i or K_j,V_j: 64 rows each
+  static constexpr int SMEM = FIX + BW_NST * STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
+  static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256, ACC1 = 384;   // buffer u: +128u
+};
+
+template <int DH>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                         const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
+  using C = BCfg2<DH>;
+  constexpr int NST = BW_NST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + C::NP * C::P128;
+  uint8_t* sS = sm + C::FIX;                           // stage s: Q at + s*STG, dO at + NP*P64
+  float* sLD = (float*)(sS + NST * C::STG);            // stage s: L[64] at + 128 s, D[64] at + 128 s + 64
+  uint64_t* bars = (uint64_t*)(sLD + NST * 128);
+  uint64_t* kv_full = bars;
+  uint64_t* st_full = bars + 1;           // [NST]  TMA tx + 32 producer lanes
+  uint64_t* st_empty = bars + 1 + NST;    // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;  // [2]
+  uint64_t* p_full = s_full + 2;          // [2]
+  uint64_t* done = p_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int k0 = kb * 128;
+  const int nq = (T_ + 63) / 64;
+  const int i0 = k0 / 64;
+  const int nblk = nq - i0;
+  const int row0 = b * T_;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&st_full[s], 33);
+      mbar_init(&st_empty[s], 1);
+    }
+    for (int u = 0; u < 2; ++u) {
+      mbar_init(&s_full[u], 1);
+      mbar_init(&p_full[u], 256);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    const float* lrow = lse + ((long)b * h + hh) * T_;
+    const float* drow = Dsum + ((long)b * h + hh) * T_;
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, C::FIX);
+      for (int p = 0; p < C::NP; ++p) {
+        tma_load(sK + p * C::P128, &tm_kv, kv_full, d + hh * DH + 64 * p, row0 + k0);
+        tma_load(sV + p * C::P128, &tm_kv, kv_full, 2 * d + hh * DH + 64 * p, row0 + k0);
+      }
+    }
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it % NST, q0 = (i0 + it) * 64;
+      mbar_wait(&st_empty[s], ((it / NST) & 1) ^ 1);
+      if (lane == 0) {
+        uint8_t* q = sS + s * C::STG;
+        uint8_t* g = q + C::NP * C::P64;
+        mbar_expect_tx(&st_full[s], C::STG);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(q + p * C::P64, &tm_q, &st_full[s], hh * DH + 64 * p, row0 + q0);
+          tma_load(g + p * C::P64, &tm_do, &st_full[s], hh * DH + 64 * p, row0 + q0);
+        }
+      }
+      // queries beyond T_: L = +inf makes P (and so dS) exactly 0
+      float* L = sLD + 128 * s;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int qi = q0 + lane + 32 * e;
+        L[lane + 32 * e] = qi < T_ ? lrow[qi] * LOG2E : INFINITY;
+        L[64 + lane + 32 * e] = qi < T_ ? drow[qi] : 0.f;
+      }
+      mbar_arrive(&st_full[s]);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
+    constexpr uint32_t id_g = idesc_bf16(128, DH, false, true);    // dV += P^T dO, dK += dS^T Q
+    mbar_wait(kv_full, 0);
+    auto issue_s = [&](int it) {
+      const int s = it % NST, u = it & 1;
+      mbar_wait(&st_full[s], (it / NST) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t q = smem_u32(sS + s * C::STG), g = q + C::NP * C::P64;
+        const uint32_t k = smem_u32(sK), v = smem_u32(sV);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
+          mma(tbase + C::ST_COL + 128 * u, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + C::DPT_COL + 128 * u, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s,
+              kk > 0);
+        }
+        commit(&s_full[u]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it % NST, u = it & 1;
+      if (it + 1 < nblk) issue_s(it + 1);
+      mbar_wait(&p_full[u], (it >> 1) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t q = smem_u32(sS + s * C::STG), g = q + C::NP * C::P64;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
+          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, desc_sw128(g + kk * 2048, C::P64, 1024),
+                 id_g, acc);
+          mma_ts(tbase + C::ACC1, tbase + C::DPT_COL + 128 * u + 8 * kk, desc_sw128(q + kk * 2048, C::P64, 1024),
+                 id_g, acc);
+        }
+        commit(&st_empty[s]);
+        if (it == nblk - 1) commit(done);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2, qw = warp & 3;
+    const int r = 32 * qw + lane, kj = k0 + r;
+    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    for (int it = 0; it < nblk; ++it) {
+      const int s = it % NST, u = it & 1, q0 = (i0 + it) * 64;
+      mbar_wait(&st_full[s], (it / NST) & 1);   // L / D of this stage visible
+      mbar_wait(&s_full[u], (it >> 1) & 1);
+      fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld32(la + C::ST_COL + 128 * u + 32 * wg, sv);
+      tmem_ld32(la + C::DPT_COL + 128 * u + 32 * wg, dv);
+      tmem_wait_ld();
+      const float* L = sLD + 128 * s + 32 * wg;
+      const float* D = L + 64;
+      const bool masked = q0 < k0 + 128;   // block straddles the diagonal
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 l4 = *(const float4*)(L + 4 * c4);
+        const float4 d4 = *(const float4*)(D + 4 * c4);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd4[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pp[4], dd[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = 4 * c4 + e;
+          float p = fast_exp2(fmaf(__uint_as_float(sv[c]), sc, -lv[e]));
+          if (masked && q0 + 32 * wg + c < kj) p = 0.f;
+          pp[e] = p;
+          dd[e] = p * (__uint_as_float(dv[c]) - dd4[e]);
+        }
+        __nv_bfloat162 a0 = __floats2bfloat162_rn(pp[0], pp[1]), a1 = __floats2bfloat162_rn(pp[2], pp[3]);
+        __nv_bfloat162 b0 = __floats2bfloat162_rn(dd[0], dd[1]), b1 = __floats2bfloat162_rn(dd[2], dd[3]);
+        pk[2 * c4] = *(uint32_t*)&a0;
+        pk[2 * c4 + 1] = *(uint32_t*)&a1;
+        dk[2 * c4] = *(uint32_t*)&b0;
+        dk[2 * c4 + 1] = *(uint32_t*)&b1;
+      }
+      named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
+      tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
+      tmem_st16(la + C::DPT_COL + 128 * u + 16 * wg, dk);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&p_full[u]);
+    }
+    mbar_wait(done, 0);
+    fence_after();
+    // warpgroup 0 writes dV, warpgroup 1 writes dK (scaled by 1/sqrt(dh))
+    const float scale = wg ? rsqrtf((float)DH) : 1.f;
+    bf16* row = dqkv + ((long)row0 + kj) * 3 * d + (wg ? d : 2 * d) + hh * DH;
+    const uint32_t acc = la + (wg ? C::ACC1 : C::ACC0);
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t gv[16];
+      tmem_ld16(acc + c, gv);
+      tmem_wait_ld();
+      if (kj < T_) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 v2 =
+              __floats2bfloat162_rn(__uint_as_float(gv[2 * i]) * scale, __uint_as_float(gv[2 * i + 1]) * scale);
+          pk[i] = *(uint32_t*)&v2;
+        }
+        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                        const __grid_constant__ CUtensorMap tm_kv, const float* __restrict__ lse,
+                        const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
+  using C = BCfg2<DH>;
+  constexpr int NST = BW_NST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;
+  uint8_t* sO = sQ + C::NP * C::P128;
+  uint8_t* sS = sm + C::FIX;   // stage s: K_j at + s*STG, V_j at + NP*P64
+  uint64_t* bars = (uint64_t*)(sS + NST * C::STG + NST * 512);
+  uint64_t* qo_full = bars;
+  uint64_t* st_full = bars + 1;           // [NST]
+  uint64_t* st_empty = bars + 1 + NST;    // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;  // [2]
+  uint64_t* p_full = s_full + 2;          // [2]
+  uint64_t* done = p_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (T_ + 127) / 128;
+  const int qb = nqb - 1 - blockIdx.x;
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int q0 = qb * 128;
+  const int nblk = min((q0 + 127) / 64 + 1, (T_ + 63) / 64);
+  const int row0 = b * T_;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qo_full, 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 1);
+    }
+    for (int u = 0; u < 2; ++u) {
+      mbar_init(&s_full[u], 1);
+      mbar_init(&p_full[u], 256);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qo_full, C::FIX);
+      for (int p = 0; p < C::NP; ++p) {
+        tma_load(sQ + p * C::P128, &tm_q, qo_full, hh * DH + 64 * p, row0 + q0);
+        tma_load(sO + p * C::P128, &tm_do, qo_full, hh * DH + 64 * p, row0 + q0);
+      }
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % NST;
+        mbar_wait(&st_empty[s], ((j / NST) & 1) ^ 1);
+        uint8_t* k = sS + s * C::STG;
+        uint8_t* v = k + C::NP * C::P64;
+        mbar_expect_tx(&st_full[s], C::STG);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(k + p * C::P64, &tm_kv, &st_full[s], d + hh * DH + 64 * p, row0 + j * 64);
+          tma_load(v + p * C::P64, &tm_kv, &st_full[s], 2 * d + hh * DH + 64 * p, row0 + j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S = Q K^T, dP = dO V^T
+    constexpr uint32_t id_q = idesc_bf16(128, DH, false, true);    // dQ += dS K
+    mbar_wait(qo_full, 0);
+    auto issue_s = [&](int j) {
+      const int s = j % NST, u = j & 1;
+      mbar_wait(&st_full[s], (j / NST) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t k = smem_u32(sS + s * C::STG), v = k + C::NP * C::P64;
+        const uint32_t q = smem_u32(sQ), g = smem_u32(sO);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
+          mma(tbase + C::ST_COL + 128 * u, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
+          mma(tbase + C::DPT_COL + 128 * u, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s,
+              kk > 0);
+        }
+        commit(&s_full[u]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nblk; ++j) {
+      const int s = j % NST, u = j & 1;
+      if (j + 1 < nblk) issue_s(j + 1);
+      mbar_wait(&p_full[u], (j >> 1) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t k = smem_u32(sS + s * C::STG);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)   // 64 keys = 4 x 16
+          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, desc_sw128(k + kk * 2048, C::P64, 1024),
+                 id_q, (j > 0 || kk > 0) ? 1u : 0u);
+        commit(&st_empty[s]);
+        if (j == nblk - 1) commit(done);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2, qw = warp & 3;
+    const int r = 32 * qw + lane, qi = q0 + r;
+    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    const float sc = rsqrtf((float)DH) * LOG2E;
+    const float L = qi < T_ ? lse[((long)b * h + hh) * T_ + qi] * LOG2E : INFINITY;
+    const float Dr = qi < T_ ? Dsum[((long)b * h + hh) * T_ + qi] : 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int u = j & 1;
+      mbar_wait(&s_full[u], (j >> 1) & 1);
+      fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld32(la + C::ST_COL + 128 * u + 32 * wg, sv);
+      tmem_ld32(la + C::DPT_COL + 128 * u + 32 * wg, dv);
+      tmem_wait_ld();
+      const int kbase = j * 64 + 32 * wg;
+      const bool masked = j * 64 + 63 > q0 || (j + 1) * 64 > T_;   // diagonal or ragged keys
+      uint32_t dk[16];
+#pragma unroll
+      for (int c2 = 0; c2 < 16; ++c2) {
+        float dd[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * c2 + e;
+          float p;
+          if (!masked && (c2 & 3) == 0) p = exp2_poly(fmaf(__uint_as_float(sv[c]), sc, -L));
+          else p = fast_exp2(fmaf(__uint_as_float(sv[c]), sc, -L));
+          if (masked && (kbase + c > qi || kbase + c >= T_)) p = 0.f;
+          dd[e] = p * (__uint_as_float(dv[c]) - Dr);
+        }
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(dd[0], dd[1]);
+        dk[c2] = *(uint32_t*)&b2;
+      }
+      named_sync(1 + qw, 64);
+      tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, dk);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(&p_full[u]);
+    }
+    mbar_wait(done, 0);
+    fence_after();
+    // each warpgroup writes half of the dQ row
+    const float isq = rsqrtf((float)DH);
+    bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
+    constexpr int HALF = ((DH / 16) + 1) / 2 * 16;   // 64 / 48 / 32 columns for warpgroup 0
+    const int c_lo = wg ? HALF : 0, c_hi = wg ? DH : HALF;
+    for (int c = c_lo; c < c_hi; c += 16) {
+      uint32_t gq[16];
+      tmem_ld16(la + C::ACC0 + c, gq);
+      tmem_wait_ld();
+      if (qi < T_) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 q2 =
+              __floats2bfloat162_rn(__uint_as_float(gq[2 * i]) * isq, __uint_as_float(gq[2 * i + 1]) * isq);
+          pk[i] = *(uint32_t*)&q2;
+        }
+        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  }
+}
+
+// D[b, h, t] = sum_f dO[t, h f] O[t, h f]: one thread per (token, head), 16-byte vectors;
+// consecutive threads take consecutive heads of a token (contiguous bytes)
+template <int DH>
 __global__ void dsum_tc_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ Dsum,
-                               int B, int T_, int h, int dh) {
-  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
-  if (gw >= (long)B * h * T_) return;
-  const int lane = threadIdx.x & 31;
-  const int t = (int)(gw % T_);
-  const int hh = (int)((gw / T_) % h);
-  const int b = (int)(gw / ((long)T_ * h));
-  const long off = ((long)b * T_ + t) * h * dh + hh * dh;
+                               int B, int T_, int h) {
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i >= (long)B * T_ * h) return;
+  const long row = i / h;
+  const int hh = (int)(i - row * h);
+  const long off = row * h * DH + hh * DH;
   float s = 0.f;
-  for (int j = lane; j < dh; j += 32) s = fmaf(__bfloat162float(o[off + j]), __bfloat162float(dout[off + j]), s);
-  s = warp_sum(s);
-  if (lane == 0) Dsum[((long)b * h + hh) * T_ + t] = s;
+#pragma unroll
+  for (int c = 0; c < DH; c += 8) {
+    const uint4 a = *(const uint4*)(o + off + c), g = *(const uint4*)(dout + off + c);
+    const bf16* ap = (const bf16*)&a;
+    const bf16* gp = (const bf16*)&g;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s = fmaf(__bfloat162float(ap[e]), __bfloat162float(gp[e]), s);
+  }
+  const long b = row / T_, t = row - b * T_;
+  Dsum[(b * h + hh) * T_ + t] = s;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -808,12 +1537,22 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
     return false;
   }
   static bool once = false;
+  static bool v1 = false;   // ATOM_ATTN_FWD_V1=1: the one-tile kernel (A/B comparisons)
   if (!once) {
+    const char* e = getenv("ATOM_ATTN_FWD_V1");
+    v1 = e && e[0] == '1';
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg2<DH>::SMEM));
     once = true;
   }
-  dim3 grid((T_ + BQ - 1) / BQ, B * h);
-  attn_fwd_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tm, o, lse, T_, h);
+  if (v1) {
+    dim3 grid((T_ + BQ - 1) / BQ, B * h);
+    attn_fwd_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tm, o, lse, T_, h);
+  } else {
+    dim3 grid((T_ + 2 * BQ - 1) / (2 * BQ), B * h);
+    attn_fwd2_tc_kernel<DH><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, o, lse, T_, h);
+  }
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
@@ -848,21 +1587,35 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
       !make_map2d(&do64, dout, d, rows, 64) || !make_map2d(&do128, dout, d, rows, 128))
     return false;
   static bool once = false;
+  static bool v1 = false;   // ATOM_ATTN_BWD_V1=1: the first-generation kernels (A/B comparisons)
   if (!once) {
+    const char* e = getenv("ATOM_ATTN_BWD_V1");
+    v1 = e && e[0] == '1';
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_KV));
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_Q));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg2<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg2<DH>::SMEM));
     once = true;
   }
-  const long warps = rows * h;
-  dsum_tc_kernel<<<(warps + 7) / 8, 256, 0, st>>>(o, dout, Dsum, B, T_, h, DH);
+  const long nthr = rows * h;
+  dsum_tc_kernel<DH><<<(nthr + 255) / 256, 256, 0, st>>>(o, dout, Dsum, B, T_, h);
   count_launch();
   dim3 grid((T_ + 127) / 128, B * h);
-  attn_bwd_dkv_tc_kernel<DH><<<grid, 256, C::SMEM_KV, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
-  count_launch();
-  attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
-  count_launch();
+  if (v1) {
+    attn_bwd_dkv_tc_kernel<DH><<<grid, 256, C::SMEM_KV, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
+    count_launch();
+    attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
+    count_launch();
+  } else {
+    attn_bwd_dkv2_kernel<DH><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
+    count_launch();
+    attn_bwd_dq2_kernel<DH><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
+    count_launch();
+  }
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }

@@ -29,6 +29,27 @@ __device__ __forceinline__ float gelu_grad_f(float u) {
   return 0.5f * (1.f + th) + 0.5f * u * (1.f - th * th) * kGeluC * (1.f + 3.f * 0.044715f * u * u);
 }
 
+// bf16 path: hardware tanh (MUFU.TANH, ~2^-11 relative error, far below bf16's 2^-8 rounding)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float u) {
+  return 0.5f * u * (1.f + tanh_fast(kGeluC * (u + 0.044715f * u * u * u)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float u) {
+  const float th = tanh_fast(kGeluC * (u + 0.044715f * u * u * u));
+  return 0.5f * (1.f + th) + 0.5f * u * (1.f - th * th) * kGeluC * (1.f + 3.f * 0.044715f * u * u);
+}
+// per activation dtype: exact for the fp32 parity path, hardware tanh for bf16
+template <typename T> __device__ __forceinline__ float gelu_t(float u);
+template <> __device__ __forceinline__ float gelu_t<float>(float u) { return gelu_f(u); }
+template <> __device__ __forceinline__ float gelu_t<bf16>(float u) { return gelu_fast(u); }
+template <typename T> __device__ __forceinline__ float gelu_grad_t(float u);
+template <> __device__ __forceinline__ float gelu_grad_t<float>(float u) { return gelu_grad_f(u); }
+template <> __device__ __forceinline__ float gelu_grad_t<bf16>(float u) { return gelu_grad_fast(u); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

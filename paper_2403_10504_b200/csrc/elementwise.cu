@@ -51,7 +51,7 @@ __device__ __forceinline__ void store_vec(T* p, const float* f) {
 }
 
 // y = LN(x) * g + b; stats[row] = (mean, rstd)                       (minGPT nn.LayerNorm)
-template <typename T>
+template <typename T, int NC>
 __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                             const T* __restrict__ b, T* __restrict__ y,
                                                             float* __restrict__ stats, int d) {
@@ -60,10 +60,10 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
   const long row = blockIdx.x;
   const int nch = d / VW;
   const T* xr = x + row * d;
-  float v[LN_MAXC][VW];
+  float v[NC][VW];
   float s = 0.f;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       load_vec<T>(xr + ch * VW, v[c]);
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
   const float mean = block_sum128(s, sh) / (float)d;
   float q = 0.f;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c)
+  for (int c = 0; c < NC; ++c)
     if (c * LN_THREADS + threadIdx.x < nch)
 #pragma unroll
       for (int i = 0; i < VW; ++i) {
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
   const float rstd = rsqrtf(var + LN_EPS);
   T* yr = y + row * d;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       float gg[VW], bb[VW], o[VW];
@@ -124,7 +124,7 @@ __global__ void ln_apply_kernel(const T* __restrict__ x, const T* __restrict__ g
 }
 
 // dx = dres + rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat))
-template <typename T>
+template <typename T, int NC>
 __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                             const float* __restrict__ stats,
                                                             const T* __restrict__ g, const T* __restrict__ dres,
@@ -134,10 +134,10 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
   const long row = blockIdx.x;
   const int nch = d / VW;
   const float mean = stats[2 * row], rstd = stats[2 * row + 1];
-  float xh[LN_MAXC][VW], dg[LN_MAXC][VW];
+  float xh[NC][VW], dg[NC][VW];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       float gg[VW];
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
   const float m1 = block_sum128(s1, sh) / (float)d;
   const float m2 = block_sum128(s2, sh) / (float)d;
 #pragma unroll
-  for (int c = 0; c < LN_MAXC; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       float o[VW], r[VW];
@@ -174,11 +174,14 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
 // Column partial sums over chunks of RED_ROWS rows (fixed order):
 //   mode 0: part0[c][j] = sum_r a[r][j]                  (bias gradient: sum of dY over tokens)
 //   mode 1: part0[c][j] = sum_r a[r][j] * xhat[r][j], part1[c][j] = sum_r a[r][j]   (LN gain / shift)
-// Each thread owns one 16-byte vector of columns (8 bf16 / 4 fp32); ncols % VW == 0.
-template <typename T>
-__global__ void col_partials_kernel(int mode, const T* __restrict__ a, long lda, const T* __restrict__ x,
-                                    const float* __restrict__ stats, long rows, int ncols, float* __restrict__ part0,
-                                    float* __restrict__ part1) {
+// Each thread owns one 16-byte vector of columns (8 bf16 / 4 fp32); ncols % VW == 0. Rows are
+// loaded CP_UNR at a time (several 16-byte loads in flight per thread: the kernel is HBM-bound
+// and a one-load-at-a-time loop ran at ~1.4 TB/s), then added in ascending row order.
+constexpr int CP_UNR = 8;
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) col_partials_kernel(const T* __restrict__ a, long lda, const T* __restrict__ x,
+                                                           const float* __restrict__ stats, long rows, int ncols,
+                                                           float* __restrict__ part0, float* __restrict__ part1) {
   constexpr int VW = Vec<T>::N;
   const int j = (blockIdx.x * blockDim.x + threadIdx.x) * VW;
   const int c = blockIdx.y;
@@ -187,27 +190,36 @@ __global__ void col_partials_kernel(int mode, const T* __restrict__ a, long lda,
   float s0[VW], s1[VW];
 #pragma unroll
   for (int i = 0; i < VW; ++i) s0[i] = s1[i] = 0.f;
-  for (long r = r0; r < r1; ++r) {
-    float v[VW];
-    load_vec<T>(a + r * lda + j, v);
-    if (mode == 1) {
-      float xv[VW];
-      load_vec<T>(x + r * ncols + j, xv);
-      const float mean = stats[2 * r], rstd = stats[2 * r + 1];
+  for (long rb = r0; rb < r1; rb += CP_UNR) {
+    float v[CP_UNR][VW], xv[MODE == 1 ? CP_UNR : 1][VW];
 #pragma unroll
-      for (int i = 0; i < VW; ++i) {
-        s0[i] = fmaf(v[i], (xv[i] - mean) * rstd, s0[i]);
-        s1[i] += v[i];
+    for (int u = 0; u < CP_UNR; ++u) {
+      if (rb + u < r1) {
+        load_vec<T>(a + (rb + u) * lda + j, v[u]);
+        if constexpr (MODE == 1) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
       }
-    } else {
+    }
 #pragma unroll
-      for (int i = 0; i < VW; ++i) s0[i] += v[i];
+    for (int u = 0; u < CP_UNR; ++u) {
+      if (rb + u < r1) {
+        if constexpr (MODE == 1) {
+          const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
+#pragma unroll
+          for (int i = 0; i < VW; ++i) {
+            s0[i] = fmaf(v[u][i], (xv[u][i] - mean) * rstd, s0[i]);
+            s1[i] += v[u][i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < VW; ++i) s0[i] += v[u][i];
+        }
+      }
     }
   }
 #pragma unroll
   for (int i = 0; i < VW; ++i) {
     part0[(long)c * ncols + j + i] = s0[i];
-    if (mode == 1) part1[(long)c * ncols + j + i] = s1[i];
+    if constexpr (MODE == 1) part1[(long)c * ncols + j + i] = s1[i];
   }
 }
 
@@ -216,6 +228,7 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int nchun
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncols) return;
   float s = 0.f;
+#pragma unroll 8
   for (int c = 0; c < nchunk; ++c) s += part[(long)c * ncols + j];
   out[j] += s;
 }
@@ -367,7 +380,7 @@ __global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ g, long n) 
     float v[VW];
     load_vec<T>(u + i * VW, v);
 #pragma unroll
-    for (int k = 0; k < VW; ++k) v[k] = gelu_f(v[k]);
+    for (int k = 0; k < VW; ++k) v[k] = gelu_t<T>(v[k]);
     store_vec<T>(g + i * VW, v);
   }
 }
@@ -470,7 +483,12 @@ bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, i
     set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
     return false;
   }
-  ln_fwd_kernel<T><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d);
+  switch ((d / Vec<T>::N + LN_THREADS - 1) / LN_THREADS) {   // chunks per thread (same order for any NC)
+#define LN_FWD_CASE(NC) \
+  case NC: ln_fwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d); break;
+    LN_FWD_CASE(1) LN_FWD_CASE(2) LN_FWD_CASE(3) LN_FWD_CASE(4) LN_FWD_CASE(5) LN_FWD_CASE(6)
+#undef LN_FWD_CASE
+  }
   LAUNCH_OK();
   return true;
 }
@@ -483,13 +501,22 @@ bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long
 template <typename T>
 bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dres, T* dx, float* dg, float* db,
             float* part, long rows, int d, cudaStream_t st) {
-  ln_bwd_kernel<T><<<rows, LN_THREADS, 0, st>>>(dy, x, stats, g, dres, dx, d);
+  if (d % Vec<T>::N || d > LN_THREADS * LN_MAXC * Vec<T>::N) {
+    set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
+    return false;
+  }
+  switch ((d / Vec<T>::N + LN_THREADS - 1) / LN_THREADS) {
+#define LN_BWD_CASE(NC) \
+  case NC: ln_bwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(dy, x, stats, g, dres, dx, d); break;
+    LN_BWD_CASE(1) LN_BWD_CASE(2) LN_BWD_CASE(3) LN_BWD_CASE(4) LN_BWD_CASE(5) LN_BWD_CASE(6)
+#undef LN_BWD_CASE
+  }
   LAUNCH_OK();
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   float* p0 = part;
   float* p1 = part + (long)nch * d;
   constexpr int VW = Vec<T>::N;
-  col_partials_kernel<T><<<dim3((d / VW + 127) / 128, nch), 128, 0, st>>>(1, dy, d, x, stats, rows, d, p0, p1);
+  col_partials_kernel<T, 1><<<dim3((d / VW + 127) / 128, nch), 128, 0, st>>>(dy, d, x, stats, rows, d, p0, p1);
   LAUNCH_OK();
   reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p0, nch, d, dg);
   LAUNCH_OK();
@@ -505,8 +532,8 @@ bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, c
     set_error("bias_grad: columns and pitch must be multiples of %d", VW);
     return false;
   }
-  col_partials_kernel<T><<<dim3((n / VW + 127) / 128, nch), 128, 0, st>>>(0, dy, ld, nullptr, nullptr, rows, n,
-                                                                           part, nullptr);
+  col_partials_kernel<T, 0><<<dim3((n / VW + 127) / 128, nch), 128, 0, st>>>(dy, ld, nullptr, nullptr, rows, n,
+                                                                              part, nullptr);
   LAUNCH_OK();
   reduce_partials_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, nch, n, db);
   LAUNCH_OK();

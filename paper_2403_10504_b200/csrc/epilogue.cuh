@@ -50,11 +50,11 @@ __device__ __forceinline__ void epi_scalar(const Epi& e, long m, long n, float a
     case EPI_BIAS_GELU: {
       T u = from_f<T>(acc + to_f(((const T*)e.bias)[n]));
       ((T*)e.out)[m * e.ldo + n] = u;
-      ((T*)e.out2)[m * e.ldo2 + n] = from_f<T>(gelu_f(to_f(u)));
+      ((T*)e.out2)[m * e.ldo2 + n] = from_f<T>(gelu_t<T>(to_f(u)));
       return;
     }
     case EPI_DGELU:
-      ((T*)e.out)[m * e.ldo + n] = from_f<T>(acc * gelu_grad_f(to_f(((const T*)e.aux)[m * e.ldx + n])));
+      ((T*)e.out)[m * e.ldo + n] = from_f<T>(acc * gelu_grad_t<T>(to_f(((const T*)e.aux)[m * e.ldx + n])));
       return;
   }
 }
@@ -89,7 +89,7 @@ __device__ __forceinline__ void epi_vec8_bf16(const Epi& e, long m, long n, cons
     uint4 xx = *(const uint4*)((const bf16*)e.aux + m * e.ldx + n);
     const bf16* xp = (const bf16*)&xx;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(__bfloat162float(xp[i]));
+    for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(__bfloat162float(xp[i]));
   }
   uint4 ov;
   bf16* op = (bf16*)&ov;
@@ -100,7 +100,7 @@ __device__ __forceinline__ void epi_vec8_bf16(const Epi& e, long m, long n, cons
     uint4 gv;
     bf16* gp = (bf16*)&gv;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) gp[i] = __float2bfloat16_rn(gelu_f(__bfloat162float(op[i])));
+    for (int i = 0; i < 8; ++i) gp[i] = __float2bfloat16_rn(gelu_fast(__bfloat162float(op[i])));
     *(uint4*)((bf16*)e.out2 + m * e.ldo2 + n) = gv;
   }
 }
