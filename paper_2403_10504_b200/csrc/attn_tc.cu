@@ -102,6 +102,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
+// one lane of a converged warp: tcgen05.mma under this predicate issues back to back (see gemm_tc.cu)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // single MUFU.EX2 (exp2f adds denormal range fix-ups around it); ex2(-inf) = 0
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -140,6 +146,52 @@ __device__ __forceinline__ float exp2_poly(float x) {
   p = fmaf(p, f, 0.99992812f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// packed fp32 pairs (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// exp2_poly on a packed pair (same arithmetic, two lanes per instruction)
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float x0, x1;
+  f2unpack(x2, x0, x1);
+  x2 = f2pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const uint64_t magic = f2pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(x2, magic);
+  const uint64_t f = fsub2(x2, fsub2(t, magic));
+  uint64_t p = ffma2(f2pack(0.05517132f, 0.05517132f), f, f2pack(0.24261054f, 0.24261054f));
+  p = ffma2(p, f, f2pack(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, f2pack(0.99992812f, 0.99992812f));
+  float p0, p1, t0, t1;
+  f2unpack(p, p0, p1);
+  f2unpack(t, t0, t1);
+  return f2pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
 
 template <int DH>
 struct Cfg {
@@ -158,7 +210,7 @@ __global__ void __launch_bounds__(256, 1)
                        int h) {
   using C = Cfg<DH>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;
   uint8_t* sKV = sQ + C::Q_BYTES;  // stage s: K at sKV + s*KV_BYTES, V at + NP*PANEL
   uint8_t* sP = sKV + 2 * C::KV_BYTES;
@@ -400,8 +452,9 @@ __global__ void __launch_bounds__(384, 1)
                         int h) {
   using C = Cfg2<DH>;
   constexpr int NS = C::NSLOT;
+  constexpr int POLY = DH >= 128 ? 3 : 4;   // of 8 pairs: MUFU.EX2 and the tensor core both near their limits
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;                        // tile t at + t * NP * PANEL
   uint8_t* sR = sQ + C::Q_BYTES;           // ring slot s at + s * SLOT
   uint64_t* bars = (uint64_t*)(sR + NS * C::SLOT);
@@ -449,6 +502,8 @@ __global__ void __launch_bounds__(384, 1)
   fence_after();
   const uint32_t tbase = *tmem_slot;
 
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
@@ -471,18 +526,22 @@ __global__ void __launch_bounds__(384, 1)
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_bf16(128, BKV, false, false);  // S = Q K^T (both K-major)
     constexpr uint32_t id_o = idesc_bf16(128, DH, false, true);    // O += P V (P in TMEM, V MN-major)
+    const bool elected = elect_one();
+    const uint64_t dq0 = desc_sw128(smem_u32(sQ), 16, 1024);          // Q tiles, K-major
+    const uint64_t dk0 = desc_sw128(smem_u32(sR), 16, 1024);          // ring slots as K (K-major)
+    const uint64_t dv0 = desc_sw128(smem_u32(sR), C::PANEL, 1024);    // ring slots as V (MN-major)
     auto wait_pos = [&](int pos) {
       mbar_wait(&r_full[pos % NS], (pos / NS) & 1);
       fence_after();
     };
     auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T; K_j resident
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sQ + t * C::NP * C::PANEL), k = smem_u32(sR + ((2 * j) % NS) * C::SLOT);
+      if (elected) {
+        const uint64_t q = dq0 + (uint64_t)((t * C::NP * C::PANEL) >> 4);
+        const uint64_t k = dk0 + (uint64_t)((((2 * j) % NS) * C::SLOT) >> 4);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::PANEL + (kk & 3) * 32;
-          mma(tbase + C::S_COL + 128 * t, desc_sw128(q + off, 16, 1024), desc_sw128(k + off, 16, 1024), id_s,
-              kk > 0);
+          const uint32_t off = ((kk >> 2) * C::PANEL + (kk & 3) * 32) >> 4;
+          mma(tbase + C::S_COL + 128 * t, q + off, k + off, id_s, kk > 0);
         }
         commit(&s_full[t]);
       }
@@ -491,17 +550,17 @@ __global__ void __launch_bounds__(384, 1)
     auto issue_pv = [&](int t, int j) {   // O_t += P_t(j) V_j
       mbar_wait(&p_full[t], j & 1);
       fence_after();
-      if (lane == 0) {
-        const uint32_t v = smem_u32(sR + ((2 * j + 1) % NS) * C::SLOT);
+      if (elected) {
+        const uint64_t v = dv0 + (uint64_t)((((2 * j + 1) % NS) * C::SLOT) >> 4);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tbase + C::O_COL + 128 * t, tbase + C::S_COL + 128 * t + 8 * kk,
-                 desc_sw128(v + kk * 2048, C::PANEL, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tbase + C::O_COL + 128 * t, tbase + C::S_COL + 128 * t + 8 * kk, v + kk * 128, id_o,
+                 (j > 0 || kk > 0) ? 1u : 0u);
       }
       __syncwarp();
     };
     auto release = [&](int pos) {
-      if (lane == 0) commit(&r_empty[pos % NS]);
+      if (elected) commit(&r_empty[pos % NS]);
       __syncwarp();
     };
     mbar_wait(q_full, 0);
@@ -516,18 +575,20 @@ __global__ void __launch_bounds__(384, 1)
       if (j < nkb0) {
         issue_pv(0, j);
         if (j + 1 < nkb0) issue_s(0, j + 1);
-        else if (lane == 0) commit(&o_full[0]);
+        else if (elected) commit(&o_full[0]);
       }
       if (j < nkb1) {
         issue_pv(1, j);
         if (j + 1 < nkb1) issue_s(1, j + 1);
-        else if (lane == 0) commit(&o_full[1]);
+        else if (elected) commit(&o_full[1]);
       }
       __syncwarp();
       release(2 * j + 1);
       if (more) release(2 * j + 2);
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     // ------------------------------------------------------------ softmax, tile t
     const int t = (warp - 4) >> 2;
     const int qw = warp & 3;
@@ -547,24 +608,21 @@ __global__ void __launch_bounds__(384, 1)
       for (int c = 0; c < BKV; c += 32) tmem_ld32(s_addr + c, raw + c);
       tmem_wait_ld();
       const bool masked = j == qb || (j + 1) * BKV > T_;
-      float mx = -INFINITY;
       if (masked) {
 #pragma unroll
         for (int c = 0; c < BKV; ++c) {
           const int kj = j * BKV + c;
-          float v = __uint_as_float(raw[c]) * sc;
-          if (kj > qi || kj >= T_) v = -INFINITY;
-          raw[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) {
-          const float v = __uint_as_float(raw[c]) * sc;
-          raw[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
+          if (kj > qi || kj >= T_) raw[c] = __float_as_uint(-INFINITY);
         }
       }
+      // row max of the raw scores (sc > 0, so max and scaling commute), four independent chains
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BKV; c += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          m4[q] = fmaxf(m4[q], fmaxf(__uint_as_float(raw[c + 2 * q]), __uint_as_float(raw[c + 2 * q + 1])));
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sc;
       const bool need = mx > m_ref + RESCALE_THRESHOLD;
       const float new_ref = need ? mx : m_ref;
       const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
@@ -582,30 +640,39 @@ __global__ void __launch_bounds__(384, 1)
       }
       l *= alpha;
       m_ref = new_ref;
-      // P = 2^(S - m_ref) -> bf16 pairs into TMEM over S (16 columns = 32 keys at a time)
-      float rs = 0.f;
+      // P = 2^(raw sc - m_ref) on packed fp32 pairs -> bf16 pairs into TMEM over S (16 columns =
+      // 32 keys per store); POLY of every 8 pairs take the FMA-pipe exponential
+      const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(-m_ref, -m_ref);
+      uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int c16 = 0; c16 < BKV / 32; ++c16) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int c = c16 * 32 + 2 * i;
-          const float x0 = __uint_as_float(raw[c]) - m_ref, x1 = __uint_as_float(raw[c + 1]) - m_ref;
-          float p0, p1;
-          if (!masked && (i & 3) == 0) {   // 1 pair in 4 on the FMA pipe
-            p0 = exp2_poly(x0);
-            p1 = exp2_poly(x1);
+          const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[c]), __uint_as_float(raw[c + 1])), sc2, nref2);
+          uint64_t p2;
+          if (!masked && (i & 7) < POLY) {
+            p2 = exp2_poly2(x2);
           } else {
-            p0 = fast_exp2(x0);
-            p1 = fast_exp2(x1);
+            float x0, x1;
+            f2unpack(x2, x0, x1);
+            p2 = f2pack(fast_exp2(x0), fast_exp2(x1));
           }
-          rs += p0 + p1;
+          rs2[i & 3] = fadd2(rs2[i & 3], p2);
+          float p0, p1;
+          f2unpack(p2, p0, p1);
           __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
           pk[i] = *(uint32_t*)&v2;
         }
         tmem_st16(s_addr + 16 * c16, pk);
       }
-      l += rs;
+      {
+        const uint64_t r = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+        float r0, r1;
+        f2unpack(r, r0, r1);
+        l += r0 + r1;
+      }
       tmem_wait_st();
       fence_before();
       mbar_arrive(&p_full[t]);
@@ -680,7 +747,7 @@ __global__ void __launch_bounds__(256, 1)
                            const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
   using C = BCfg<DH>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
   uint8_t* sQD = sm + C::KV_BYTES;                 // stage s: Q at + s*QD_BYTES, dO at + NP*P64
@@ -889,7 +956,7 @@ __global__ void __launch_bounds__(256, 1)
                           const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
   using C = BCfg<DH>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;
   uint8_t* sO = sQ + C::NP * C::P128;
   uint8_t* sKV = sm + C::QO_BYTES;    // stage s: K at + s*KVS_BYTES, V at + NP*P64
@@ -1095,8 +1162,9 @@ __global__ void __launch_bounds__(384, 1)
                          const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
   using C = BCfg2<DH>;
   constexpr int NST = BW_NST;
+  constexpr int POLY = DH < 128;   // one pair in eight on the FMA pipe when the MMAs are short
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
   uint8_t* sS = sm + C::FIX;                           // stage s: Q at + s*STG, dO at + NP*P64
@@ -1165,12 +1233,12 @@ __global__ void __launch_bounds__(384, 1)
           tma_load(g + p * C::P64, &tm_do, &st_full[s], hh * DH + 64 * p, row0 + q0);
         }
       }
-      // queries beyond T_: L = +inf makes P (and so dS) exactly 0
+      // queries beyond T_: L = +inf makes P (and so dS) exactly 0 (the ring holds -L)
       float* L = sLD + 128 * s;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int qi = q0 + lane + 32 * e;
-        L[lane + 32 * e] = qi < T_ ? lrow[qi] * LOG2E : INFINITY;
+        L[lane + 32 * e] = qi < T_ ? -lrow[qi] * LOG2E : -INFINITY;   // stored negated
         L[64 + lane + 32 * e] = qi < T_ ? drow[qi] : 0.f;
       }
       mbar_arrive(&st_full[s]);
@@ -1179,19 +1247,22 @@ __global__ void __launch_bounds__(384, 1)
     constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
     constexpr uint32_t id_g = idesc_bf16(128, DH, false, true);    // dV += P^T dO, dK += dS^T Q
     mbar_wait(kv_full, 0);
+    const bool elected = elect_one();
+    const uint64_t dk = desc_sw128(smem_u32(sK), 16, 1024), dv = desc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t ds_k = desc_sw128(smem_u32(sS), 16, 1024);       // stage tiles, K-major
+    const uint64_t ds_mn = desc_sw128(smem_u32(sS), C::P64, 1024);  // stage tiles, MN-major
     auto issue_s = [&](int it) {
       const int s = it % NST, u = it & 1;
       mbar_wait(&st_full[s], (it / NST) & 1);
       fence_after();
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sS + s * C::STG), g = q + C::NP * C::P64;
-        const uint32_t k = smem_u32(sK), v = smem_u32(sV);
+      if (elected) {
+        const uint64_t q = ds_k + (uint64_t)((s * C::STG) >> 4), g = q + ((C::NP * C::P64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + C::ST_COL + 128 * u, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + C::DPT_COL + 128 * u, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s,
-              kk > 0);
+          const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
+          mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
+          mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
         }
         commit(&s_full[u]);
       }
@@ -1203,15 +1274,13 @@ __global__ void __launch_bounds__(384, 1)
       if (it + 1 < nblk) issue_s(it + 1);
       mbar_wait(&p_full[u], (it >> 1) & 1);
       fence_after();
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sS + s * C::STG), g = q + C::NP * C::P64;
+      if (elected) {
+        const uint64_t q = ds_mn + (uint64_t)((s * C::STG) >> 4), g = q + ((C::NP * C::P64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
           const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, desc_sw128(g + kk * 2048, C::P64, 1024),
-                 id_g, acc);
-          mma_ts(tbase + C::ACC1, tbase + C::DPT_COL + 128 * u + 8 * kk, desc_sw128(q + kk * 2048, C::P64, 1024),
-                 id_g, acc);
+          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, g + kk * 128, id_g, acc);
+          mma_ts(tbase + C::ACC1, tbase + C::DPT_COL + 128 * u + 8 * kk, q + kk * 128, id_g, acc);
         }
         commit(&st_empty[s]);
         if (it == nblk - 1) commit(done);
@@ -1236,26 +1305,38 @@ __global__ void __launch_bounds__(384, 1)
       const float* D = L + 64;
       const bool masked = q0 < k0 + 128;   // block straddles the diagonal
       uint32_t pk[16], dk[16];
+      const uint64_t sc2 = f2pack(sc, sc);
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 l4 = *(const float4*)(L + 4 * c4);
+        const float4 l4 = *(const float4*)(L + 4 * c4);   // -L
         const float4 d4 = *(const float4*)(D + 4 * c4);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd4[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pp[4], dd[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = 4 * c4 + e;
-          float p = fast_exp2(fmaf(__uint_as_float(sv[c]), sc, -lv[e]));
-          if (masked && q0 + 32 * wg + c < kj) p = 0.f;
-          pp[e] = p;
-          dd[e] = p * (__uint_as_float(dv[c]) - dd4[e]);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = 4 * c4 + 2 * h2;
+          const uint64_t nl2 = h2 ? f2pack(l4.z, l4.w) : f2pack(l4.x, l4.y);
+          const uint64_t d2 = h2 ? f2pack(d4.z, d4.w) : f2pack(d4.x, d4.y);
+          const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
+          uint64_t p2;
+          if (!masked && POLY && (c4 & 3) == 0 && h2 == 0) {
+            p2 = exp2_poly2(x2);
+          } else {
+            float x0, x1;
+            f2unpack(x2, x0, x1);
+            float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            if (masked) {
+              if (q0 + 32 * wg + c < kj) p0 = 0.f;
+              if (q0 + 32 * wg + c + 1 < kj) p1 = 0.f;
+            }
+            p2 = f2pack(p0, p1);
+          }
+          const uint64_t ds2 = fmul2(p2, fsub2(f2pack(__uint_as_float(dv[c]), __uint_as_float(dv[c + 1])), d2));
+          float p0, p1, g0, g1;
+          f2unpack(p2, p0, p1);
+          f2unpack(ds2, g0, g1);
+          __nv_bfloat162 a2 = __floats2bfloat162_rn(p0, p1), b2 = __floats2bfloat162_rn(g0, g1);
+          pk[2 * c4 + h2] = *(uint32_t*)&a2;
+          dk[2 * c4 + h2] = *(uint32_t*)&b2;
         }
-        __nv_bfloat162 a0 = __floats2bfloat162_rn(pp[0], pp[1]), a1 = __floats2bfloat162_rn(pp[2], pp[3]);
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(dd[0], dd[1]), b1 = __floats2bfloat162_rn(dd[2], dd[3]);
-        pk[2 * c4] = *(uint32_t*)&a0;
-        pk[2 * c4 + 1] = *(uint32_t*)&a1;
-        dk[2 * c4] = *(uint32_t*)&b0;
-        dk[2 * c4 + 1] = *(uint32_t*)&b1;
       }
       named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
       tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
@@ -1304,7 +1385,7 @@ __global__ void __launch_bounds__(384, 1)
   using C = BCfg2<DH>;
   constexpr int NST = BW_NST;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;
   uint8_t* sO = sQ + C::NP * C::P128;
   uint8_t* sS = sm + C::FIX;   // stage s: K_j at + s*STG, V_j at + NP*P64
@@ -1372,19 +1453,22 @@ __global__ void __launch_bounds__(384, 1)
     constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S = Q K^T, dP = dO V^T
     constexpr uint32_t id_q = idesc_bf16(128, DH, false, true);    // dQ += dS K
     mbar_wait(qo_full, 0);
+    const bool elected = elect_one();
+    const uint64_t dq = desc_sw128(smem_u32(sQ), 16, 1024), dg = desc_sw128(smem_u32(sO), 16, 1024);
+    const uint64_t ds_k = desc_sw128(smem_u32(sS), 16, 1024);       // stage tiles, K-major
+    const uint64_t ds_mn = desc_sw128(smem_u32(sS), C::P64, 1024);  // stage tiles, MN-major
     auto issue_s = [&](int j) {
       const int s = j % NST, u = j & 1;
       mbar_wait(&st_full[s], (j / NST) & 1);
       fence_after();
-      if (lane == 0) {
-        const uint32_t k = smem_u32(sS + s * C::STG), v = k + C::NP * C::P64;
-        const uint32_t q = smem_u32(sQ), g = smem_u32(sO);
+      if (elected) {
+        const uint64_t k = ds_k + (uint64_t)((s * C::STG) >> 4), v = k + ((C::NP * C::P64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + C::ST_COL + 128 * u, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + C::DPT_COL + 128 * u, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s,
-              kk > 0);
+          const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
+          mma(tbase + C::ST_COL + 128 * u, dq + oa, k + ob, id_s, kk > 0);
+          mma(tbase + C::DPT_COL + 128 * u, dg + oa, v + ob, id_s, kk > 0);
         }
         commit(&s_full[u]);
       }
@@ -1396,12 +1480,12 @@ __global__ void __launch_bounds__(384, 1)
       if (j + 1 < nblk) issue_s(j + 1);
       mbar_wait(&p_full[u], (j >> 1) & 1);
       fence_after();
-      if (lane == 0) {
-        const uint32_t k = smem_u32(sS + s * C::STG);
+      if (elected) {
+        const uint64_t k = ds_mn + (uint64_t)((s * C::STG) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)   // 64 keys = 4 x 16
-          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, desc_sw128(k + kk * 2048, C::P64, 1024),
-                 id_q, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tbase + C::ACC0, tbase + C::ST_COL + 128 * u + 8 * kk, k + kk * 128, id_q,
+                 (j > 0 || kk > 0) ? 1u : 0u);
         commit(&st_empty[s]);
         if (j == nblk - 1) commit(done);
       }
@@ -1425,19 +1509,28 @@ __global__ void __launch_bounds__(384, 1)
       const int kbase = j * 64 + 32 * wg;
       const bool masked = j * 64 + 63 > q0 || (j + 1) * 64 > T_;   // diagonal or ragged keys
       uint32_t dk[16];
+      const uint64_t sc2 = f2pack(sc, sc), nl2 = f2pack(-L, -L), d2 = f2pack(Dr, Dr);
 #pragma unroll
       for (int c2 = 0; c2 < 16; ++c2) {
-        float dd[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = 2 * c2 + e;
-          float p;
-          if (!masked && (c2 & 3) == 0) p = exp2_poly(fmaf(__uint_as_float(sv[c]), sc, -L));
-          else p = fast_exp2(fmaf(__uint_as_float(sv[c]), sc, -L));
-          if (masked && (kbase + c > qi || kbase + c >= T_)) p = 0.f;
-          dd[e] = p * (__uint_as_float(dv[c]) - Dr);
+        const int c = 2 * c2;
+        const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
+        uint64_t p2;
+        if (!masked && (c2 & 3) == 0) {
+          p2 = exp2_poly2(x2);
+        } else {
+          float x0, x1;
+          f2unpack(x2, x0, x1);
+          float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+          if (masked) {
+            if (kbase + c > qi || kbase + c >= T_) p0 = 0.f;
+            if (kbase + c + 1 > qi || kbase + c + 1 >= T_) p1 = 0.f;
+          }
+          p2 = f2pack(p0, p1);
         }
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(dd[0], dd[1]);
+        const uint64_t ds2 = fmul2(p2, fsub2(f2pack(__uint_as_float(dv[c]), __uint_as_float(dv[c + 1])), d2));
+        float g0, g1;
+        f2unpack(ds2, g0, g1);
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(g0, g1);
         dk[c2] = *(uint32_t*)&b2;
       }
       named_sync(1 + qw, 64);

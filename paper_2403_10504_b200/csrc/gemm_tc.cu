@@ -99,6 +99,14 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)2 << 61;
   return d;
 }
+// One lane of a converged warp (elect.sync). MMAs issued under this predicate compile to
+// back-to-back UTCHMMA; under `lane == 0` ptxas wraps every tcgen05.mma in its own
+// ELECT / BRA.U.ANY loop, which limited issue to ~100 cycles per MMA (tools/tmem_bw.cu).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(p));
+  return p != 0;
+}
 // Instruction descriptor, kind::f16: D fp32 (bit 4), A/B bf16 (bits 7, 10), major bits 15/16,
 // N>>3 at bit 17, M>>4 at bit 24.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(256, 1)
                    int K, Epi epi) {
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
@@ -216,6 +224,11 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    const bool elected = elect_one();
+    // stage-0 descriptors; stage s and K step kk only add constants to the address field
+    const uint64_t a_desc0 = A_MN ? desc_sw128(smem_u32(smem), 8192, 1024) : desc_sw128(smem_u32(smem), 16, 1024);
+    const uint64_t b_desc0 = B_MN ? desc_sw128(smem_u32(smem) + Cfg::A_BYTES, 8192, 1024)
+                                  : desc_sw128(smem_u32(smem) + Cfg::A_BYTES, 16, 1024);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -228,13 +241,12 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint32_t sb = sa + Cfg::A_BYTES;
+        if (elected) {
+          const uint64_t sofs = (uint64_t)((stage * Cfg::STAGE_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? desc_sw128(sa + kk * 2048, 8192, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t bd = B_MN ? desc_sw128(sb + kk * 2048, 8192, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
+            const uint64_t ad = a_desc0 + sofs + (A_MN ? kk * 128 : kk * 2);
+            const uint64_t bd = b_desc0 + sofs + (B_MN ? kk * 128 : kk * 2);
             tc_mma(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
@@ -352,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   using Cfg = Tc2Cfg;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
@@ -438,6 +450,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------------------------------------------------------- MMA issuer (leader only)
     if (leader) {
       constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, A_MN, B_MN);
+      const bool elected = elect_one();
+      const uint64_t a_desc0 =
+          A_MN ? desc_sw128(smem_u32(smem), 8192, 1024) : desc_sw128(smem_u32(smem), 16, 1024);
+      const uint64_t b_desc0 = B_MN ? desc_sw128(smem_u32(smem) + Cfg::A_BYTES, 8192, 1024)
+                                    : desc_sw128(smem_u32(smem) + Cfg::A_BYTES, 16, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -450,15 +467,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-            const uint32_t sb = sa + Cfg::A_BYTES;
+          if (elected) {
+            const uint64_t sofs = (uint64_t)((stage * Cfg::STAGE_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t ad =
-                  A_MN ? desc_sw128(sa + kk * 2048, 8192, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
-              const uint64_t bd =
-                  B_MN ? desc_sw128(sb + kk * 2048, 8192, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
+              const uint64_t ad = a_desc0 + sofs + (A_MN ? kk * 128 : kk * 2);
+              const uint64_t bd = b_desc0 + sofs + (B_MN ? kk * 128 : kk * 2);
               tc_mma_pair(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
             }
             tc_commit_pair(&empty[stage]);
