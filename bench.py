@@ -160,6 +160,24 @@ def run_reference(args, g, wl_desc):
     print(json.dumps(line), flush=True)
 
 
+def compute_busy_pct(trace, step_ms):
+    """Share of the last step's device time in which the compute lane runs an op (union of the
+    traced compute-lane intervals): what is left is the compute stream waiting on swaps."""
+    iv = sorted((float(f[5]), float(f[6])) for f in (l.split() for l in trace.splitlines())
+                if len(f) >= 7 and f[0] == "compute")
+    busy, cur_s, cur_e = 0.0, None, None
+    for a, b in iv:
+        if cur_e is None or a > cur_e:
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    if cur_e is not None:
+        busy += cur_e - cur_s
+    return 100.0 * busy / 1000.0 / step_ms if step_ms else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -263,6 +281,7 @@ def main():
             "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
                               "flops_per_token": f_alg_per_token(g)},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
+            "compute_busy_pct": compute_busy_pct(peer.trace(), st["step_ms"]),
             "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
             "loss_first_last": [losses[0], losses[-1]],
             "clocks": clk.summary(),

@@ -13,6 +13,7 @@
 // Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
 #include <cuda.h>
 #include <stdlib.h>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -452,7 +453,9 @@ __global__ void __launch_bounds__(384, 1)
                         int h) {
   using C = Cfg2<DH>;
   constexpr int NS = C::NSLOT;
-  constexpr int POLY = DH >= 128 ? 3 : 4;   // of 8 pairs: MUFU.EX2 and the tensor core both near their limits
+  // of 8 pairs on the FMA pipe: MUFU.EX2 (16/clk/SM) keeps pace with the MMAs at d_h = 128 but
+  // not with the shorter MMAs of d_h = 80 / 64
+  constexpr int POLY = DH >= 128 ? 0 : (DH >= 80 ? 1 : 2);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;                        // tile t at + t * NP * PANEL
@@ -641,38 +644,41 @@ __global__ void __launch_bounds__(384, 1)
       l *= alpha;
       m_ref = new_ref;
       // P = 2^(raw sc - m_ref) on packed fp32 pairs -> bf16 pairs into TMEM over S (16 columns =
-      // 32 keys per store); POLY of every 8 pairs take the FMA-pipe exponential
+      // 32 keys per store). Unmasked blocks send POLY of every 8 pairs to the FMA-pipe exponential;
+      // the two variants are separate code paths (a shared, predicated loop issued both).
       const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(-m_ref, -m_ref);
-      uint64_t rs2[4] = {0, 0, 0, 0};
+      auto p_block = [&](auto use_poly) {
+        uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int c16 = 0; c16 < BKV / 32; ++c16) {
-        uint32_t pk[16];
+        for (int c16 = 0; c16 < BKV / 32; ++c16) {
+          uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int c = c16 * 32 + 2 * i;
-          const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[c]), __uint_as_float(raw[c + 1])), sc2, nref2);
-          uint64_t p2;
-          if (!masked && (i & 7) < POLY) {
-            p2 = exp2_poly2(x2);
-          } else {
-            float x0, x1;
-            f2unpack(x2, x0, x1);
-            p2 = f2pack(fast_exp2(x0), fast_exp2(x1));
+          for (int i = 0; i < 16; ++i) {
+            const int c = c16 * 32 + 2 * i;
+            const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[c]), __uint_as_float(raw[c + 1])), sc2, nref2);
+            uint64_t p2;
+            if (decltype(use_poly)::value && (i & 7) < POLY) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              f2unpack(x2, x0, x1);
+              p2 = f2pack(fast_exp2(x0), fast_exp2(x1));
+            }
+            rs2[i & 3] = fadd2(rs2[i & 3], p2);
+            float p0, p1;
+            f2unpack(p2, p0, p1);
+            __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+            pk[i] = *(uint32_t*)&v2;
           }
-          rs2[i & 3] = fadd2(rs2[i & 3], p2);
-          float p0, p1;
-          f2unpack(p2, p0, p1);
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-          pk[i] = *(uint32_t*)&v2;
+          tmem_st16(s_addr + 16 * c16, pk);
         }
-        tmem_st16(s_addr + 16 * c16, pk);
-      }
-      {
         const uint64_t r = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
         float r0, r1;
         f2unpack(r, r0, r1);
-        l += r0 + r1;
-      }
+        return r0 + r1;
+      };
+      if (POLY == 0 || masked) l += p_block(std::false_type{});
+      else l += p_block(std::true_type{});
       tmem_wait_st();
       fence_before();
       mbar_arrive(&p_full[t]);
@@ -682,24 +688,25 @@ __global__ void __launch_bounds__(384, 1)
       fence_after();
       const float inv = 1.f / l;
       bf16* orow = o + ((long)b * T_ + qi) * d + hh * DH;
+      uint32_t ov[DH];   // all loads in flight, one wait
 #pragma unroll
-      for (int c = 0; c < DH; c += 16) {
-        uint32_t ov[16];
-        tmem_ld16(o_addr + c, ov);
-        tmem_wait_ld();
-        if (qi < T_) {
+      for (int c = 0; c < DH; c += 16) tmem_ld16(o_addr + c, ov + c);
+      tmem_wait_ld();
+      if (qi < T_) {
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            __nv_bfloat162 v2 =
-                __floats2bfloat162_rn(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
+            __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(ov[c + 2 * i]) * inv,
+                                                      __uint_as_float(ov[c + 2 * i + 1]) * inv);
             pk[i] = *(uint32_t*)&v2;
           }
           *(uint4*)(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *(uint4*)(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
+        lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
       }
-      if (qi < T_) lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
     }
   }
   fence_before();
@@ -1351,17 +1358,18 @@ __global__ void __launch_bounds__(384, 1)
     const float scale = wg ? rsqrtf((float)DH) : 1.f;
     bf16* row = dqkv + ((long)row0 + kj) * 3 * d + (wg ? d : 2 * d) + hh * DH;
     const uint32_t acc = la + (wg ? C::ACC1 : C::ACC0);
+    uint32_t gv[DH];   // all loads in flight, one wait
 #pragma unroll
-    for (int c = 0; c < DH; c += 16) {
-      uint32_t gv[16];
-      tmem_ld16(acc + c, gv);
-      tmem_wait_ld();
-      if (kj < T_) {
+    for (int c = 0; c < DH; c += 16) tmem_ld16(acc + c, gv + c);
+    tmem_wait_ld();
+    if (kj < T_) {
+#pragma unroll
+      for (int c = 0; c < DH; c += 16) {
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 v2 =
-              __floats2bfloat162_rn(__uint_as_float(gv[2 * i]) * scale, __uint_as_float(gv[2 * i + 1]) * scale);
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(gv[c + 2 * i]) * scale,
+                                                    __uint_as_float(gv[c + 2 * i + 1]) * scale);
           pk[i] = *(uint32_t*)&v2;
         }
         *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -1545,23 +1553,29 @@ __global__ void __launch_bounds__(384, 1)
     const float isq = rsqrtf((float)DH);
     bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
     constexpr int HALF = ((DH / 16) + 1) / 2 * 16;   // 64 / 48 / 32 columns for warpgroup 0
-    const int c_lo = wg ? HALF : 0, c_hi = wg ? DH : HALF;
-    for (int c = c_lo; c < c_hi; c += 16) {
-      uint32_t gq[16];
-      tmem_ld16(la + C::ACC0 + c, gq);
+    auto store_cols = [&](auto lo_c, auto hi_c) {   // columns [lo, hi): loads in flight, one wait
+      constexpr int LO = decltype(lo_c)::value, HI = decltype(hi_c)::value;
+      uint32_t gq[HI - LO];
+#pragma unroll
+      for (int c = LO; c < HI; c += 16) tmem_ld16(la + C::ACC0 + c, gq + (c - LO));
       tmem_wait_ld();
       if (qi < T_) {
-        uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 q2 =
-              __floats2bfloat162_rn(__uint_as_float(gq[2 * i]) * isq, __uint_as_float(gq[2 * i + 1]) * isq);
-          pk[i] = *(uint32_t*)&q2;
+        for (int c = LO; c < HI; c += 16) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            __nv_bfloat162 q2 = __floats2bfloat162_rn(__uint_as_float(gq[c - LO + 2 * i]) * isq,
+                                                      __uint_as_float(gq[c - LO + 2 * i + 1]) * isq);
+            pk[i] = *(uint32_t*)&q2;
+          }
+          *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
-        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
-    }
+    };
+    if (wg) store_cols(std::integral_constant<int, HALF>{}, std::integral_constant<int, DH>{});
+    else store_cols(std::integral_constant<int, 0>{}, std::integral_constant<int, HALF>{});
   }
   fence_before();
   __syncthreads();
