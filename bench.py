@@ -161,8 +161,10 @@ def run_reference(args, g, wl_desc):
 
 
 def compute_busy_pct(trace, step_ms):
-    """Share of the last step's device time in which the compute lane runs an op (union of the
-    traced compute-lane intervals): what is left is the compute stream waiting on swaps."""
+    """Share of the compute lane's span in the last step (its first op start -> last op end) in
+    which it runs an op (union of the traced intervals): what is left is the compute stream waiting
+    on swaps. (The step's first prefetch loads start during the previous step, so the whole-trace
+    span is longer than the step.)"""
     iv = sorted((float(f[5]), float(f[6])) for f in (l.split() for l in trace.splitlines())
                 if len(f) >= 7 and f[0] == "compute")
     busy, cur_s, cur_e = 0.0, None, None
@@ -175,7 +177,8 @@ def compute_busy_pct(trace, step_ms):
             cur_e = max(cur_e, b)
     if cur_e is not None:
         busy += cur_e - cur_s
-    return 100.0 * busy / 1000.0 / step_ms if step_ms else None
+    span = max(b for _, b in iv) - iv[0][0] if iv else 0.0
+    return 100.0 * busy / span if span > 0 else None
 
 
 def main():
@@ -187,6 +190,7 @@ def main():
     ap.add_argument("--impl", default="atom", choices=["atom", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--link-gbs", type=float, default=BIDIR_GBS)
+    ap.add_argument("--trace-out", default="", help="write the last step's per-op trace here (rank 0)")
     args = ap.parse_args()
     cfg_name, state_cap, wl_desc = WORKLOADS[args.config]
     g = synth.CONFIGS[cfg_name]
@@ -256,6 +260,10 @@ def main():
     ms_step = ms / args.steps
     t_roof = max(tok_step * f_alg_per_token(g) / (pk["bf16_tflops"] * 1e12),
                  14 * synth.n_params(g) / (H2D_GBS * 1e9), 12 * synth.n_params(g) / (D2H_GBS * 1e9))
+    trace = peer.trace()
+    if rank == 0 and args.trace_out:
+        with open(args.trace_out, "w") as f:
+            f.write(trace)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -281,7 +289,7 @@ def main():
             "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
                               "flops_per_token": f_alg_per_token(g)},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
-            "compute_busy_pct": compute_busy_pct(peer.trace(), st["step_ms"]),
+            "compute_busy_pct": compute_busy_pct(trace, st["step_ms"]),
             "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
             "loss_first_last": [losses[0], losses[-1]],
             "clocks": clk.summary(),

@@ -117,6 +117,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -126,6 +130,24 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
       "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
       "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+// A-operand rows into TMEM: thread = lane = row, DH bf16 of `src` (or zeros) as DH / 2 columns
+template <int DH>
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const bf16* src, bool valid) {
+  uint32_t v[DH / 2];
+#pragma unroll
+  for (int c = 0; c < DH / 8; ++c) {
+    const uint4 q = valid ? *(const uint4*)(src + 8 * c) : make_uint4(0, 0, 0, 0);
+    v[4 * c] = q.x;
+    v[4 * c + 1] = q.y;
+    v[4 * c + 2] = q.z;
+    v[4 * c + 3] = q.w;
+  }
+#pragma unroll
+  for (int c = 0; c < DH / 2; c += 16) {
+    if (c + 16 <= DH / 2) tmem_st16(taddr + c, v + c);
+    else tmem_st8(taddr + c, v + c);
+  }
 }
 // D[tmem] (+)= A[tmem] * B[smem]: A is M x 16 bf16 at lanes 0..M-1, 8 columns (two bf16 per
 // 32-bit column, even k in the low half) -- the "TS" form of tcgen05.mma.
@@ -435,7 +457,7 @@ __global__ void __launch_bounds__(256, 1)
 // the commit that publishes S_t(j+1) also certifies that PV_t(j) finished (O_t is stable for
 // the lazy rescale).
 // ======================================================================================
-template <int DH>
+template <int DH, bool TSA_ = false>
 struct Cfg2 {
   static constexpr int NP = (DH + 63) / 64;
   static constexpr int PANEL = 128 * 128;
@@ -445,13 +467,17 @@ struct Cfg2 {
   static constexpr int NSLOT = NSLOT_FIT > 8 ? 8 : NSLOT_FIT;
   static constexpr int SMEM = Q_BYTES + NSLOT * SLOT + 1024 + 512;
   static constexpr uint32_t S_COL = 0, O_COL = 256;  // tile t: S/P at 128t, O at 256 + 128t
+  // d_h <= 80: Q_t lives in TMEM after O_t and S = Q K^T is a TS MMA (no smem A reads)
+  static constexpr bool TSA = TSA_ && DH <= 80;
+  static constexpr uint32_t Q_COL = O_COL + (DH + 15) / 16 * 16;   // tile t: + 128t
+  static_assert(!TSA || Q_COL + 128 + DH / 2 <= 512, "TMEM budget");
 };
 
-template <int DH>
+template <int DH, bool TSA>
 __global__ void __launch_bounds__(384, 1)
-    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, float* __restrict__ lse, int T_,
-                        int h) {
-  using C = Cfg2<DH>;
+    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, const bf16* __restrict__ qkv, bf16* __restrict__ o,
+                        float* __restrict__ lse, int T_, int h) {
+  using C = Cfg2<DH, TSA>;
   constexpr int NS = C::NSLOT;
   // of 8 pairs on the FMA pipe: MUFU.EX2 (16/clk/SM) keeps pace with the MMAs at d_h = 128 but
   // not with the shorter MMAs of d_h = 80 / 64
@@ -483,7 +509,7 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = b * T_;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    mbar_init(q_full, C::TSA ? 256 : 1);   // TSA: the softmax threads store their Q rows into TMEM
     for (int s = 0; s < NS; ++s) {
       mbar_init(&r_full[s], 1);
       mbar_init(&r_empty[s], 1);
@@ -511,10 +537,12 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
       const int ntile = nkb1 > 0 ? 2 : 1;
-      mbar_expect_tx(q_full, ntile * C::NP * C::PANEL);
-      for (int t = 0; t < ntile; ++t)
-        for (int p = 0; p < C::NP; ++p)
-          tma_load(sQ + (t * C::NP + p) * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + (qb0 + t) * BQ);
+      if (!C::TSA) {
+        mbar_expect_tx(q_full, ntile * C::NP * C::PANEL);
+        for (int t = 0; t < ntile; ++t)
+          for (int p = 0; p < C::NP; ++p)
+            tma_load(sQ + (t * C::NP + p) * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + (qb0 + t) * BQ);
+      }
       // ring positions: K_j at 2j, V_j at 2j + 1
       for (int pos = 0; pos < 2 * nkb; ++pos) {
         const int s = pos % NS, use = pos / NS, j = pos >> 1;
@@ -544,7 +572,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = ((kk >> 2) * C::PANEL + (kk & 3) * 32) >> 4;
-          mma(tbase + C::S_COL + 128 * t, q + off, k + off, id_s, kk > 0);
+          if constexpr (C::TSA) mma_ts(tbase + C::S_COL + 128 * t, tbase + C::Q_COL + 128 * t + 8 * kk, k + off, id_s, kk > 0);
+          else mma(tbase + C::S_COL + 128 * t, q + off, k + off, id_s, kk > 0);
         }
         commit(&s_full[t]);
       }
@@ -602,6 +631,12 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_addr = tbase + ((uint32_t)(32 * qw) << 16);
     const uint32_t s_addr = lane_addr + C::S_COL + 128 * t, o_addr = lane_addr + C::O_COL + 128 * t;
     const float sc = rsqrtf((float)DH) * LOG2E;
+    if constexpr (C::TSA) {   // this thread's Q row into TMEM (zeros beyond T_)
+      row_to_tmem<DH>(lane_addr + C::Q_COL + 128 * t, qkv + ((long)row0 + qi) * 3 * d + hh * DH, qi < T_);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(q_full);
+    }
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < my_nkb; ++j) {
       mbar_wait(&s_full[t], j & 1);
@@ -1152,22 +1187,31 @@ __global__ void __launch_bounds__(256, 1)
 // ======================================================================================
 constexpr int BW_NST = 4;   // ring stages
 
-template <int DH>
+template <int DH, bool TSA_ = false>
 struct BCfg2 {
   static constexpr int NP = (DH + 63) / 64;
   static constexpr int P128 = 128 * 128, P64 = 64 * 128;
   static constexpr int FIX = 2 * NP * P128;          // K,V (dK/dV kernel) or Q,dO (dQ kernel)
   static constexpr int STG = 2 * NP * P64;           // Q_i,dO_i or K_j,V_j: 64 rows each
   static constexpr int SMEM = FIX + BW_NST * STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
-  static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256, ACC1 = 384;   // buffer u: +128u
+  // d_h <= 80: the per-CTA fixed operands (K, V or Q, dO) live in TMEM as A operands of S / dP
+  // (TS MMAs: no shared-memory A reads, which bound the SS MMAs); d_h = 128 has no TMEM room
+  static constexpr bool TSA = TSA_ && DH <= 80;
+  static constexpr uint32_t AL16(uint32_t x) { return (x + 15) / 16 * 16; }
+  static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256;   // buffer u: +128u
+  static constexpr uint32_t FA_COL = ACC0 + AL16(DH);               // fixed operand A (K or Q)
+  static constexpr uint32_t FB_COL = FA_COL + AL16(DH / 2);         // fixed operand B (V or dO)
+  static constexpr uint32_t ACC1 = TSA ? FB_COL + AL16(DH / 2) : 384;
+  static_assert(!TSA || ACC1 + DH <= 512, "TMEM budget");
 };
 
-template <int DH>
+template <int DH, bool TSA>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
-                         const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
-  using C = BCfg2<DH>;
+                         const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ qkv,
+                         const float* __restrict__ lse, const float* __restrict__ Dsum, bf16* __restrict__ dqkv,
+                         int T_, int h) {
+  using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   constexpr int POLY = DH < 128;   // one pair in eight on the FMA pipe when the MMAs are short
   extern __shared__ uint8_t smem_raw[];
@@ -1196,7 +1240,7 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = b * T_;
 
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1);
+    mbar_init(kv_full, C::TSA ? 256 : 1);   // TSA: the elementwise threads store K, V rows into TMEM
     for (int s = 0; s < NST; ++s) {
       mbar_init(&st_full[s], 33);
       mbar_init(&st_empty[s], 1);
@@ -1221,7 +1265,7 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     const float* lrow = lse + ((long)b * h + hh) * T_;
     const float* drow = Dsum + ((long)b * h + hh) * T_;
-    if (lane == 0) {
+    if (!C::TSA && lane == 0) {
       mbar_expect_tx(kv_full, C::FIX);
       for (int p = 0; p < C::NP; ++p) {
         tma_load(sK + p * C::P128, &tm_kv, kv_full, d + hh * DH + 64 * p, row0 + k0);
@@ -1268,8 +1312,13 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
           const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
-          mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
-          mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
+          if constexpr (C::TSA) {
+            mma_ts(tbase + C::ST_COL + 128 * u, tbase + C::FA_COL + 8 * kk, q + ob, id_s, kk > 0);
+            mma_ts(tbase + C::DPT_COL + 128 * u, tbase + C::FB_COL + 8 * kk, g + ob, id_s, kk > 0);
+          } else {
+            mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
+            mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
+          }
         }
         commit(&s_full[u]);
       }
@@ -1299,6 +1348,13 @@ __global__ void __launch_bounds__(384, 1)
     const int r = 32 * qw + lane, kj = k0 + r;
     const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
     const float sc = rsqrtf((float)DH) * LOG2E;
+    if constexpr (C::TSA) {   // K row (warpgroup 0) / V row (warpgroup 1) of this thread's key
+      row_to_tmem<DH>(la + (wg ? C::FB_COL : C::FA_COL),
+                      qkv + ((long)row0 + kj) * 3 * d + (wg ? 2 * d : d) + hh * DH, kj < T_);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(kv_full);
+    }
     for (int it = 0; it < nblk; ++it) {
       const int s = it % NST, u = it & 1, q0 = (i0 + it) * 64;
       mbar_wait(&st_full[s], (it / NST) & 1);   // L / D of this stage visible
@@ -1385,12 +1441,13 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int DH>
+template <int DH, bool TSA>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                        const __grid_constant__ CUtensorMap tm_kv, const float* __restrict__ lse,
+                        const __grid_constant__ CUtensorMap tm_kv, const bf16* __restrict__ qkv,
+                        const bf16* __restrict__ dout, const float* __restrict__ lse,
                         const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
-  using C = BCfg2<DH>;
+  using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
@@ -1416,7 +1473,7 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = b * T_;
 
   if (threadIdx.x == 0) {
-    mbar_init(qo_full, 1);
+    mbar_init(qo_full, C::TSA ? 256 : 1);   // TSA: the elementwise threads store Q, dO rows into TMEM
     for (int s = 0; s < NST; ++s) {
       mbar_init(&st_full[s], 1);
       mbar_init(&st_empty[s], 1);
@@ -1440,10 +1497,12 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(qo_full, C::FIX);
-      for (int p = 0; p < C::NP; ++p) {
-        tma_load(sQ + p * C::P128, &tm_q, qo_full, hh * DH + 64 * p, row0 + q0);
-        tma_load(sO + p * C::P128, &tm_do, qo_full, hh * DH + 64 * p, row0 + q0);
+      if (!C::TSA) {
+        mbar_expect_tx(qo_full, C::FIX);
+        for (int p = 0; p < C::NP; ++p) {
+          tma_load(sQ + p * C::P128, &tm_q, qo_full, hh * DH + 64 * p, row0 + q0);
+          tma_load(sO + p * C::P128, &tm_do, qo_full, hh * DH + 64 * p, row0 + q0);
+        }
       }
       for (int j = 0; j < nblk; ++j) {
         const int s = j % NST;
@@ -1475,8 +1534,13 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
           const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
-          mma(tbase + C::ST_COL + 128 * u, dq + oa, k + ob, id_s, kk > 0);
-          mma(tbase + C::DPT_COL + 128 * u, dg + oa, v + ob, id_s, kk > 0);
+          if constexpr (C::TSA) {
+            mma_ts(tbase + C::ST_COL + 128 * u, tbase + C::FA_COL + 8 * kk, k + ob, id_s, kk > 0);
+            mma_ts(tbase + C::DPT_COL + 128 * u, tbase + C::FB_COL + 8 * kk, v + ob, id_s, kk > 0);
+          } else {
+            mma(tbase + C::ST_COL + 128 * u, dq + oa, k + ob, id_s, kk > 0);
+            mma(tbase + C::DPT_COL + 128 * u, dg + oa, v + ob, id_s, kk > 0);
+          }
         }
         commit(&s_full[u]);
       }
@@ -1506,6 +1570,14 @@ __global__ void __launch_bounds__(384, 1)
     const float sc = rsqrtf((float)DH) * LOG2E;
     const float L = qi < T_ ? lse[((long)b * h + hh) * T_ + qi] * LOG2E : INFINITY;
     const float Dr = qi < T_ ? Dsum[((long)b * h + hh) * T_ + qi] : 0.f;
+    if constexpr (C::TSA) {   // Q row (warpgroup 0) / dO row (warpgroup 1) of this thread's query
+      row_to_tmem<DH>(la + (wg ? C::FB_COL : C::FA_COL),
+                      wg ? dout + ((long)row0 + qi) * d + hh * DH : qkv + ((long)row0 + qi) * 3 * d + hh * DH,
+                      qi < T_);
+      tmem_wait_st();
+      fence_before();
+      mbar_arrive(qo_full);
+    }
     for (int j = 0; j < nblk; ++j) {
       const int u = j & 1;
       mbar_wait(&s_full[u], (j >> 1) & 1);
@@ -1608,6 +1680,15 @@ __global__ void dsum_tc_kernel(const bf16* __restrict__ o, const bf16* __restric
   Dsum[(b * h + hh) * T_ + t] = s;
 }
 
+// Fixed MMA operands in TMEM (TS MMAs, d_h <= 80) per kernel: bit 0 forward Q, bit 1 dK/dV K,V,
+// bit 2 dQ Q,dO. Default: dQ only (measured: it helps the dQ kernel, slows the other two).
+// ATOM_ATTN_TSA=<mask> overrides for A/B runs.
+static bool tsa_mask(int bit) {
+  const char* e = getenv("ATOM_ATTN_TSA");
+  const int m = e ? atoi(e) : 4;
+  return (m >> bit) & 1;
+}
+
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1645,12 +1726,16 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
   }
   static bool once = false;
   static bool v1 = false;   // ATOM_ATTN_FWD_V1=1: the one-tile kernel (A/B comparisons)
+  static bool tsa = false;
   if (!once) {
     const char* e = getenv("ATOM_ATTN_FWD_V1");
     v1 = e && e[0] == '1';
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cfg2<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg2<DH>::SMEM));
+    tsa = tsa_mask(0);
     once = true;
   }
   if (v1) {
@@ -1658,7 +1743,8 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
     attn_fwd_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tm, o, lse, T_, h);
   } else {
     dim3 grid((T_ + 2 * BQ - 1) / (2 * BQ), B * h);
-    attn_fwd2_tc_kernel<DH><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, o, lse, T_, h);
+    if (tsa) attn_fwd2_tc_kernel<DH, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
+    else attn_fwd2_tc_kernel<DH, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
   }
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
@@ -1695,6 +1781,7 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     return false;
   static bool once = false;
   static bool v1 = false;   // ATOM_ATTN_BWD_V1=1: the first-generation kernels (A/B comparisons)
+  static bool tsa_kv = false, tsa_q = false;
   if (!once) {
     const char* e = getenv("ATOM_ATTN_BWD_V1");
     v1 = e && e[0] == '1';
@@ -1702,10 +1789,16 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
                                       C::SMEM_KV));
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_Q));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       BCfg2<DH>::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       BCfg2<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg2<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg2<DH>::SMEM));
+    tsa_kv = tsa_mask(1);
+    tsa_q = tsa_mask(2);
     once = true;
   }
   const long nthr = rows * h;
@@ -1718,9 +1811,19 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
     count_launch();
   } else {
-    attn_bwd_dkv2_kernel<DH><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
+    if (tsa_kv)
+      attn_bwd_dkv2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
+                                                                        T_, h);
+    else
+      attn_bwd_dkv2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
+                                                                         T_, h);
     count_launch();
-    attn_bwd_dq2_kernel<DH><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
+    if (tsa_q)
+      attn_bwd_dq2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
+                                                                       dqkv, T_, h);
+    else
+      attn_bwd_dq2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
+                                                                        dqkv, T_, h);
     count_launch();
   }
   ATOM_CUDA_OK(cudaGetLastError());

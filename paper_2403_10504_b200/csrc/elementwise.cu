@@ -171,66 +171,99 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
   }
 }
 
-// Column partial sums over chunks of RED_ROWS rows (fixed order):
-//   mode 0: part0[c][j] = sum_r a[r][j]                  (bias gradient: sum of dY over tokens)
-//   mode 1: part0[c][j] = sum_r a[r][j] * xhat[r][j], part1[c][j] = sum_r a[r][j]   (LN gain / shift)
-// Each thread owns one 16-byte vector of columns (8 bf16 / 4 fp32); ncols % VW == 0. Rows are
-// loaded CP_UNR at a time (several 16-byte loads in flight per thread: the kernel is HBM-bound
-// and a one-load-at-a-time loop ran at ~1.4 TB/s), then added in ascending row order.
-constexpr int CP_UNR = 8;
+// Column sums over rows in a fixed order (bias gradients, LN gain / shift gradients):
+//   mode 0: out0[j] += sum_r a[r][j]
+//   mode 1: out0[j] += sum_r a[r][j] * xhat[r][j],  out1[j] += sum_r a[r][j]
+// One CTA per (column block of 128 x VW columns, chunk of RED_ROWS rows); its four thread groups
+// sum 32 rows each (CP_UNR 16-byte loads in flight per thread), combined in group order into one
+// partial per chunk. The last CTA of a column block to finish (atomic ticket; the ticket only
+// picks who, never the order) adds the chunk partials in chunk order and resets the ticket.
+constexpr int CP_UNR = 8, CP_GROUPS = 4, CP_GROWS = RED_ROWS / CP_GROUPS;
 template <typename T, int MODE>
-__global__ void __launch_bounds__(128) col_partials_kernel(const T* __restrict__ a, long lda, const T* __restrict__ x,
-                                                           const float* __restrict__ stats, long rows, int ncols,
-                                                           float* __restrict__ part0, float* __restrict__ part1) {
+__global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __restrict__ a, long lda,
+                                                                   const T* __restrict__ x,
+                                                                   const float* __restrict__ stats, long rows,
+                                                                   int ncols, float* __restrict__ part0,
+                                                                   float* __restrict__ part1, float* __restrict__ out0,
+                                                                   float* __restrict__ out1, int* __restrict__ ticket) {
   constexpr int VW = Vec<T>::N;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) * VW;
-  const int c = blockIdx.y;
-  if (j >= ncols) return;
-  const long r0 = (long)c * RED_ROWS, r1 = min(rows, r0 + RED_ROWS);
+  __shared__ float sh[CP_GROUPS][MODE == 1 ? 2 : 1][128 * VW];
+  __shared__ int last;
+  const int tx = threadIdx.x, g = threadIdx.y;
+  const int j = (blockIdx.x * 128 + tx) * VW;
+  const int c = blockIdx.y, nch = gridDim.y;
   float s0[VW], s1[VW];
 #pragma unroll
   for (int i = 0; i < VW; ++i) s0[i] = s1[i] = 0.f;
-  for (long rb = r0; rb < r1; rb += CP_UNR) {
-    float v[CP_UNR][VW], xv[MODE == 1 ? CP_UNR : 1][VW];
+  if (j < ncols) {
+    const long r0 = (long)c * RED_ROWS + g * CP_GROWS, r1 = min(rows, r0 + CP_GROWS);
+    for (long rb = r0; rb < r1; rb += CP_UNR) {
+      float v[CP_UNR][VW], xv[MODE == 1 ? CP_UNR : 1][VW];
 #pragma unroll
-    for (int u = 0; u < CP_UNR; ++u) {
-      if (rb + u < r1) {
-        load_vec<T>(a + (rb + u) * lda + j, v[u]);
-        if constexpr (MODE == 1) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
+      for (int u = 0; u < CP_UNR; ++u) {
+        if (rb + u < r1) {
+          load_vec<T>(a + (rb + u) * lda + j, v[u]);
+          if constexpr (MODE == 1) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < CP_UNR; ++u) {
-      if (rb + u < r1) {
-        if constexpr (MODE == 1) {
-          const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
+      for (int u = 0; u < CP_UNR; ++u) {
+        if (rb + u < r1) {
+          if constexpr (MODE == 1) {
+            const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
 #pragma unroll
-          for (int i = 0; i < VW; ++i) {
-            s0[i] = fmaf(v[u][i], (xv[u][i] - mean) * rstd, s0[i]);
-            s1[i] += v[u][i];
+            for (int i = 0; i < VW; ++i) {
+              s0[i] = fmaf(v[u][i], (xv[u][i] - mean) * rstd, s0[i]);
+              s1[i] += v[u][i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < VW; ++i) s0[i] += v[u][i];
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < VW; ++i) s0[i] += v[u][i];
         }
       }
     }
   }
 #pragma unroll
   for (int i = 0; i < VW; ++i) {
-    part0[(long)c * ncols + j + i] = s0[i];
-    if constexpr (MODE == 1) part1[(long)c * ncols + j + i] = s1[i];
+    sh[g][0][tx * VW + i] = s0[i];
+    if constexpr (MODE == 1) sh[g][MODE == 1 ? 1 : 0][tx * VW + i] = s1[i];
   }
-}
-
-// out[j] += sum_c part[c][j], chunks in order
-__global__ void reduce_partials_kernel(const float* __restrict__ part, int nchunk, int ncols, float* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
-  float s = 0.f;
+  __syncthreads();
+  // combine the groups in group order: thread (tx, g) finishes columns tx * VW + e, e = g, g + CP_GROUPS, ...
+  const long cb = (long)blockIdx.x * 128 * VW;
+  for (int e = g; e < VW; e += CP_GROUPS) {
+    const int col = tx * VW + e;
+    if (cb + col < ncols) {
+      float t0 = sh[0][0][col];
+      for (int q = 1; q < CP_GROUPS; ++q) t0 += sh[q][0][col];
+      part0[(long)c * ncols + cb + col] = t0;
+      if constexpr (MODE == 1) {
+        float t1 = sh[0][MODE == 1 ? 1 : 0][col];
+        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][MODE == 1 ? 1 : 0][col];
+        part1[(long)c * ncols + cb + col] = t1;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tx == 0 && g == 0) last = atomicAdd(&ticket[blockIdx.x], 1) == nch - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // final reduction of this column block over the chunks, chunk order
+  for (int col = g * 128 + tx; col < 128 * VW; col += 128 * CP_GROUPS) {
+    if (cb + col >= ncols) continue;
+    float t0 = 0.f, t1 = 0.f;
 #pragma unroll 8
-  for (int c = 0; c < nchunk; ++c) s += part[(long)c * ncols + j];
-  out[j] += s;
+    for (int q = 0; q < nch; ++q) {
+      t0 += __ldcg(part0 + (long)q * ncols + cb + col);
+      if constexpr (MODE == 1) t1 += __ldcg(part1 + (long)q * ncols + cb + col);
+    }
+    out0[cb + col] += t0;
+    if constexpr (MODE == 1) out1[cb + col] += t1;
+  }
+  if (tx == 0 && g == 0) ticket[blockIdx.x] = 0;
 }
 
 // Cross-entropy over one row of logits ("softmax" layer):
@@ -500,7 +533,7 @@ bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long
 }
 template <typename T>
 bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dres, T* dx, float* dg, float* db,
-            float* part, long rows, int d, cudaStream_t st) {
+            float* part, int* ticket, long rows, int d, cudaStream_t st) {
   if (d % Vec<T>::N || d > LN_THREADS * LN_MAXC * Vec<T>::N) {
     set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
     return false;
@@ -513,29 +546,30 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
   }
   LAUNCH_OK();
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
-  float* p0 = part;
-  float* p1 = part + (long)nch * d;
   constexpr int VW = Vec<T>::N;
-  col_partials_kernel<T, 1><<<dim3((d / VW + 127) / 128, nch), 128, 0, st>>>(dy, d, x, stats, rows, d, p0, p1);
-  LAUNCH_OK();
-  reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p0, nch, d, dg);
-  LAUNCH_OK();
-  reduce_partials_kernel<<<(d + 127) / 128, 128, 0, st>>>(p1, nch, d, db);
+  if ((d / VW + 127) / 128 > CS_TICKETS) {
+    set_error("ln_bwd: %d columns exceed the column-sum ticket slots", d);
+    return false;
+  }
+  col_sums_kernel<T, 1><<<dim3((d / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+      dy, d, x, stats, rows, d, part, part + (long)nch * d, dg, db, ticket);
   LAUNCH_OK();
   return true;
 }
 template <typename T>
-bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, cudaStream_t st) {
+bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   constexpr int VW = Vec<T>::N;
   if (n % VW || ld % VW) {
     set_error("bias_grad: columns and pitch must be multiples of %d", VW);
     return false;
   }
-  col_partials_kernel<T, 0><<<dim3((n / VW + 127) / 128, nch), 128, 0, st>>>(dy, ld, nullptr, nullptr, rows, n,
-                                                                              part, nullptr);
-  LAUNCH_OK();
-  reduce_partials_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, nch, n, db);
+  if ((n / VW + 127) / 128 > CS_TICKETS) {
+    set_error("bias_grad: %d columns exceed the column-sum ticket slots", n);
+    return false;
+  }
+  col_sums_kernel<T, 0><<<dim3((n / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+      dy, ld, nullptr, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
   LAUNCH_OK();
   return true;
 }
@@ -616,9 +650,9 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
 #define INST(T)                                                                                                 \
   template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t);                   \
   template bool ln_apply<T>(const T*, const T*, const T*, const float*, T*, long, int, cudaStream_t);           \
-  template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, long, \
+  template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, int*, long, \
                           int, cudaStream_t);                                                                   \
-  template bool bias_grad<T>(const T*, long, long, int, float*, float*, cudaStream_t);                          \
+  template bool bias_grad<T>(const T*, long, long, int, float*, float*, int*, cudaStream_t);                    \
   template bool cross_entropy<T>(T*, long, int, const int32_t*, long, int, long, float, float*, cudaStream_t);  \
   template bool embed_fwd<T>(const int32_t*, long, int, long, const T*, const T*, T*, int, cudaStream_t);       \
   template bool embed_bwd<T>(const int32_t*, long, int, int, const T*, int, int, float*, float*, int*,         \

@@ -238,11 +238,16 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   Scratch sc = scratch_view(p);
   T* dy = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
   T* G = (T*)sc.G;
-  if (!p->blk_full[l]) {
+  const bool rc = !p->blk_full[l];
+  // LN outputs the weight gradients read: re-applied from the stash, or (recompute) kept from the
+  // re-run forward -- LN1(x) in A, LN2(x2) in DA (free until the fc data-gradient GEMM)
+  T* ln1 = (T*)sc.A;
+  T* ln2 = rc ? (T*)sc.DA : (T*)sc.A;
+  if (rc) {
     // ACT_RECOMPUTE: re-run the block forward from its input checkpoint into the shared entry
     // (same kernels and inputs as the forward: bit-identical tensors); the MLP projection's
     // output is not needed by the backward and is skipped
-    PEER_OK(ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
+    PEER_OK(ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), ln1, s.st1, M, d, p->s_comp));
     Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
     e.bias = w(T_BQKV);
     PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
@@ -252,39 +257,42 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
     e.res = s.x;
     e.ldr = d;
     PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp));
-    e = epi(EPI_BIAS, s.u, 4 * d);
+    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp));
+    e = epi(EPI_BIAS_GELU, s.u, 4 * d);   // u and GELU(u) in one pass, as in the forward
     e.bias = w(T_BFC);
-    PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)sc.A, d, false, w(T_WFC), d, false, e));
+    e.out2 = G;
+    e.ldo2 = 4 * d;
+    PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)ln2, d, false, w(T_WFC), d, false, e));
+  } else {
+    PEER_OK(gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   }
   // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
-  PEER_OK(gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
-  PEER_OK(bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->s_comp));
+  PEER_OK(bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
   Epi e = epi(EPI_DGELU, G, 4 * d);
   e.aux = s.u;
   e.ldx = 4 * d;
   PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, e));
   // MLP fc: u = LN2(x2) W_fc^T + b_fc
-  PEER_OK(ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, (T*)sc.A, M, d, p->s_comp));
-  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)sc.A, d, true, epi(EPI_ACC_F32, g(T_WFC), d)));
-  PEER_OK(bias_grad<T>(G, 4 * d, M, 4 * d, g(T_BFC), p->red, p->s_comp));
+  if (!rc) PEER_OK(ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
+  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d)));
+  PEER_OK(bias_grad<T>(G, 4 * d, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
   PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
-                    M, d, p->s_comp));
+                    p->red_ticket, M, d, p->s_comp));
   // attention projection: x2 = x + o W_o^T + b_o
   PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d)));
-  PEER_OK(bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->s_comp));
+  PEER_OK(bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, d, (const T*)sc.DX2, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
   // attention
   PEER_OK(attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
   // QKV: qkv = LN1(x) W_qkv^T + b_qkv
-  PEER_OK(ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, (T*)sc.A, M, d, p->s_comp));
-  PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)sc.A, d, true, epi(EPI_ACC_F32, g(T_WQKV), d)));
-  PEER_OK(bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->s_comp));
+  if (!rc) PEER_OK(ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, ln1, M, d, p->s_comp));
+  PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)ln1, d, true, epi(EPI_ACC_F32, g(T_WQKV), d)));
+  PEER_OK(bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
   PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
-                    p->red, M, d, p->s_comp));
+                    p->red, p->red_ticket, M, d, p->s_comp));
   return true;
 }
 
@@ -307,8 +315,8 @@ bool head(atom_peer* p, int mb, const SegView& sv) {
   PEER_OK(gemm<T>(p, M, d, V, (const T*)sc.logits, Vp, false, w(T_WLM), d, true, epi(EPI_STORE, sc.dz, d)));
   PEER_OK(gemm<T>(p, V, d, M, (const T*)sc.logits, Vp, true, (const T*)sc.z, d, true, epi(EPI_ACC_F32, g(T_WLM), d)));
   T* dout = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
-  PEER_OK(ln_bwd<T>((const T*)sc.dz, h, sc.hst, w(T_LNFG), nullptr, dout, g(T_LNFG), g(T_LNFB), p->red, M, d,
-                    p->s_comp));
+  PEER_OK(ln_bwd<T>((const T*)sc.dz, h, sc.hst, w(T_LNFG), nullptr, dout, g(T_LNFG), g(T_LNFB), p->red,
+                    p->red_ticket, M, d, p->s_comp));
   return true;
 }
 
@@ -577,12 +585,15 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
                 al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
   p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);
   p->emb = (int*)a; a += al256(4LL * (3 * dm.V + 1 + M));
-  p->loss_dev = (float*)a; a += 256;
+  p->loss_dev = (float*)a;                 // 256-byte slot: the step loss at 0,
+  p->red_ticket = (int*)(a + 64);          // column-sum tickets at 64 (48 ints, zeroed below)
+  a += 256;
   if (a - p->arena != p->plan.device_bytes) {
     set_error("internal: arena carve %lld != plan.device_bytes %lld", (long long)(a - p->arena),
               (long long)p->plan.device_bytes);
     return false;
   }
+  PEER_CUDA(cudaMemsetAsync(p->loss_dev, 0, 256, p->s_comp));
   // initial parameters -> host master (padded layout)
   memset(p->h_master, 0, nb);
   if (init_params) {

@@ -43,6 +43,7 @@ struct atom_peer {
   float* red = nullptr;
   int* emb = nullptr;
   float* loss_dev = nullptr;
+  int* red_ticket = nullptr;            // CS_TICKETS zeroed ints (column-sum kernels)
 
   // ---- host arenas (library-owned, pinned), padded canonical layout ----
   float* h_master = nullptr;

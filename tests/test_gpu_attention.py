@@ -21,7 +21,8 @@ def ref_attention(qkv, B, T, h, dh):
 
 
 CASES = [(2, 128, 2, 64), (1, 300, 3, 64), (2, 256, 2, 128), (1, 384, 2, 128), (1, 200, 2, 80), (2, 256, 4, 80),
-         (1, 2048, 2, 128), (2, 50, 2, 64), (3, 640, 2, 80), (1, 1, 1, 128)]
+         (1, 2048, 2, 128), (2, 50, 2, 64), (3, 640, 2, 80), (1, 1, 1, 128), (1, 1024, 2, 64),
+         (2, 1024, 2, 80)]
 
 
 @pytest.mark.parametrize("impl", [atom.ATTN_TC, atom.ATTN_MMA], ids=["tcgen05", "mma_sync"])
@@ -40,7 +41,7 @@ def test_attention_forward(impl, case):
 
 
 BWD_CASES = [(2, 256, 2, 64), (1, 200, 2, 80), (1, 384, 2, 128), (1, 300, 3, 64), (1, 2048, 1, 128),
-             (2, 130, 2, 80)]
+             (2, 130, 2, 80), (1, 1024, 2, 80), (1, 64, 1, 64)]
 
 
 @pytest.mark.parametrize("impl", [atom.ATTN_TC, atom.ATTN_MMA], ids=["tcgen05", "mma_sync"])
