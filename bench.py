@@ -48,7 +48,8 @@ WORKLOADS = {
     # name: (config, model-state cap bytes, description)
     "xl": ("xl", 10 * 2 ** 30, "GPT-3 XL 1.3B (24L, d=2048, 16x128 heads, T=2048, b=8), model state capped at 10 GiB"),
     "2.7b": ("2.7b", 20 * 2 ** 30, "GPT-3 2.7B (32L, d=2560, 32x80 heads, T=2048, b=8), model state capped at "
-             "20 GiB (resident would need 50 GB), block re-forward in the backward (full stash does not fit)"),
+             "20 GiB (resident would need 50 GB); sub-models, C and the activation policy planned from a "
+             "profiled compute rate"),
     "small": ("small", 0, "GPT-3 Small 125M (12L, d=768), per-layer sub-models"),
     "tiny": ("tiny", 3 * 10 ** 6, "tiny GPT (4L, d=64, T=32, V=256)"),
 }
@@ -191,6 +192,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--link-gbs", type=float, default=BIDIR_GBS)
     ap.add_argument("--trace-out", default="", help="write the last step's per-op trace here (rank 0)")
+    ap.add_argument("--planner-tflops", type=float, default=0.0,
+                    help="compute rate the planner's cost model assumes (default: measured by a profile run)")
+    ap.add_argument("--no-profile", action="store_true",
+                    help="plan with the measured bf16 peak instead of a profiled compute rate")
     args = ap.parse_args()
     cfg_name, state_cap, wl_desc = WORKLOADS[args.config]
     g = synth.CONFIGS[cfg_name]
@@ -212,9 +217,34 @@ def main():
     free, total = torch.cuda.mem_get_info()
     hbm_budget = int(free - 6 * 2 ** 30)
     # peer averaging cadence from a global batch of 512 sequences (reading R17)
-    cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(pk["bf16_tflops"] * 1e12),
+    plan_tf = args.planner_tflops or pk["bf16_tflops"]
+    cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(plan_tf * 1e12),
                         state_budget=state_cap, lr=1e-4, warmup_steps=3000)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
+    profiled = None
+    if not args.planner_tflops and not args.no_profile:
+        # measured profile -> plan (R34): run the first plan for a few
+        # steps, measure the compute rate it sustains, re-plan with that rate (min over ranks so
+        # every peer gets the same plan)
+        from paper_2403_10504_b200 import profile as aprof
+        toks0 = [torch.tensor(synth.tokens(g, plan.C * g.micro_batch, synth.step_seed(rank, 10 ** 6 + s)),
+                              device=f"cuda:{local}") for s in range(2)]
+        m = aprof.measure(cfg, plan, toks0, device=local, steps=3)
+        del toks0
+        rates = [m["flops"], m["h2d"] or args.link_gbs * 1e9, m["d2h"] or args.link_gbs * 1e9]
+        if world > 1:
+            import torch.distributed as dist
+            r = torch.tensor(rates, dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(r, op=dist.ReduceOp.MIN)
+            rates = [float(x) for x in r.tolist()]
+        profiled = {"first_plan": {"C": plan.C, "act_policy": plan.act_policy, "sub_models": plan.ends()},
+                    "measured_tflops": rates[0] / 1e12, "measured_h2d_GBs": rates[1] / 1e9,
+                    "measured_d2h_GBs": rates[2] / 1e9}
+        plan_tf = rates[0] / 1e12
+        cfg.peak_flops = int(rates[0])
+        cfg.d2h_bw = int(min(rates[2], args.link_gbs * 1e9))
+        link_bw = int(min(rates[1], args.link_gbs * 1e9))
+        plan = atom.atom_plan(cfg, hbm_budget, link_bw)
     tok_step = plan.C * g.micro_batch * g.seq_len
     cfg.sync_every = adist.sync_every(world, plan.C, g.micro_batch)     # global batch 512
     nccl_id = adist.bootstrap_nccl_id(atom.atom_nccl_unique_id) if world > 1 else None
@@ -275,6 +305,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_desc, "model": g.name, "global_batch": world * n_seq, "seq_len": g.seq_len,
                        "micro_batch": g.micro_batch, "C": plan.C, "sub_models": plan.ends(),
+                       "act_policy": {0: "auto", 1: "stash", 2: "recompute"}.get(plan.act_policy),
+                       "planner_tflops": plan_tf, "profile": profiled,
                        "state_budget_bytes": state_cap, "device_arena_bytes": plan.device_bytes,
                        "parallelism": f"peers{world}", "sync_every": cfg.sync_every,
                        "l2": "inputs larger than L2 (weights/activations stream through HBM every step)"},

@@ -1,0 +1,77 @@
+"""Measured profile feeding the planner ("the model is profiled
+offline", "We empirically determine C offline via profiling for a particular GPU").
+
+The planner's cost table is analytic (FLOPs / rate, bytes / link). Profiling here measures the
+one number that table needs from this GPU and these kernels: the compute rate the step actually
+sustains, i.e. the FLOPs a step executes (including a re-forward, if the plan has one) divided by
+the busy time of the compute stream, taken from the library's per-op CUDA-event trace of a few
+steps run with a first plan. The plan is then recomputed with that rate (R34).
+"""
+from . import atom
+
+
+def compute_busy_ms(trace: str) -> float:
+    """Union of the compute-lane intervals of a step trace (atom_get_trace), in ms."""
+    iv = sorted((float(f[5]), float(f[6])) for f in (l.split() for l in trace.splitlines())
+                if len(f) >= 7 and f[0] == "compute")
+    busy, cur_s, cur_e = 0.0, None, None
+    for a, b in iv:
+        if cur_e is None or a > cur_e:
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    if cur_e is not None:
+        busy += cur_e - cur_s
+    return busy / 1000.0
+
+
+def compute_span_ms(trace: str) -> float:
+    """First compute-lane op start -> last compute-lane op end, in ms."""
+    iv = [(float(f[5]), float(f[6])) for f in (l.split() for l in trace.splitlines())
+          if len(f) >= 7 and f[0] == "compute"]
+    return (max(b for _, b in iv) - min(a for a, _ in iv)) / 1000.0 if iv else 0.0
+
+
+def executed_flops(g, plan) -> float:
+    """FLOPs one step executes: 6 N-style model FLOPs per token (plan.pred_flops) plus the
+    re-forward of every block outside the last segment under ACT_RECOMPUTE (R28:
+    the QKV, attention-projection and fc GEMMs, 16 d^2 per token, and the attention forward,
+    2 d (T + 1) per token)."""
+    fl = float(plan.pred_flops)
+    if plan.act_policy == atom.ACT_RECOMPUTE:
+        ends = plan.ends()
+        L, d, T = g.n_layer, g.d_model, g.seq_len
+        nb_last = L - ends[-2] if len(ends) >= 2 and ends[-2] < L else 0
+        tokens = plan.C * g.micro_batch * T
+        fl += (L - nb_last) * tokens * (16.0 * d * d + 2.0 * d * (T + 1))
+    return fl
+
+
+def lane_ms(trace: str, lane: str) -> float:
+    """Summed op durations of one lane (copies do not overlap within a lane), in ms."""
+    return sum(float(f[6]) - float(f[5]) for f in (l.split() for l in trace.splitlines())
+               if len(f) >= 7 and f[0] == lane) / 1000.0
+
+
+def measure(cfg, plan, tokens_dev, device: int = 0, steps: int = 3) -> dict:
+    """Profile `plan` on this GPU: run `steps` steps on device tokens and read the last step's
+    trace. Returns the sustained compute rate (FLOPs executed / compute-lane busy time) and the
+    achieved host->device and device->host copy rates (planned bytes / copy-lane busy time): the
+    per-layer execution and loading times of P:329 folded into the cost model's two rates."""
+    peer = atom.Peer(cfg, plan, device=device, init_params=None, seed=1234)
+    try:
+        for s in range(steps):
+            peer.step_device(tokens_dev[s % len(tokens_dev)])
+        tr = peer.trace()
+    finally:
+        import torch
+        peer.destroy()
+        peer.arena = None          # hand the arena back to the driver before the real plan allocates
+        torch.cuda.empty_cache()
+    busy = compute_busy_ms(tr)
+    h2d, d2h = lane_ms(tr, "h2d"), lane_ms(tr, "d2h")
+    return {"flops": executed_flops(cfg, plan) / (busy / 1000.0),
+            "h2d": plan.pred_h2d_B / (h2d / 1000.0) if h2d > 0 else 0.0,
+            "d2h": plan.pred_d2h_B / (d2h / 1000.0) if d2h > 0 else 0.0}
