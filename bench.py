@@ -280,6 +280,7 @@ def main():
     with Clocks(local) as clk:
         ms, losses = timed(peer.step_device, dev_batches[args.warmup:args.warmup + args.steps])
     st = peer.stats()
+    gemm_shapes = sorted(peer.gemm_log(), key=lambda r: -r["ms"])
     # e2e: host tokens through atom_step (pinned staging + H2D in the step), loss read back
     ms_e2e, _ = timed(peer.step, host_batches[args.warmup + args.steps:])
     value = world * args.steps * tok_step / (ms / 1000.0)
@@ -317,7 +318,10 @@ def main():
                          "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                         "gemm_share_of_step": st["gemm_ms"] / ms if ms else None},
+                         "gemm_share_of_step": st["gemm_ms"] / ms if ms else None,
+                         "by_shape": [[r["M"], r["N"], r["K"], r["a_mn"], r["b_mn"], r["epilogue"], r["launches"],
+                                       round(r["ms"], 2), round(r["tflops"], 1)] for r in gemm_shapes],
+                         "by_shape_fields": "M N K a_mn b_mn epilogue launches ms TFLOP/s"},
             "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
                               "flops_per_token": f_alg_per_token(g)},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,

@@ -169,6 +169,10 @@ typedef struct {
   double step_ms;                 /* device time of the last step (first op start -> last op end)     */
 } atom_stats_t;
 atom_status atom_get_stats(atom_peer* peer, atom_stats_t* out);
+/* GEMM time per shape since the last reset (timing on): one line per distinct launch shape,
+ *   "<M> <N> <K> <a_mn> <b_mn> <epilogue> <launches> <ms> <TFLOP/s>"
+ * (ms summed over the launches' CUDA-event durations).  Same buffer rules as atom_plan_schedule. */
+atom_status atom_get_gemm_log(atom_peer* peer, char* buf, int64_t cap, int64_t* len);
 /* Reset counters; timing != 0 brackets every GEMM launch with CUDA events (GEMM-time roofline). */
 atom_status atom_reset_stats(atom_peer* peer, int32_t timing);
 

@@ -166,6 +166,8 @@ lib.atom_get_params.restype = C.c_int
 lib.atom_get_params.argtypes = [_P, C.c_void_p, C.c_void_p, C.c_void_p]
 lib.atom_get_trace.restype = C.c_int
 lib.atom_get_trace.argtypes = [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+lib.atom_get_gemm_log.restype = C.c_int
+lib.atom_get_gemm_log.argtypes = [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
 lib.atom_get_stats.restype = C.c_int
 lib.atom_get_stats.argtypes = [_P, C.POINTER(Stats)]
 lib.atom_reset_stats.restype = C.c_int
@@ -232,6 +234,20 @@ class Peer:
         buf = C.create_string_buffer(n.value + 1)
         check(lib.atom_get_trace(self.h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
+
+    def gemm_log(self) -> list:
+        """Per-shape GEMM timing since the last reset_stats(timing=True): dicts with M, N, K,
+        a_mn, b_mn, epilogue, launches, ms, tflops."""
+        n = C.c_int64(0)
+        lib.atom_get_gemm_log(self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib.atom_get_gemm_log(self.h, buf, n.value + 1, C.byref(n)))
+        keys = ("M", "N", "K", "a_mn", "b_mn", "epilogue", "launches", "ms", "tflops")
+        out = []
+        for line in buf.value.decode().splitlines():
+            f = line.split()
+            out.append({k: (float(v) if k in ("ms", "tflops") else int(v)) for k, v in zip(keys, f)})
+        return out
 
     def stats(self) -> dict:
         s = Stats()

@@ -12,6 +12,7 @@ bool peer_flush_average(atom_peer* p);
 bool peer_get_params(atom_peer* p, float* master, float* m, float* v);
 bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms);
 bool peer_stats(atom_peer* p, atom_stats_t* s);
+bool peer_gemm_log(atom_peer* p, std::string* out);
 void peer_reset_stats(atom_peer* p, int timing);
 void peer_free(atom_peer* p);
 bool peer_stream_sync(atom_peer* p);
@@ -173,6 +174,20 @@ atom_status atom_get_trace(atom_peer* p, char* buf, int64_t cap, int64_t* len) {
   std::string s;
   double a, b, c;
   if (!peer_trace(p, &s, &a, &b, &c)) return fail(p, ATOM_E_CUDA);
+  if (len) *len = (int64_t)s.size();
+  if (!buf || cap < (int64_t)s.size() + 1) {
+    set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);
+    return ATOM_E_INVALID;
+  }
+  memcpy(buf, s.data(), s.size());
+  buf[s.size()] = 0;
+  return ATOM_OK;
+}
+
+atom_status atom_get_gemm_log(atom_peer* p, char* buf, int64_t cap, int64_t* len) {
+  if (!p) { set_error("atom_get_gemm_log: NULL peer"); return ATOM_E_INVALID; }
+  std::string s;
+  if (!peer_gemm_log(p, &s)) return fail(p, ATOM_E_CUDA);
   if (len) *len = (int64_t)s.size();
   if (!buf || cap < (int64_t)s.size() + 1) {
     set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);

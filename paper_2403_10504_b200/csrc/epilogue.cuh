@@ -105,4 +105,42 @@ __device__ __forceinline__ void epi_vec8_bf16(const Epi& e, long m, long n, cons
   }
 }
 
+// Same as epi_vec8_bf16 for the bf16-output modes, with its operands already in hand: bias8 the
+// 8 bias values (shared memory), x8 the 8 residual (EPI_BIAS_RES) or pre-activation (EPI_DGELU)
+// values prefetched by the caller one chunk ahead (the per-chunk global-load latency was what
+// bounded the K = 2560 GEMMs' epilogues).
+__device__ __forceinline__ void epi_vec8_bf16_pre(const Epi& e, long m, long n, const float* acc, uint4 bias8,
+                                                  uint4 x8) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = acc[i];
+  if (e.mode == EPI_BIAS || e.mode == EPI_BIAS_RES || e.mode == EPI_BIAS_GELU) {
+    const bf16* bp = (const bf16*)&bias8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += __bfloat162float(bp[i]);
+  }
+  if (e.mode == EPI_BIAS_RES) {
+    const bf16* rp = (const bf16*)&x8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += __bfloat162float(rp[i]);
+  }
+  if (e.mode == EPI_DGELU) {
+    const bf16* xp = (const bf16*)&x8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_fast(__bfloat162float(xp[i]));
+  }
+  uint4 ov;
+  bf16* op = (bf16*)&ov;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) op[i] = __float2bfloat16_rn(v[i]);
+  *(uint4*)((bf16*)e.out + m * e.ldo + n) = ov;
+  if (e.mode == EPI_BIAS_GELU) {
+    uint4 gv;
+    bf16* gp = (bf16*)&gv;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) gp[i] = __float2bfloat16_rn(gelu_fast(__bfloat162float(op[i])));
+    *(uint4*)((bf16*)e.out2 + m * e.ldo2 + n) = gv;
+  }
+}
+
 }  // namespace atom

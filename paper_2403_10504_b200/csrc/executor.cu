@@ -154,7 +154,11 @@ bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, co
   if (p->timing) {
     PEER_CUDA(cudaEventRecord(e1, p->s_comp));
     if (p->gemm_fl.size() < p->gemm_n + 1) p->gemm_fl.resize(p->gemm_n + 1);
+    if (p->gemm_key.size() < p->gemm_n + 1) p->gemm_key.resize(p->gemm_n + 1);
     p->gemm_fl[p->gemm_n] = 2.0 * M * N * (double)K;
+    char key[96];
+    snprintf(key, sizeof key, "%d %d %d %d %d %d", M, N, K, (int)a_mn, (int)b_mn, e.mode);
+    p->gemm_key[p->gemm_n] = key;
     p->gemm_n++;
   }
   return true;
@@ -757,6 +761,9 @@ bool peer_stats(atom_peer* p, atom_stats_t* s) {
     PEER_CUDA(cudaEventElapsedTime(&ms, p->gemm_ev[2 * i], p->gemm_ev[2 * i + 1]));
     p->gemm_ms_acc += ms;
     p->gemm_fl_acc += p->gemm_fl[i];
+    auto& agg = p->gemm_by_shape[p->gemm_key[i]];
+    agg.first += 1;
+    agg.second += ms;
   }
   p->gemm_n = 0;
   memset(s, 0, sizeof(*s));
@@ -772,11 +779,28 @@ bool peer_stats(atom_peer* p, atom_stats_t* s) {
   return true;
 }
 
+// per-shape GEMM timing since the last reset: "M N K a_mn b_mn epilogue launches ms TFLOP/s" lines
+bool peer_gemm_log(atom_peer* p, std::string* out) {
+  atom_stats_t s;
+  PEER_OK(peer_stats(p, &s));   // folds the pending launch events into gemm_by_shape
+  out->clear();
+  char buf[192];
+  for (auto& kv : p->gemm_by_shape) {
+    int M, N, K, a, b, m;
+    sscanf(kv.first.c_str(), "%d %d %d %d %d %d", &M, &N, &K, &a, &b, &m);
+    const double tf = kv.second.second > 0 ? 2.0 * M * N * (double)K * kv.second.first / (kv.second.second * 1e-3) / 1e12 : 0;
+    snprintf(buf, sizeof buf, "%s %lld %.3f %.1f\n", kv.first.c_str(), (long long)kv.second.first, kv.second.second, tf);
+    *out += buf;
+  }
+  return true;
+}
+
 void peer_reset_stats(atom_peer* p, int timing) {
   p->steps = 0;
   p->gemm_launches = 0;
   p->gemm_ms_acc = p->gemm_fl_acc = 0;
   p->gemm_n = 0;
+  p->gemm_by_shape.clear();
   p->h2d_bytes = p->d2h_bytes = 0;
   p->launch_base = g_launch_count;
   p->timing = timing;

@@ -88,6 +88,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait (the caller overlaps it with other work, then tmem_wait_ld())
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // UMMA shared-memory descriptor, 128-byte swizzle (sm100 encoding: version 1 at bit 46,
 // layout type SWIZZLE_128B = 2 at bits 61..63; LBO / SBO in 16-byte units).
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -138,7 +153,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BIAS_BYTES = 4 * BN * 2;   // one bias row per epilogue warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BIAS_BYTES;
 };
 
 template <int BN, bool A_MN, bool B_MN>
@@ -153,6 +169,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  bf16* sbias = (bf16*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [4][BN]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -270,20 +287,65 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(tile, num_m, num_n, &mb, &nb);
       const int m0 = mb * BM;
       const int n0 = nb * BN;
+      const long m = m0 + 32 * q + lane;
+      const bool fast = epi.mode != EPI_ACC_F32 && m0 + BM <= M && n0 + BN <= N;
+      const bool has_bias = epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_RES || epi.mode == EPI_BIAS_GELU;
+      bf16* sb = sbias + q * BN;
+      if (fast && has_bias) {   // this tile's bias row into the warp's smem row (before the wait)
+        __syncwarp();
+        *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const long m = m0 + 32 * q + lane;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + c0, v);
-        const int nb = n0 + c0;
-        if (m < M && nb < N) {
-          if (nb + 32 <= N) {
+      const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+      if (fast) {
+        // interior tile: TMEM chunk c + 1 and its residual / pre-activation operands are in flight
+        // while chunk c is finished and stored
+        const bf16* xrow = epi.mode == EPI_BIAS_RES ? (const bf16*)epi.res + m * epi.ldr
+                         : epi.mode == EPI_DGELU   ? (const bf16*)epi.aux + m * epi.ldx : nullptr;
+        uint32_t va[32], vb[32];
+        uint4 xa[4], xb[4];
+        // chunk c's operands in (vc, xc); chunk c + 1's are loaded into (vn, xn) meanwhile
+        auto chunk = [&](int c, uint32_t (&vc)[32], uint4 (&xc)[4], uint32_t (&vn)[32], uint4 (&xn)[4]) {
+          if (c + 1 < BN / 32) {
+            tmem_ld32_nw(trow + 32 * (c + 1), vn);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) epi_vec8_bf16(epi, m, nb + 8 * j, v + 8 * j);
-          } else {
-            for (int j = 0; j < 32 && nb + j < N; ++j) epi_scalar<bf16>(epi, m, nb + j, v[j]);
+            for (int j = 0; j < 4; ++j)
+              xn[j] = xrow ? *(const uint4*)(xrow + n0 + 32 * (c + 1) + 8 * j) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __uint_as_float(vc[8 * j + i]);
+            const uint4 b8 = has_bias ? *(const uint4*)(sb + 32 * c + 8 * j) : make_uint4(0, 0, 0, 0);
+            epi_vec8_bf16_pre(epi, m, n0 + 32 * c + 8 * j, a, b8, xc[j]);
+          }
+          if (c + 1 < BN / 32) tmem_wait_ld();
+        };
+        tmem_ld32_nw(trow, va);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xa[j] = xrow ? *(const uint4*)(xrow + n0 + 8 * j) : make_uint4(0, 0, 0, 0);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < BN / 32; c += 2) {
+          chunk(c, va, xa, vb, xb);
+          chunk(c + 1, vb, xb, va, xa);
+        }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(trow + c0, v);
+          const int nb = n0 + c0;
+          if (m < M && nb < N) {
+            if (nb + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) epi_vec8_bf16(epi, m, nb + 8 * j, v + 8 * j);
+            } else {
+              for (int j = 0; j < 32 && nb + j < N; ++j) epi_scalar<bf16>(epi, m, nb + j, v[j]);
+            }
           }
         }
       }
@@ -354,7 +416,8 @@ struct Tc2Cfg {
   static constexpr int B_BYTES = HB * BK * 2;  // this CTA's 128 rows of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BIAS_BYTES = 4 * BN * 2;   // one bias row per epilogue warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_BIAS_BYTES;
 };
 
 template <bool A_MN, bool B_MN>
@@ -370,6 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  bf16* sbias = (bf16*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [4][BN]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -497,23 +561,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tile_coords(tile, num_m, num_n, &mb, &nb);
       const int m0 = mb * 2 * BM + rank * BM;
       const int n0 = nb * BN;
+      const long m = m0 + 32 * q + lane;
+      const bool fast = epi.mode != EPI_ACC_F32 && m0 + BM <= M && n0 + BN <= N;
+      const bool has_bias = epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_RES || epi.mode == EPI_BIAS_GELU;
+      bf16* sb = sbias + q * BN;
+      if (fast && has_bias) {   // this tile's bias row into the warp's smem row (before the wait)
+        __syncwarp();
+        *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const long m = m0 + 32 * q + lane;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + c0, v);
-        const int nb = n0 + c0;
-        if (m < M && nb < N) {
-          if (nb + 32 <= N) {
+      const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+      if (fast) {
+        // interior tile: TMEM chunk c + 1 and its residual / pre-activation operands are in flight
+        // while chunk c is finished and stored
+        const bf16* xrow = epi.mode == EPI_BIAS_RES ? (const bf16*)epi.res + m * epi.ldr
+                         : epi.mode == EPI_DGELU   ? (const bf16*)epi.aux + m * epi.ldx : nullptr;
+        uint32_t va[32], vb[32];
+        uint4 xa[4], xb[4];
+        // chunk c's operands in (vc, xc); chunk c + 1's are loaded into (vn, xn) meanwhile
+        auto chunk = [&](int c, uint32_t (&vc)[32], uint4 (&xc)[4], uint32_t (&vn)[32], uint4 (&xn)[4]) {
+          if (c + 1 < BN / 32) {
+            tmem_ld32_nw(trow + 32 * (c + 1), vn);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) epi_vec8_bf16(epi, m, nb + 8 * j, v + 8 * j);
-          } else {
-            for (int j = 0; j < 32 && nb + j < N; ++j) epi_scalar<bf16>(epi, m, nb + j, v[j]);
+            for (int j = 0; j < 4; ++j)
+              xn[j] = xrow ? *(const uint4*)(xrow + n0 + 32 * (c + 1) + 8 * j) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __uint_as_float(vc[8 * j + i]);
+            const uint4 b8 = has_bias ? *(const uint4*)(sb + 32 * c + 8 * j) : make_uint4(0, 0, 0, 0);
+            epi_vec8_bf16_pre(epi, m, n0 + 32 * c + 8 * j, a, b8, xc[j]);
+          }
+          if (c + 1 < BN / 32) tmem_wait_ld();
+        };
+        tmem_ld32_nw(trow, va);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xa[j] = xrow ? *(const uint4*)(xrow + n0 + 8 * j) : make_uint4(0, 0, 0, 0);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < BN / 32; c += 2) {
+          chunk(c, va, xa, vb, xb);
+          chunk(c + 1, vb, xb, va, xa);
+        }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(trow + c0, v);
+          const int nb = n0 + c0;
+          if (m < M && nb < N) {
+            if (nb + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) epi_vec8_bf16(epi, m, nb + 8 * j, v + 8 * j);
+            } else {
+              for (int j = 0; j < 32 && nb + j < N; ++j) epi_scalar<bf16>(epi, m, nb + j, v[j]);
+            }
           }
         }
       }
+
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));

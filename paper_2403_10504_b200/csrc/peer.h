@@ -76,6 +76,8 @@ struct atom_peer {
   int timing = 0;
   std::vector<cudaEvent_t> gemm_ev;
   std::vector<double> gemm_fl;
+  std::vector<std::string> gemm_key;    // "M N K a_mn b_mn epilogue" of each timed launch
+  std::map<std::string, std::pair<int64_t, double>> gemm_by_shape;   // launches, ms (since reset)
   size_t gemm_n = 0;
   int64_t steps = 0, gemm_launches = 0;
   unsigned long long launch_base = 0;
