@@ -161,6 +161,30 @@ def run_reference(args, g, wl_desc):
     print(json.dumps(line), flush=True)
 
 
+GEMM_NCU = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01f_gemm_step_ncu.json")
+GEMM_NCU_SHAPES = [("qkv", 16384, 7680, 2560, 0), ("proj", 16384, 2560, 2560, 1), ("fc", 16384, 10240, 2560, 1),
+                   ("fc2", 16384, 2560, 10240, 1)]
+
+
+def gemm_traffic():
+    """DRAM bytes per GEMM launch from the committed `ncu --set full` capture of the first four
+    GEMMs of a 2.7B step (one block forward: QKV, projection, fc, fc2), next to their algorithmic
+    bytes (A + B + outputs + residual)."""
+    try:
+        with open(GEMM_NCU) as f:
+            caps = json.load(f)
+    except OSError:
+        return {"traffic": None}
+    per, alg = [], []
+    for c, (name, M, N, K, extra) in zip(caps, GEMM_NCU_SHAPES):
+        per.append(c["dram_read"] + c["dram_write"])
+        outs = 2 if name == "fc" else 1   # fc stores the pre-activation and GELU(u)
+        alg.append(2.0 * (M * K + N * K + outs * M * N + extra * M * N))
+    return {"traffic": sum(per) / len(per),
+            "traffic_detail": {"shapes": [s[0] for s in GEMM_NCU_SHAPES], "dram_bytes": per,
+                               "algorithmic_bytes": alg, "source": os.path.relpath(GEMM_NCU, os.path.dirname(GEMM_NCU) + "/..")}}
+
+
 def compute_busy_pct(trace, step_ms):
     """Share of the compute lane's span in the last step (its first op start -> last op end) in
     which it runs an op (union of the traced intervals): what is left is the compute stream waiting
@@ -316,7 +340,7 @@ def main():
             "gpu_launches": st["kernel_launches"],
             "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05)", "achieved": gemm_tf,
                          "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": (gemm_tf / peak_tf) if gemm_tf else None, "traffic": None,
+                         "frac": (gemm_tf / peak_tf) if gemm_tf else None, **gemm_traffic(),
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "gemm_share_of_step": st["gemm_ms"] / ms if ms else None,
                          "by_shape": [[r["M"], r["N"], r["K"], r["a_mn"], r["b_mn"], r["epilogue"], r["launches"],

@@ -198,18 +198,26 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
   if (j < ncols) {
     const long r0 = (long)c * RED_ROWS + g * CP_GROWS, r1 = min(rows, r0 + CP_GROWS);
     for (long rb = r0; rb < r1; rb += CP_UNR) {
-      float v[CP_UNR][VW], xv[MODE == 1 ? CP_UNR : 1][VW];
+      float v[CP_UNR][VW], xv[MODE != 0 ? CP_UNR : 1][VW];
 #pragma unroll
       for (int u = 0; u < CP_UNR; ++u) {
         if (rb + u < r1) {
           load_vec<T>(a + (rb + u) * lda + j, v[u]);
-          if constexpr (MODE == 1) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
+          if constexpr (MODE != 0) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
         }
       }
 #pragma unroll
       for (int u = 0; u < CP_UNR; ++u) {
         if (rb + u < r1) {
-          if constexpr (MODE == 1) {
+          if constexpr (MODE == 2) {   // a <- T(a * gelu'(x)) in place; sums of the stored values
+            float o[VW];
+#pragma unroll
+            for (int i = 0; i < VW; ++i) {
+              o[i] = round_t<T>(v[u][i] * gelu_grad_t<T>(xv[u][i]));
+              s0[i] += o[i];
+            }
+            store_vec<T>(const_cast<T*>(a) + (rb + u) * lda + j, o);
+          } else if constexpr (MODE == 1) {
             const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
 #pragma unroll
             for (int i = 0; i < VW; ++i) {
@@ -556,6 +564,21 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
   LAUNCH_OK();
   return true;
 }
+// dy <- T(dy * gelu'(u)) in place (dy [rows, n] at pitch n, u likewise) and db += column sums of
+// the result: the fc pre-activation gradient and its bias gradient in one pass
+template <typename T>
+bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
+  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
+  constexpr int VW = Vec<T>::N;
+  if (n % VW || (n / VW + 127) / 128 > CS_TICKETS) {
+    set_error("dgelu_bias_grad: %d columns (multiple of %d, at most %d blocks)", n, VW, CS_TICKETS);
+    return false;
+  }
+  col_sums_kernel<T, 2><<<dim3((n / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+      dy, n, u, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
+  LAUNCH_OK();
+  return true;
+}
 template <typename T>
 bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
   const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
@@ -653,6 +676,7 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
   template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, int*, long, \
                           int, cudaStream_t);                                                                   \
   template bool bias_grad<T>(const T*, long, long, int, float*, float*, int*, cudaStream_t);                    \
+  template bool dgelu_bias_grad<T>(T*, const T*, long, int, float*, float*, int*, cudaStream_t);              \
   template bool cross_entropy<T>(T*, long, int, const int32_t*, long, int, long, float, float*, cudaStream_t);  \
   template bool embed_fwd<T>(const int32_t*, long, int, long, const T*, const T*, T*, int, cudaStream_t);       \
   template bool embed_bwd<T>(const int32_t*, long, int, int, const T*, int, int, float*, float*, int*,         \

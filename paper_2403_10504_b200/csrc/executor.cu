@@ -132,7 +132,8 @@ Scratch scratch_view(const atom_peer* p) {
 // ------------------------------------------------------------------ compute dispatch
 template <typename T>
 bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B, long ldb, bool b_mn,
-          const Epi& e) {
+          const Epi& e, cudaStream_t stream = nullptr) {
+  const cudaStream_t st = stream ? stream : p->s_comp;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing) {
     while (p->gemm_ev.size() < 2 * (p->gemm_n + 1)) {
@@ -142,17 +143,17 @@ bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, co
     }
     e0 = p->gemm_ev[2 * p->gemm_n];
     e1 = p->gemm_ev[2 * p->gemm_n + 1];
-    PEER_CUDA(cudaEventRecord(e0, p->s_comp));
+    PEER_CUDA(cudaEventRecord(e0, st));
   }
   bool ok;
   if constexpr (std::is_same<T, bf16>::value)
-    ok = gemm_tc(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, p->s_comp);
+    ok = gemm_tc(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, st);
   else
-    ok = gemm_simt<T>(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, p->s_comp);
+    ok = gemm_simt<T>(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, st);
   if (!ok) return false;
   p->gemm_launches++;
   if (p->timing) {
-    PEER_CUDA(cudaEventRecord(e1, p->s_comp));
+    PEER_CUDA(cudaEventRecord(e1, st));
     if (p->gemm_fl.size() < p->gemm_n + 1) p->gemm_fl.resize(p->gemm_n + 1);
     if (p->gemm_key.size() < p->gemm_n + 1) p->gemm_key.resize(p->gemm_n + 1);
     p->gemm_fl[p->gemm_n] = 2.0 * M * N * (double)K;
@@ -273,30 +274,63 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
   PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
   PEER_OK(bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
-  Epi e = epi(EPI_DGELU, G, 4 * d);
-  e.aux = s.u;
-  e.ldx = 4 * d;
-  PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, e));
-  // MLP fc: u = LN2(x2) W_fc^T + b_fc
+  // fc pre-activation gradient: (dy W_pr) with a plain-store epilogue, then the GELU derivative
+  // and the fc bias gradient in one pass over it (the GEMM epilogue reading u per row was the
+  // slow part of the fused form)
+  PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
+  PEER_OK(dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
+  // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
+  // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
+  // LN2 output (A under stash) is rewritten by LN1's re-apply after the attention backward, which
+  // also rewrites G; WO reads DX2 / o, WQKV reads G / A; the next block rewrites G, A, DX2.
+  const bool side = p->side_wgrad;
+  const cudaStream_t sd = side ? p->s_side : p->s_comp;
+  auto fork = [&]() -> bool {
+    if (side) {
+      PEER_CUDA(cudaEventRecord(p->ev_side[0], p->s_comp));
+      PEER_CUDA(cudaStreamWaitEvent(p->s_side, p->ev_side[0], 0));
+    }
+    return true;
+  };
+  auto mark = [&](int i) -> bool {
+    if (side) PEER_CUDA(cudaEventRecord(p->ev_side[i], p->s_side));
+    return true;
+  };
+  auto join = [&](int i) -> bool {
+    if (side) PEER_CUDA(cudaStreamWaitEvent(p->s_comp, p->ev_side[i], 0));
+    return true;
+  };
+  // MLP fc: u = LN2(x2) W_fc^T + b_fc (under recompute LN2's output is DA, rewritten just below:
+  // that gradient stays on the main stream)
   if (!rc) PEER_OK(ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
-  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d)));
-  PEER_OK(bias_grad<T>(G, 4 * d, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
+  if (!rc) PEER_OK(fork());
+  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d),
+                  rc ? p->s_comp : sd));
+  if (!rc) PEER_OK(mark(1));
   PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
   PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
                     p->red_ticket, M, d, p->s_comp));
   // attention projection: x2 = x + o W_o^T + b_o
-  PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d)));
+  PEER_OK(fork());
+  PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d),
+                  sd));
+  PEER_OK(mark(2));
   PEER_OK(bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, d, (const T*)sc.DX2, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
-  // attention
+  // attention (writes G, which the fc weight gradient reads)
+  if (!rc) PEER_OK(join(1));
   PEER_OK(attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
   // QKV: qkv = LN1(x) W_qkv^T + b_qkv
   if (!rc) PEER_OK(ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, ln1, M, d, p->s_comp));
-  PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)ln1, d, true, epi(EPI_ACC_F32, g(T_WQKV), d)));
+  PEER_OK(fork());
+  PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)ln1, d, true, epi(EPI_ACC_F32, g(T_WQKV), d), sd));
+  PEER_OK(mark(3));
   PEER_OK(bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
   PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
                     p->red, p->red_ticket, M, d, p->s_comp));
+  // the side stream is in order: its last mark covers WO and WQKV (and WFC)
+  PEER_OK(join(3));
   return true;
 }
 
@@ -507,7 +541,7 @@ namespace atom {
 
 bool peer_stream_sync(atom_peer* p) {
   PEER_CUDA(cudaSetDevice(p->device));
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
     if (s) PEER_CUDA(cudaStreamSynchronize(s));
   return true;
 }
@@ -536,6 +570,12 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_side, cudaStreamNonBlocking));
+  for (auto& ev : p->ev_side) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  {
+    const char* e = getenv("ATOM_SIDE_WGRAD");   // 0: all block-backward kernels on one stream
+    p->side_wgrad = !(e && e[0] == '0');
+  }
   for (int kind = K_CAST; kind <= K_STORE; ++kind)
     for (int k = 1; k <= p->S; ++k) {
       cudaEvent_t ev;
@@ -808,15 +848,17 @@ void peer_reset_stats(atom_peer* p, int timing) {
 
 void peer_free(atom_peer* p) {
   cudaSetDevice(p->device);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
     if (s) cudaStreamSynchronize(s);
   if (p->comm) ncclCommDestroy(p->comm);
+  for (auto ev : p->ev_side)
+    if (ev) cudaEventDestroy(ev);
   for (auto& kv : p->op_ev) cudaEventDestroy(kv.second);
   for (auto ev : p->trace_ev) cudaEventDestroy(ev);
   for (auto ev : p->gemm_ev) cudaEventDestroy(ev);
   if (p->ev_loss) cudaEventDestroy(p->ev_loss);
   if (p->step_start) cudaEventDestroy(p->step_start);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
     if (s) cudaStreamDestroy(s);
   for (float* h : {p->h_master, p->h_m, p->h_v, p->h_loss})
     if (h) cudaFreeHost(h);

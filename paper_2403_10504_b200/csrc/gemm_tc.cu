@@ -135,12 +135,14 @@ constexpr int BK = 64;
 // Grouped raster: consecutive tiles walk GROUP_M m-blocks down before moving right, so the
 // ~148 tiles in flight cover a GROUP_M x (148 / GROUP_M) block of the output and re-read A and
 // B from L2 instead of DRAM.
+// GROUP_M adapts to K (host side, group_m_for): the A row panels of a group must stay in L2
+// next to B; with a fixed 16 the K = 10240 projection GEMM read A from DRAM 2.5x over.
 constexpr int GROUP_M = 16;
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int* mb, int* nb) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int* mb, int* nb, int group_m) {
+  const int per_group = group_m * num_n;
   const int g = tile / per_group;
-  const int first = g * GROUP_M;
-  const int gsz = min(num_m - first, GROUP_M);
+  const int first = g * group_m;
+  const int gsz = min(num_m - first, group_m);
   const int r = tile - g * per_group;
   *mb = first + r % gsz;
   *nb = r / gsz;
@@ -160,7 +162,7 @@ struct TcCfg {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, Epi epi) {
+                   int K, Epi epi, int group_m) {
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, &mb, &nb);
+        tile_coords(tile, num_m, num_n, &mb, &nb, group_m);
         const int m0 = mb * BM;
         const int n0 = nb * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -284,16 +286,19 @@ __global__ void __launch_bounds__(256, 1)
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mb, nb;
-      tile_coords(tile, num_m, num_n, &mb, &nb);
+      tile_coords(tile, num_m, num_n, &mb, &nb, group_m);
       const int m0 = mb * BM;
       const int n0 = nb * BN;
       const long m = m0 + 32 * q + lane;
-      const bool fast = epi.mode != EPI_ACC_F32 && m0 + BM <= M && n0 + BN <= N;
+      // fast path: interior tiles of the modes without per-row global operands (the residual /
+      // pre-activation prefetch of EPI_BIAS_RES / EPI_DGELU measured slower than the plain loop)
+      const bool fast = (epi.mode == EPI_STORE || epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_GELU) &&
+                        m0 + BM <= M && n0 + BN <= N;
       const bool has_bias = epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_RES || epi.mode == EPI_BIAS_GELU;
       bf16* sb = sbias + q * BN;
       if (fast && has_bias) {   // this tile's bias row into the warp's smem row (before the wait)
         __syncwarp();
-        *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
+        if (8 * lane < BN) *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
         __syncwarp();
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -423,7 +428,7 @@ struct Tc2Cfg {
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, Epi epi) {
+                    int K, Epi epi, int group_m) {
   using Cfg = Tc2Cfg;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -478,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, &mb, &nb);
+        tile_coords(tile, num_m, num_n, &mb, &nb, group_m);
         const int m0 = mb * 2 * BM + rank * BM;
         const int n0 = nb * BN + rank * Cfg::HB;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -558,16 +563,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mb, nb;
-      tile_coords(tile, num_m, num_n, &mb, &nb);
+      tile_coords(tile, num_m, num_n, &mb, &nb, group_m);
       const int m0 = mb * 2 * BM + rank * BM;
       const int n0 = nb * BN;
       const long m = m0 + 32 * q + lane;
-      const bool fast = epi.mode != EPI_ACC_F32 && m0 + BM <= M && n0 + BN <= N;
+      // fast path: interior tiles of the modes without per-row global operands (the residual /
+      // pre-activation prefetch of EPI_BIAS_RES / EPI_DGELU measured slower than the plain loop)
+      const bool fast = (epi.mode == EPI_STORE || epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_GELU) &&
+                        m0 + BM <= M && n0 + BN <= N;
       const bool has_bias = epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_RES || epi.mode == EPI_BIAS_GELU;
       bf16* sb = sbias + q * BN;
       if (fast && has_bias) {   // this tile's bias row into the warp's smem row (before the wait)
         __syncwarp();
-        *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
+        if (8 * lane < BN) *(uint4*)(sb + 8 * lane) = *(const uint4*)((const bf16*)epi.bias + n0 + 8 * lane);
         __syncwarp();
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -688,6 +696,13 @@ static int num_sms() {
   return n;
 }
 
+// m-blocks per raster group: keep ~40 MB of A row panels (group_m x rows x K bf16) live in L2
+static int group_m_for(int K, int ctas_per_tile) {
+  const long panel = (long)BM * ctas_per_tile * K * 2;
+  long g = (40L << 20) / (panel > 0 ? panel : 1);
+  return (int)(g < 2 ? 2 : g > GROUP_M ? GROUP_M : g);
+}
+
 template <int BN, bool A_MN, bool B_MN>
 static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e,
                       cudaStream_t st) {
@@ -700,7 +715,7 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, e);
+  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 1));
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
@@ -717,7 +732,7 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + Tc2Cfg::BN - 1) / Tc2Cfg::BN);
   const int clusters = std::min(tiles, num_sms() / 2);
-  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, M, N, K, e);
+  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 2));
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;

@@ -54,6 +54,12 @@ struct atom_peer {
 
   // ---- streams / events ----
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_comm = nullptr;
+  // block backward: weight-gradient GEMMs that no later kernel of the block waits for run on a
+  // side stream, filling the SMs their tile tails (and the main stream's HBM-bound kernels) leave
+  // idle; ev_side[0] forks, ev_side[1..3] mark the WFC / WO / WQKV gradients done
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool side_wgrad = true;
   std::map<std::pair<int, int>, cudaEvent_t> op_ev;  // (kind, seg) -> completion event
   cudaEvent_t ev_loss = nullptr;
 
