@@ -1770,9 +1770,11 @@ static bool make_map2d(CUtensorMap* m, const bf16* base, long cols, long rows, i
   return true;
 }
 
+// st2 != NULL: the dQ kernel runs on st2 concurrently with the dK/dV kernel (independent outputs;
+// each fills the SMs the other's causal tail leaves idle), joined back into st
 template <int DH>
 bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B, int T_,
-         int h, cudaStream_t st) {
+         int h, cudaStream_t st, cudaStream_t st2) {
   using C = BCfg<DH>;
   const long d = (long)h * DH, rows = (long)B * T_;
   CUtensorMap qkv64, qkv128, do64, do128;
@@ -1811,6 +1813,16 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
     count_launch();
   } else {
+    static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (st2 && !ev_fork) {
+      ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    if (st2) {   // dQ's inputs (qkv, dO, LSE, D) are ready once dsum has run on st
+      ATOM_CUDA_OK(cudaEventRecord(ev_fork, st));
+      ATOM_CUDA_OK(cudaStreamWaitEvent(st2, ev_fork, 0));
+    }
+    const cudaStream_t sq = st2 ? st2 : st;
     if (tsa_kv)
       attn_bwd_dkv2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
                                                                         T_, h);
@@ -1819,11 +1831,16 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
                                                                          T_, h);
     count_launch();
     if (tsa_q)
-      attn_bwd_dq2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
+      attn_bwd_dq2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
                                                                        dqkv, T_, h);
     else
-      attn_bwd_dq2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
+      attn_bwd_dq2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
                                                                         dqkv, T_, h);
+    if (st2) {
+      ATOM_CUDA_OK(cudaGetLastError());
+      ATOM_CUDA_OK(cudaEventRecord(ev_join, st2));
+      ATOM_CUDA_OK(cudaStreamWaitEvent(st, ev_join, 0));
+    }
     count_launch();
   }
   ATOM_CUDA_OK(cudaGetLastError());
@@ -1835,11 +1852,11 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
 bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 80 || dh == 128) && ((3 * d) % 8 == 0); }
 
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st) {
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2) {
   switch (dh) {
-    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
-    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
-    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st);
+    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
+    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
+    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
   }
   set_error("tcgen05 attention: unsupported head size %d", dh);
   return false;

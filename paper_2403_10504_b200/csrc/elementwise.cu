@@ -51,10 +51,12 @@ __device__ __forceinline__ void store_vec(T* p, const float* f) {
 }
 
 // y = LN(x) * g + b; stats[row] = (mean, rstd)                       (minGPT nn.LayerNorm)
+// With res: x <- T(x + res) first (written back; the residual add of the producing GEMM moved here)
 template <typename T, int NC>
 __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                             const T* __restrict__ b, T* __restrict__ y,
-                                                            float* __restrict__ stats, int d) {
+                                                            float* __restrict__ stats, int d,
+                                                            const T* __restrict__ res) {
   constexpr int VW = Vec<T>::N;
   __shared__ float sh[4];
   const long row = blockIdx.x;
@@ -67,6 +69,13 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       load_vec<T>(xr + ch * VW, v[c]);
+      if (res) {
+        float r[VW];
+        load_vec<T>(res + row * d + ch * VW, r);
+#pragma unroll
+        for (int i = 0; i < VW; ++i) v[c][i] = round_t<T>(v[c][i] + r[i]);
+        store_vec<T>(const_cast<T*>(xr) + ch * VW, v[c]);
+      }
 #pragma unroll
       for (int i = 0; i < VW; ++i) s += v[c][i];
     }
@@ -198,35 +207,41 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
   if (j < ncols) {
     const long r0 = (long)c * RED_ROWS + g * CP_GROWS, r1 = min(rows, r0 + CP_GROWS);
     for (long rb = r0; rb < r1; rb += CP_UNR) {
-      float v[CP_UNR][VW], xv[MODE != 0 ? CP_UNR : 1][VW];
+      // raw 16-byte loads first (all in flight), conversions after
+      uint4 ra[CP_UNR], rx[MODE != 0 ? CP_UNR : 1];
 #pragma unroll
       for (int u = 0; u < CP_UNR; ++u) {
-        if (rb + u < r1) {
-          load_vec<T>(a + (rb + u) * lda + j, v[u]);
-          if constexpr (MODE != 0) load_vec<T>(x + (rb + u) * ncols + j, xv[u]);
-        }
+        const bool ok = rb + u < r1;
+        ra[u] = ok ? *(const uint4*)(a + (rb + u) * lda + j) : make_uint4(0, 0, 0, 0);
+        if constexpr (MODE != 0) rx[u] = ok ? *(const uint4*)(x + (rb + u) * ncols + j) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < CP_UNR; ++u) {
         if (rb + u < r1) {
+          float v[VW];
+          const T* ep = (const T*)&ra[u];
+#pragma unroll
+          for (int i = 0; i < VW; ++i) v[i] = to_f(ep[i]);
           if constexpr (MODE == 2) {   // a <- T(a * gelu'(x)) in place; sums of the stored values
+            const T* xp = (const T*)&rx[u];
             float o[VW];
 #pragma unroll
             for (int i = 0; i < VW; ++i) {
-              o[i] = round_t<T>(v[u][i] * gelu_grad_t<T>(xv[u][i]));
+              o[i] = round_t<T>(v[i] * gelu_grad_t<T>(to_f(xp[i])));
               s0[i] += o[i];
             }
             store_vec<T>(const_cast<T*>(a) + (rb + u) * lda + j, o);
           } else if constexpr (MODE == 1) {
+            const T* xp = (const T*)&rx[u];
             const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
 #pragma unroll
             for (int i = 0; i < VW; ++i) {
-              s0[i] = fmaf(v[u][i], (xv[u][i] - mean) * rstd, s0[i]);
-              s1[i] += v[u][i];
+              s0[i] = fmaf(v[i], (to_f(xp[i]) - mean) * rstd, s0[i]);
+              s1[i] += v[i];
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < VW; ++i) s0[i] += v[u][i];
+            for (int i = 0; i < VW; ++i) s0[i] += v[i];
           }
         }
       }
@@ -259,17 +274,45 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // final reduction of this column block over the chunks, chunk order
-  for (int col = g * 128 + tx; col < 128 * VW; col += 128 * CP_GROUPS) {
-    if (cb + col >= ncols) continue;
-    float t0 = 0.f, t1 = 0.f;
-#pragma unroll 8
-    for (int q = 0; q < nch; ++q) {
-      t0 += __ldcg(part0 + (long)q * ncols + cb + col);
-      if constexpr (MODE == 1) t1 += __ldcg(part1 + (long)q * ncols + cb + col);
+  // final reduction of this column block over the chunks: thread (tx, g) sums its VW columns over
+  // chunks g, g + CP_GROUPS, ... (16-byte loads, several in flight), then the groups are added in
+  // group order -- a fixed order, so the result is deterministic
+  float r0[VW], r1[VW];
+#pragma unroll
+  for (int i = 0; i < VW; ++i) r0[i] = r1[i] = 0.f;
+  if (j < ncols) {
+#pragma unroll 4
+    for (int q = g; q < nch; q += CP_GROUPS) {
+#pragma unroll
+      for (int i4 = 0; i4 < VW; i4 += 4) {
+        const float4 a4 = __ldcg((const float4*)(part0 + (long)q * ncols + j + i4));
+        r0[i4] += a4.x; r0[i4 + 1] += a4.y; r0[i4 + 2] += a4.z; r0[i4 + 3] += a4.w;
+        if constexpr (MODE == 1) {
+          const float4 b4 = __ldcg((const float4*)(part1 + (long)q * ncols + j + i4));
+          r1[i4] += b4.x; r1[i4 + 1] += b4.y; r1[i4 + 2] += b4.z; r1[i4 + 3] += b4.w;
+        }
+      }
     }
-    out0[cb + col] += t0;
-    if constexpr (MODE == 1) out1[cb + col] += t1;
+  }
+  __syncthreads();   // the group-combine reads of sh above are done
+#pragma unroll
+  for (int i = 0; i < VW; ++i) {
+    sh[g][0][tx * VW + i] = r0[i];
+    if constexpr (MODE == 1) sh[g][MODE == 1 ? 1 : 0][tx * VW + i] = r1[i];
+  }
+  __syncthreads();
+  for (int e = g; e < VW; e += CP_GROUPS) {
+    const int col = tx * VW + e;
+    if (cb + col < ncols) {
+      float t0 = sh[0][0][col];
+      for (int q = 1; q < CP_GROUPS; ++q) t0 += sh[q][0][col];
+      out0[cb + col] += t0;
+      if constexpr (MODE == 1) {
+        float t1 = sh[0][MODE == 1 ? 1 : 0][col];
+        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][MODE == 1 ? 1 : 0][col];
+        out1[cb + col] += t1;
+      }
+    }
   }
   if (tx == 0 && g == 0) ticket[blockIdx.x] = 0;
 }
@@ -519,14 +562,15 @@ static inline int grid_for(long n, int threads = 256) {
   } while (0)
 
 template <typename T>
-bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st) {
+bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st,
+            const T* res) {
   if (d % Vec<T>::N || d > LN_THREADS * LN_MAXC * Vec<T>::N) {
     set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
     return false;
   }
   switch ((d / Vec<T>::N + LN_THREADS - 1) / LN_THREADS) {   // chunks per thread (same order for any NC)
 #define LN_FWD_CASE(NC) \
-  case NC: ln_fwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d); break;
+  case NC: ln_fwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d, res); break;
     LN_FWD_CASE(1) LN_FWD_CASE(2) LN_FWD_CASE(3) LN_FWD_CASE(4) LN_FWD_CASE(5) LN_FWD_CASE(6)
 #undef LN_FWD_CASE
   }
@@ -671,7 +715,7 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
 }
 
 #define INST(T)                                                                                                 \
-  template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t);                   \
+  template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t, const T*);                   \
   template bool ln_apply<T>(const T*, const T*, const T*, const float*, T*, long, int, cudaStream_t);           \
   template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, int*, long, \
                           int, cudaStream_t);                                                                   \

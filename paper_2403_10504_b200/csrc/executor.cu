@@ -180,7 +180,9 @@ bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float
   const ModelDims& dm = p->dm;
   const int dh = dm.d / dm.h;
   if constexpr (std::is_same<T, bf16>::value) {
-    if (attn_tc_supported(dh, dm.d)) return attn_bwd_tc(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
+    if (attn_tc_supported(dh, dm.d))
+      return attn_bwd_tc(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp,
+                         p->side_wgrad ? p->s_attn : nullptr);
     if (attn_fa_supported(dh)) return attn_bwd_fa(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
   }
   return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
@@ -210,12 +212,12 @@ bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   e.bias = w(T_BQKV);
   PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
   PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
-  e = epi(EPI_BIAS_RES, s.x2, d);
+  // x2 = x + o W_o^T + b_o: the GEMM stores o W_o^T + b_o (plain epilogue), LN2 adds the residual
+  // (a per-row residual read in the GEMM epilogue held this K = d GEMM well below the others)
+  e = epi(EPI_BIAS, s.x2, d);
   e.bias = w(T_BO);
-  e.res = x;
-  e.ldr = d;
   PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-  PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp));
+  PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x));
   e = epi(EPI_BIAS_GELU, s.u, 4 * d);
   e.bias = w(T_BFC);
   e.out2 = sc.G;
@@ -257,12 +259,10 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
     e.bias = w(T_BQKV);
     PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
     PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
-    e = epi(EPI_BIAS_RES, s.x2, d);
+    e = epi(EPI_BIAS, s.x2, d);
     e.bias = w(T_BO);
-    e.res = s.x;
-    e.ldr = d;
     PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp));
+    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp, (const T*)s.x));
     e = epi(EPI_BIAS_GELU, s.u, 4 * d);   // u and GELU(u) in one pass, as in the forward
     e.bias = w(T_BFC);
     e.out2 = G;
@@ -541,7 +541,7 @@ namespace atom {
 
 bool peer_stream_sync(atom_peer* p) {
   PEER_CUDA(cudaSetDevice(p->device));
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
     if (s) PEER_CUDA(cudaStreamSynchronize(s));
   return true;
 }
@@ -571,6 +571,7 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_side, cudaStreamNonBlocking));
+  PEER_CUDA(cudaStreamCreateWithFlags(&p->s_attn, cudaStreamNonBlocking));
   for (auto& ev : p->ev_side) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   {
     const char* e = getenv("ATOM_SIDE_WGRAD");   // 0: all block-backward kernels on one stream
@@ -848,7 +849,7 @@ void peer_reset_stats(atom_peer* p, int timing) {
 
 void peer_free(atom_peer* p) {
   cudaSetDevice(p->device);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
     if (s) cudaStreamSynchronize(s);
   if (p->comm) ncclCommDestroy(p->comm);
   for (auto ev : p->ev_side)
@@ -858,7 +859,7 @@ void peer_free(atom_peer* p) {
   for (auto ev : p->gemm_ev) cudaEventDestroy(ev);
   if (p->ev_loss) cudaEventDestroy(p->ev_loss);
   if (p->step_start) cudaEventDestroy(p->step_start);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
     if (s) cudaStreamDestroy(s);
   for (float* h : {p->h_master, p->h_m, p->h_v, p->h_loss})
     if (h) cudaFreeHost(h);

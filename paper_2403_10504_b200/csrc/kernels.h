@@ -16,7 +16,9 @@ bool gemm_simt(int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
                cudaStream_t st);
 
 // elementwise / reductions (elementwise.cu)
-template <typename T> bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st);
+// res != NULL: x <- T(x + res) in place first (a producing GEMM's residual add, moved here)
+template <typename T> bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st,
+                                  const T* res = nullptr);
 template <typename T> bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st);
 // part: fp32 chunk partials (2 x ceil(rows / RED_ROWS) x d for ln_bwd); ticket: CS_TICKETS zeroed
 // ints, one per block of 128 x (16 / sizeof(T)) columns, returned to zero by the kernel
@@ -53,6 +55,6 @@ bool attn_fa_supported(int dh);
 bool attn_tc_supported(int dh, int d);
 bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st);
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2 = nullptr);
 
 }  // namespace atom

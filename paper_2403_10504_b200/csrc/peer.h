@@ -58,6 +58,7 @@ struct atom_peer {
   // side stream, filling the SMs their tile tails (and the main stream's HBM-bound kernels) leave
   // idle; ev_side[0] forks, ev_side[1..3] mark the WFC / WO / WQKV gradients done
   cudaStream_t s_side = nullptr;
+  cudaStream_t s_attn = nullptr;        // the attention backward's dQ kernel, beside dK/dV
   cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
   bool side_wgrad = true;
   std::map<std::pair<int, int>, cudaEvent_t> op_ev;  // (kind, seg) -> completion event
