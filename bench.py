@@ -261,13 +261,24 @@ def main():
             r = torch.tensor(rates, dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(r, op=dist.ReduceOp.MIN)
             rates = [float(x) for x in r.tolist()]
+        table = m["cost_table"]
+        if world > 1 and table:   # the slowest rank's per-node times (max), so all plans agree
+            import torch.distributed as dist
+            t = torch.tensor(table, dtype=torch.int64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            table = [int(x) for x in t.tolist()]
         profiled = {"first_plan": {"C": plan.C, "act_policy": plan.act_policy, "sub_models": plan.ends()},
                     "measured_tflops": rates[0] / 1e12, "measured_h2d_GBs": rates[1] / 1e9,
-                    "measured_d2h_GBs": rates[2] / 1e9}
+                    "measured_d2h_GBs": rates[2] / 1e9,
+                    "cost_table_ms": ({"block_fwd": table[2] / 1e6, "block_bwd": table[3] / 1e6,
+                                       "head_fwd": table[-2] / 1e6, "head_bwd": table[-1] / 1e6,
+                                       "embed_fwd": table[0] / 1e6, "embed_bwd": table[1] / 1e6}
+                                      if table else None)}
         plan_tf = rates[0] / 1e12
-        cfg.peak_flops = int(rates[0])
-        cfg.d2h_bw = int(min(rates[2], args.link_gbs * 1e9))
         link_bw = int(min(rates[1], args.link_gbs * 1e9))
+        cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(rates[0]), state_budget=state_cap,
+                            lr=1e-4, warmup_steps=3000, cost_table=table or None,
+                            d2h_bw=int(min(rates[2], args.link_gbs * 1e9)))
         plan = atom.atom_plan(cfg, hbm_budget, link_bw)
     tok_step = plan.C * g.micro_batch * g.seq_len
     cfg.sync_every = adist.sync_every(world, plan.C, g.micro_batch)     # global batch 512

@@ -55,6 +55,51 @@ def lane_ms(trace: str, lane: str) -> float:
                if len(f) >= 7 and f[0] == lane) / 1000.0
 
 
+def op_means_us(trace: str, lane: str = "compute") -> dict:
+    """Mean duration (us) of each (KIND, segment) op of one lane over its micro-batches."""
+    acc = {}
+    for f in (l.split() for l in trace.splitlines()):
+        if len(f) >= 7 and f[0] == lane:
+            key = (f[1], int(f[2]))
+            n, t = acc.get(key, (0, 0.0))
+            acc[key] = (n + 1, t + float(f[6]) - float(f[5]))
+    return {k: t / n for k, (n, t) in acc.items()}
+
+
+def cost_table_from_trace(trace: str, plan, n_layer: int) -> list:
+    """Per-node {t_f_ns, t_b_ns} (one micro-batch) for atom_model_cfg.cost_table, from the traced
+    FWD / BWD op of every segment (execution time per layer, profiled).
+
+    Node order E, B_0..B_{L-1}, H. Blocks share one cost: the blocks-only segments' times divided
+    by their block counts (the backward without the re-forward, which the planner adds back under
+    ACT_RECOMPUTE, R28). E and H get what is left of their segments: FWD(1) / BWD(1)
+    minus its blocks; FWD(S) carries the head's forward and backward (run back to back per
+    micro-batch), split 1 : 2 as their FLOPs are. Returns [] when no segment holds only
+    blocks (the caller falls back to the single measured rate)."""
+    ops = op_means_us(trace)
+    ends = plan.ends()
+    S, L = len(ends), n_layer
+    lo = [0] + [e + 1 for e in ends[:-1]]
+    nblk = [sum(1 for v in range(lo[k], ends[k] + 1) if 1 <= v <= L) for k in range(S)]
+    rc = plan.act_policy == atom.ACT_RECOMPUTE
+    mids = [k for k in range(S) if all(1 <= v <= L for v in range(lo[k], ends[k] + 1))
+            and ("FWD", k + 1) in ops and ("BWD", k + 1) in ops and k < S - 1]
+    if not mids:
+        return []
+    nb = sum(nblk[k] for k in mids)
+    tf_b = sum(ops[("FWD", k + 1)] for k in mids) / nb
+    tb_b = sum(ops[("BWD", k + 1)] for k in mids) / nb - (tf_b if rc else 0.0)
+    tf_e = max(ops.get(("FWD", 1), 0.0) - nblk[0] * tf_b, 0.0) if lo[0] == 0 else 0.0
+    tb_e = max(ops.get(("BWD", 1), 0.0) - nblk[0] * (tb_b + (tf_b if rc and S > 1 else 0.0)), 0.0)
+    head = max(ops.get(("FWD", S), 0.0) - nblk[S - 1] * tf_b, 0.0)
+    ns = lambda us: max(int(round(us * 1000.0)), 1)
+    table = [ns(tf_e), ns(tb_e)]
+    for _ in range(L):
+        table += [ns(tf_b), ns(tb_b)]
+    table += [ns(head / 3.0), ns(2.0 * head / 3.0)]
+    return table
+
+
 def measure(cfg, plan, tokens_dev, device: int = 0, steps: int = 3) -> dict:
     """Profile `plan` on this GPU: run `steps` steps on device tokens and read the last step's
     trace. Returns the sustained compute rate (FLOPs executed / compute-lane busy time) and the
@@ -74,4 +119,5 @@ def measure(cfg, plan, tokens_dev, device: int = 0, steps: int = 3) -> dict:
     h2d, d2h = lane_ms(tr, "h2d"), lane_ms(tr, "d2h")
     return {"flops": executed_flops(cfg, plan) / (busy / 1000.0),
             "h2d": plan.pred_h2d_B / (h2d / 1000.0) if h2d > 0 else 0.0,
-            "d2h": plan.pred_d2h_B / (d2h / 1000.0) if d2h > 0 else 0.0}
+            "d2h": plan.pred_d2h_B / (d2h / 1000.0) if d2h > 0 else 0.0,
+            "cost_table": cost_table_from_trace(tr, plan, cfg.n_layer)}

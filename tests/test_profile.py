@@ -34,3 +34,35 @@ def test_executed_flops_counts_the_reforward():
                           act_policy=atom.ACT_STASH)
     plan_s = atom.atom_plan(cfg_s, int(178e9), int(49.7e9))
     assert aprof.executed_flops(cfg_s, plan_s) == float(plan_s.pred_flops)
+
+
+class _Plan:
+    def __init__(self, ends, policy):
+        self._ends, self.act_policy = ends, policy
+
+    def ends(self):
+        return self._ends
+
+
+def test_cost_table_from_trace_blocks_embed_head():
+    # L = 4: nodes E, B0..B3, H; segments [E, B0] [B1, B2] [B3, H]; 2 micro-batches each
+    tf, tb, emb_f, emb_b, hf, hb = 100.0, 250.0, 7.0, 11.0, 30.0, 60.0
+    lines = []
+    for mb in range(2):
+        lines.append(f"compute FWD 1 {mb} - 0 {emb_f + tf}")
+        lines.append(f"compute BWD 1 {mb} - 0 {emb_b + tb}")
+        lines.append(f"compute FWD 2 {mb} - 0 {2 * tf}")
+        lines.append(f"compute BWD 2 {mb} - 0 {2 * tb}")
+        lines.append(f"compute FWD 3 {mb} - 0 {tf + hf + hb}")   # head fwd + bwd inside FWD(S)
+        lines.append(f"compute BWD 3 {mb} - 0 {tb}")
+    t = aprof.cost_table_from_trace("\n".join(lines), _Plan([1, 3, 5], atom.ACT_STASH), 4)
+    us = [x / 1000.0 for x in t]
+    assert us[2:10] == [tf, tb] * 4
+    assert abs(us[0] - emb_f) < 1e-6 and abs(us[1] - emb_b) < 1e-6
+    assert abs(us[10] - (hf + hb) / 3) < 1e-3 and abs(us[11] - 2 * (hf + hb) / 3) < 1e-3
+    # under the re-forward policy the traced backward includes one forward per block: removed
+    lines_rc = [l.replace(f"BWD 2 ", "BWD 2 ") for l in lines]
+    lines_rc = [(f"compute BWD 2 {l.split()[3]} - 0 {2 * (tb + tf)}" if l.split()[1:3] == ["BWD", "2"] else l)
+                for l in lines_rc]
+    t_rc = aprof.cost_table_from_trace("\n".join(lines_rc), _Plan([1, 3, 5], atom.ACT_RECOMPUTE), 4)
+    assert abs(t_rc[3] / 1000.0 - tb) < 1e-6
