@@ -143,4 +143,25 @@ __device__ __forceinline__ void epi_vec8_bf16_pre(const Epi& e, long m, long n, 
   }
 }
 
+// The store / bias / bias+GELU modes' 8 outputs packed, not stored (TMA-store epilogue):
+// ov = T(acc [+ bias]); gv = T(gelu(ov)) for EPI_BIAS_GELU.
+__device__ __forceinline__ void epi_pack8_bf16(int mode, const float* acc, uint4 bias8, uint4* ov, uint4* gv) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = acc[i];
+  if (mode == EPI_BIAS || mode == EPI_BIAS_GELU) {
+    const bf16* bp = (const bf16*)&bias8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += __bfloat162float(bp[i]);
+  }
+  bf16* op = (bf16*)ov;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) op[i] = __float2bfloat16_rn(v[i]);
+  if (mode == EPI_BIAS_GELU) {
+    bf16* gp = (bf16*)gv;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) gp[i] = __float2bfloat16_rn(gelu_fast(__bfloat162float(op[i])));
+  }
+}
+
 }  // namespace atom

@@ -422,23 +422,38 @@ struct Tc2Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int EPI_BIAS_BYTES = 4 * BN * 2;   // one bias row per epilogue warp
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_BIAS_BYTES;
+  // TMA-store staging: per epilogue warp one 32 x 32 bf16 box per output (64B-swizzled rows)
+  static constexpr int STG_BOX = 32 * 32 * 2;
+  static constexpr int STG_BYTES = 4 * 2 * STG_BOX;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_BIAS_BYTES + STG_BYTES;
 };
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
                     int K, Epi epi, int group_m) {
   using Cfg = Tc2Cfg;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sstage = smem + Cfg::STAGES * Cfg::STAGE_BYTES;   // 1024-aligned: [4 warps][2 outputs] boxes
+  uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STG_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  bf16* sbias = (bf16*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);   // [4][BN]
+  bf16* sbias = (bf16*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::STG_BYTES + 256);   // [4][BN]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -582,38 +597,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
       if (fast) {
-        // interior tile: TMEM chunk c + 1 and its residual / pre-activation operands are in flight
-        // while chunk c is finished and stored
-        const bf16* xrow = epi.mode == EPI_BIAS_RES ? (const bf16*)epi.res + m * epi.ldr
-                         : epi.mode == EPI_DGELU   ? (const bf16*)epi.aux + m * epi.ldx : nullptr;
+        // interior tile, TMEM chunk c + 1 in flight while chunk c is finished.
+        // TMA-store epilogue: each warp packs its 32 rows x 32 columns of a chunk into a 64B-swizzled
+        // smem box per output and one lane stores the box (full-line writes instead of 32 scattered
+        // 16-byte pieces per instruction)
+        const bool gelu2 = epi.mode == EPI_BIAS_GELU;
+        uint8_t* stg = sstage + q * 2 * Cfg::STG_BOX;
+        const uint32_t stg0 = smem_u32(stg), stg1 = stg0 + Cfg::STG_BOX;
+        const uint32_t row_off = (uint32_t)lane * 64;
+        const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+        const int mrow = m0 + 32 * q;
         uint32_t va[32], vb[32];
-        uint4 xa[4], xb[4];
-        // chunk c's operands in (vc, xc); chunk c + 1's are loaded into (vn, xn) meanwhile
-        auto chunk = [&](int c, uint32_t (&vc)[32], uint4 (&xc)[4], uint32_t (&vn)[32], uint4 (&xn)[4]) {
-          if (c + 1 < BN / 32) {
-            tmem_ld32_nw(trow + 32 * (c + 1), vn);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              xn[j] = xrow ? *(const uint4*)(xrow + n0 + 32 * (c + 1) + 8 * j) : make_uint4(0, 0, 0, 0);
-          }
+        auto chunk = [&](int c, uint32_t (&vc)[32], uint32_t (&vn)[32]) {
+          if (c + 1 < BN / 32) tmem_ld32_nw(trow + 32 * (c + 1), vn);
+          uint4 ov[4], gv[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            float a[8];
+            float a8[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = __uint_as_float(vc[8 * j + i]);
+            for (int i = 0; i < 8; ++i) a8[i] = __uint_as_float(vc[8 * j + i]);
             const uint4 b8 = has_bias ? *(const uint4*)(sb + 32 * c + 8 * j) : make_uint4(0, 0, 0, 0);
-            epi_vec8_bf16_pre(epi, m, n0 + 32 * c + 8 * j, a, b8, xc[j]);
+            epi_pack8_bf16(epi.mode, a8, b8, &ov[j], &gv[j]);
+          }
+          if (lane == 0) bulk_wait_read0();   // the previous chunk's boxes have been read out
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t off = row_off + ((((uint32_t)j) ^ swz) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg0 + off), "r"(ov[j].x), "r"(ov[j].y),
+                         "r"(ov[j].z), "r"(ov[j].w)
+                         : "memory");
+            if (gelu2)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg1 + off), "r"(gv[j].x), "r"(gv[j].y),
+                           "r"(gv[j].z), "r"(gv[j].w)
+                           : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmO, stg0, n0 + 32 * c, mrow);
+            if (gelu2) tma_store_2d(&tmO2, stg1, n0 + 32 * c, mrow);
+            bulk_commit();
           }
           if (c + 1 < BN / 32) tmem_wait_ld();
         };
         tmem_ld32_nw(trow, va);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xa[j] = xrow ? *(const uint4*)(xrow + n0 + 8 * j) : make_uint4(0, 0, 0, 0);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < BN / 32; c += 2) {
-          chunk(c, va, xa, vb, xb);
-          chunk(c + 1, vb, xb, va, xa);
+          chunk(c, va, vb);
+          chunk(c + 1, vb, va);
         }
       } else {
 #pragma unroll 1
@@ -637,6 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
     }
   }
+  if (warp >= 4 && lane == 0) bulk_wait_all();   // TMA stores complete before the CTA retires
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
@@ -665,7 +699,7 @@ static PFN_encodeTiled get_encode() {
 
 // 2-D bf16 tensor map: inner dimension `inner` (contiguous), `outer` rows of pitch ld elements.
 static bool make_map(CUtensorMap* map, const void* base, long inner, long outer, long ld, int box_inner,
-                     int box_outer) {
+                     int box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -676,7 +710,7 @@ static bool make_map(CUtensorMap* map, const void* base, long inner, long outer,
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): inner=%ld outer=%ld ld=%ld", (int)r, inner, outer, ld);
@@ -724,6 +758,16 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
 template <bool A_MN, bool B_MN>
 static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e,
                        cudaStream_t st) {
+  // output boxes for the TMA-store epilogue (store / bias / bias+GELU modes): 32 x 32, 64B swizzle
+  CUtensorMap to, to2;
+  memset(&to, 0, sizeof to);
+  memset(&to2, 0, sizeof to2);
+  const bool tma_out = e.mode == EPI_STORE || e.mode == EPI_BIAS || e.mode == EPI_BIAS_GELU;
+  if (tma_out) {
+    if (!make_map(&to, e.out, N, M, e.ldo, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
+    if (e.mode == EPI_BIAS_GELU && !make_map(&to2, e.out2, N, M, e.ldo2, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
+  }
   auto kern = gemm_tc2_kernel<A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -732,7 +776,7 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + Tc2Cfg::BN - 1) / Tc2Cfg::BN);
   const int clusters = std::min(tiles, num_sms() / 2);
-  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 2));
+  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2));
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
