@@ -50,9 +50,87 @@ WORKLOADS = {
     "2.7b": ("2.7b", 20 * 2 ** 30, "GPT-3 2.7B (32L, d=2560, 32x80 heads, T=2048, b=8), model state capped at "
              "20 GiB (resident would need 50 GB); sub-models, C and the activation policy planned from a "
              "profiled compute rate"),
+    "13b": ("13b", 0, "GPT-3 13B (40L, d=5120, 40x128 heads, T=2048, b=4): weights and AdamW state host-resident "
+            "(236 GB of device state would be needed), swapped per sub-model through the whole HBM"),
     "small": ("small", 0, "GPT-3 Small 125M (12L, d=768), per-layer sub-models"),
     "tiny": ("tiny", 3 * 10 ** 6, "tiny GPT (4L, d=64, T=32, V=256)"),
 }
+
+
+def host_mem_available():
+    """Bytes this process may still pin: MemAvailable, capped by the cgroup limit when one is set."""
+    avail = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                avail = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    try:
+        lim = open("/sys/fs/cgroup/memory.max").read().strip()
+        if lim != "max":
+            used = int(open("/sys/fs/cgroup/memory.current").read())
+            avail = min(avail or 1 << 62, int(lim) - used)
+    except (OSError, ValueError):
+        pass
+    return avail
+
+
+def bind_to_gpu_numa(local):
+    """Run this rank on the CPUs NVML reports as local to its GPU, so the pinned host arenas are
+    first-touched on that NUMA node (8 peers over two sockets would otherwise share one memory
+    controller). No-op when NVML or the affinity call is unavailable."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(local)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
+def link_probe(local, world, nbytes=1 << 30, reps=3):
+    """Pinned host<->device rate per direction when every rank copies both ways at once (the
+    backward phase's traffic): host DRAM, not PCIe, is what several peers share (4 GPUs of one
+    socket: ~22 GB/s each way per GPU vs 49.7 alone, tools/host_bw_probe.py). Min over ranks."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    rate = 0.0
+    for _ in range(2):
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            torch.cuda.synchronize()
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            for _ in range(reps):
+                d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            for _ in range(reps):
+                h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        rate = reps * nbytes / (time.perf_counter() - t)
+    del h, h2, d, d2
+    torch.cuda.empty_cache()
+    if world > 1:
+        import torch.distributed as dist
+        r = torch.tensor([rate], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(r, op=dist.ReduceOp.MIN)
+        rate = float(r.item())
+    return rate
 
 
 def f_alg_per_token(g):
@@ -214,7 +292,8 @@ def main():
     ap.add_argument("--config", default="2.7b", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="atom", choices=["atom", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--link-gbs", type=float, default=BIDIR_GBS)
+    ap.add_argument("--link-gbs", type=float, default=0.0,
+                    help="host-link GB/s per direction the planner assumes (default: measured, all ranks at once)")
     ap.add_argument("--trace-out", default="", help="write the last step's per-op trace here (rank 0)")
     ap.add_argument("--planner-tflops", type=float, default=0.0,
                     help="compute rate the planner's cost model assumes (default: measured by a profile run)")
@@ -234,9 +313,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    numa_cpus = bind_to_gpu_numa(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # every peer pins 12 B/param (fp32 master, m, v): refuse up front rather than drive the
+    # host out of memory (all local ranks check before any of them pins)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    need = local_world * (12 * synth.n_params(g) + 4 * 2 ** 30)
+    avail = host_mem_available()
+    if avail is not None and need > avail:
+        raise SystemExit(f"bench: {local_world} peer(s) of {g.name} need {need / 1e9:.1f} GB of pinned host memory, "
+                         f"{avail / 1e9:.1f} GB available")
+    if args.link_gbs <= 0:
+        args.link_gbs = link_probe(local, world) / 1e9
     pk = peaks()
     free, total = torch.cuda.mem_get_info()
     hbm_budget = int(free - 6 * 2 ** 30)
@@ -345,6 +435,7 @@ def main():
                        "planner_tflops": plan_tf, "profile": profiled,
                        "state_budget_bytes": state_cap, "device_arena_bytes": plan.device_bytes,
                        "parallelism": f"peers{world}", "sync_every": cfg.sync_every,
+                       "link_GBs_bidir_probe": args.link_gbs, "numa_cpus": numa_cpus,
                        "l2": "inputs larger than L2 (weights/activations stream through HBM every step)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 4 * n_seq * (g.seq_len + 1),
                     "d2h_bytes_per_step": 4},
@@ -358,7 +449,11 @@ def main():
                                        round(r["ms"], 2), round(r["tflops"], 1)] for r in gemm_shapes],
                          "by_shape_fields": "M N K a_mn b_mn epilogue launches ms TFLOP/s"},
             "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
-                              "flops_per_token": f_alg_per_token(g)},
+                              "flops_per_token": f_alg_per_token(g),
+                              # the same bound with the host link as all ranks see it at once
+                              # (link_probe: host DRAM shared by the peers of one socket)
+                              "t_roof_contended_ms": 1000.0 * max(t_roof, 12 * synth.n_params(g) / (args.link_gbs * 1e9)),
+                              "frac_contended": 1000.0 * max(t_roof, 12 * synth.n_params(g) / (args.link_gbs * 1e9)) / ms_step},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
             "compute_busy_pct": compute_busy_pct(trace, st["step_ms"]),
             "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
