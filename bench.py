@@ -357,7 +357,8 @@ def main():
             t = torch.tensor(table, dtype=torch.int64, device=f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             table = [int(x) for x in t.tolist()]
-        profiled = {"first_plan": {"C": plan.C, "act_policy": plan.act_policy, "sub_models": plan.ends()},
+        profiled = {"first_plan": {"C": plan.C, "act_policy": plan.act_policy, "n_recompute": plan.n_recompute,
+                                   "sub_models": plan.ends()},
                     "measured_tflops": rates[0] / 1e12, "measured_h2d_GBs": rates[1] / 1e9,
                     "measured_d2h_GBs": rates[2] / 1e9,
                     "cost_table_ms": ({"block_fwd": table[2] / 1e6, "block_bwd": table[3] / 1e6,
@@ -431,7 +432,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_desc, "model": g.name, "global_batch": world * n_seq, "seq_len": g.seq_len,
                        "micro_batch": g.micro_batch, "C": plan.C, "sub_models": plan.ends(),
-                       "act_policy": {0: "auto", 1: "stash", 2: "recompute"}.get(plan.act_policy),
+                       "act_policy": {0: "auto", 1: "stash", 2: "recompute", 3: "hybrid"}.get(plan.act_policy),
+                       "n_recompute": plan.n_recompute,
                        "planner_tflops": plan_tf, "profile": profiled,
                        "state_budget_bytes": state_cap, "device_arena_bytes": plan.device_bytes,
                        "parallelism": f"peers{world}", "sync_every": cfg.sync_every,

@@ -136,7 +136,7 @@ def determine_C(t_fwd_segs, t_load_segs, max_C=64):
 # 2. the B200 cost model
 # ----------------------------------------------------------------------------
 FP32, BF16 = 0, 1
-ACT_AUTO, ACT_STASH, ACT_RECOMPUTE = 0, 1, 2
+ACT_AUTO, ACT_STASH, ACT_RECOMPUTE, ACT_HYBRID = 0, 1, 2, 3
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -171,8 +171,9 @@ class PlanCfg:
     d2h_bw: int = 0               # 0 = link_bw
     cost_table: Optional[List[int]] = None    # per node [t_f_ns, t_b_ns] flattened
     state_budget: int = 0         # 0 = none; else cap on R1 + NSLOT*slot (model state on device)
-    act_policy: int = ACT_AUTO    # AUTO = stash if any plan is feasible, else recompute
+    act_policy: int = ACT_AUTO    # AUTO: fewest re-forwarded blocks R = 0 (stash), 1, ..., L (reading R35)
     forced_ends: Optional[List[int]] = None
+    n_recompute: int = 0          # ACT_HYBRID: re-forward blocks 1..n_recompute (those before the last segment)
 
     @classmethod
     def from_gpt(cls, g, **kw):
@@ -266,20 +267,24 @@ def hfin_bytes(c):
     return al256(wbytes(c) * c.micro_batch * c.seq_len * c.d_model)
 
 
-def stash_bytes(c: PlanCfg, C: int, nb_last: int, S: int, policy: int = 1) -> int:
+def n_rc(c: PlanCfg, R: int, nb_last: int) -> int:
+    """Re-forwarded blocks of a plan: blocks 1..R, but never one of the interleaved last segment."""
+    return min(R, c.n_layer - nb_last)
+
+
+def stash_bytes(c: PlanCfg, C: int, nb_last: int, S: int, R: int = 0) -> int:
     """Block stashes (C micro-batches for blocks before the last segment, 1 for blocks of the
     interleaved last segment) + [M, d] activation buffers at the last segment's boundary:
     its input for all C micro-batches (S >= 2) and the final hidden state (when the last
     segment has blocks; it is the input itself when the last segment is the head alone).
-    ACT_RECOMPUTE keeps only each earlier block's input (C copies) plus one full stash entry
-    that the backward re-forward fills block by block."""
+    The first R blocks before the last segment (R = L: all of them, ACT_RECOMPUTE) keep only
+    their input (C copies); one full stash entry is then shared by their backward re-forwards."""
     L = c.n_layer
     nh = 1 if S == 1 else (C if nb_last == 0 else C + 1)
     nb_pre = L - nb_last
-    if policy == ACT_RECOMPUTE:
-        return (hfin_bytes(c) * C * nb_pre + stash_blk_bytes(c) * nb_last + hfin_bytes(c) * nh
-                + (stash_blk_bytes(c) if nb_pre > 0 else 0))
-    return stash_blk_bytes(c) * (C * nb_pre + nb_last) + hfin_bytes(c) * nh
+    r = n_rc(c, R, nb_last)
+    return (stash_blk_bytes(c) * (C * (nb_pre - r) + nb_last) + hfin_bytes(c) * C * r + hfin_bytes(c) * nh
+            + (stash_blk_bytes(c) if r > 0 else 0))
 
 
 RED_ROWS = 128   # rows per partial-sum chunk in the deterministic column reductions
@@ -328,6 +333,7 @@ class Plan:
     pred_d2h_B: int
     pred_flops: int
     act_policy: int = ACT_STASH
+    n_recompute: int = 0
     pred_step_ns: int = 0
     pred_hidden_ppm: int = 0
 
@@ -346,15 +352,18 @@ def _seg_tables(c: PlanCfg, k: Costs):
 class Evaluator:
     """Feasibility of a partition under the cost model (memory + per-phase overlap)."""
 
-    def __init__(self, c: PlanCfg, budget: int, link_bw: int, policy: int = ACT_STASH):
-        self.c, self.budget, self.policy = c, budget, policy
+    def __init__(self, c: PlanCfg, budget: int, link_bw: int, R: int = 0):
+        """R: blocks 1..R are re-forwarded inside their backward (those before the last segment)."""
+        self.c, self.budget, self.R = c, budget, R
         self.k = node_costs(c, link_bw)
         self.pre, self.n = _seg_tables(c, self.k)
         self.L = c.n_layer
+        tbx = [self.k.tbr[v] if 1 <= v <= R else self.k.tb[v] for v in range(self.n)]
+        self.pre["tbx"] = _seg_tables(c, dataclasses.replace(self.k, tbr=tbx))[0]["tbr"]
 
     def tbn(self, i, j):
-        """backward time of a segment that is not the last one (re-forward under recompute)"""
-        return self.s("tbr" if self.policy == ACT_RECOMPUTE else "tb", i, j)
+        """backward time of a segment that is not the last one (its re-forwarded blocks included)"""
+        return self.s("tbx", i, j)
 
     def s(self, name, i, j):
         p = self.pre[name]
@@ -374,7 +383,7 @@ class Evaluator:
 
     def mem_fixed(self, C, e1, il, S, Q):
         """device bytes for first segment [0..e1], last [il..n-1], S segments, max need Q."""
-        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1), S, self.policy)
+        return (self.r1(e1) + nslot(S) * al256(Q) + stash_bytes(self.c, C, self.nblocks(il, self.n - 1), S, self.R)
                 + work_bytes(self.c, C))
 
     def pair_ok(self, C, a, b, last):
@@ -437,7 +446,9 @@ class Evaluator:
         S = len(ends)
         Q = self.slot_need(ends)
         nb_last = self.nblocks(segs[-1][0], self.n - 1)
-        st = stash_bytes(c, C, nb_last, S, self.policy)
+        st = stash_bytes(c, C, nb_last, S, self.R)
+        r = n_rc(c, self.R, nb_last)
+        pol = ACT_STASH if r == 0 else (ACT_RECOMPUTE if r == self.L - nb_last else ACT_HYBRID)
         wk = work_bytes(c, C)
         r1 = self.r1(ends[0])
         M = c.micro_batch * c.seq_len
@@ -447,12 +458,17 @@ class Evaluator:
         d2h = sum(12 * p for p in P[1:])
         return Plan(S, list(ends), C, nslot(S), (S - 1) * wbytes(c) * M * c.d_model, r1, al256(Q), st, wk,
                     r1 + nslot(S) * al256(Q) + st + wk, h2d, d2h,
-                    C * sum(3 * f for f in self.k.ff), self.policy)
+                    C * sum(3 * f for f in self.k.ff), pol, r)
 
 
 def policies(c: PlanCfg):
-    """ACT_AUTO tries the full stash first and falls back to recompute (reading R28)."""
-    return [ACT_STASH, ACT_RECOMPUTE] if c.act_policy == ACT_AUTO else [c.act_policy]
+    """Re-forward counts R to try, in order. ACT_AUTO: R = 0 (full stash), 1, ..., L (R = L
+    re-forwards every block before the last segment, ACT_RECOMPUTE): every re-forwarded block
+    costs its forward again, so the fewest that make a plan feasible wins, then the smallest C
+    (readings R28, R35)."""
+    if c.act_policy == ACT_AUTO:
+        return list(range(c.n_layer + 1))
+    return {ACT_STASH: [0], ACT_RECOMPUTE: [c.n_layer], ACT_HYBRID: [c.n_recompute]}[c.act_policy]
 
 
 def brute_force_plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
@@ -510,7 +526,7 @@ def _dp_for_C(ev: Evaluator, C: int):
             # admissible last segments [il..n-1]
             term = [il for il in range(e1 + 2, n)
                     if ev.need(il, n - 1) <= Q
-                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1), 3, ev.policy) <= rem]
+                    and stash_bytes(ev.c, C, ev.nblocks(il, n - 1), 3, ev.R) <= rem]
             if not term:
                 continue
             tset = set(term)
@@ -572,13 +588,18 @@ def dp_plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
     return None
 
 
+def plan_R(c: PlanCfg, p: Plan) -> int:
+    """The R an evaluator needs to reproduce plan p (its re-forwarded blocks are 1..n_recompute)."""
+    return p.n_recompute
+
+
 def plan(c: PlanCfg, budget: int, link_bw: int) -> Optional[Plan]:
     """The planner's answer: the optimum of the cost model (exact DP), with the
     schedule simulation attached."""
     p = dp_plan(c, budget, link_bw)
     if p is not None:
         from . import schedule
-        ev = Evaluator(c, budget, link_bw, p.act_policy)
+        ev = Evaluator(c, budget, link_bw, plan_R(c, p))
         sim = schedule.simulate(schedule.emit(p.n_seg, p.C, False), ev, p)
         p.pred_step_ns, p.pred_hidden_ppm = sim["makespan"], sim["hidden_ppm"]
     return p

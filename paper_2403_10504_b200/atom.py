@@ -22,7 +22,7 @@ lib = C.CDLL(LIB_PATH)
 ATOM_OK, ATOM_E_INVALID, ATOM_E_INFEASIBLE, ATOM_E_CAPACITY = 0, -1, -2, -3
 ATOM_E_CUDA, ATOM_E_NCCL, ATOM_E_OOM, ATOM_E_STATE = -4, -5, -6, -7
 FP32, BF16 = 0, 1
-ACT_AUTO, ACT_STASH, ACT_RECOMPUTE = 0, 1, 2
+ACT_AUTO, ACT_STASH, ACT_RECOMPUTE, ACT_HYBRID = 0, 1, 2, 3
 MAX_SEG = 256
 IMPL_TC, IMPL_SIMT = 0, 1
 EPI_STORE, EPI_BIAS, EPI_BIAS_RES, EPI_BIAS_GELU, EPI_DGELU, EPI_ACC_F32 = range(6)
@@ -77,7 +77,7 @@ class ModelCfg(C.Structure):
                 ("cost_table", C.POINTER(C.c_int64)), ("forced_ends", C.POINTER(C.c_int32)),
                 ("n_forced", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("eps", C.c_float), ("weight_decay", C.c_float), ("warmup_steps", C.c_int32),
-                ("sync_every", C.c_int32)]
+                ("sync_every", C.c_int32), ("n_recompute", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -86,20 +86,20 @@ class Plan(C.Structure):
                 ("stash_bytes", C.c_int64), ("work_bytes", C.c_int64), ("device_bytes", C.c_int64),
                 ("pred_step_ns", C.c_int64), ("pred_hidden_ppm", C.c_int64), ("pred_h2d_B", C.c_int64),
                 ("pred_d2h_B", C.c_int64), ("pred_flops", C.c_int64), ("hbm_budget", C.c_int64),
-                ("link_bw", C.c_int64)]
+                ("link_bw", C.c_int64), ("n_recompute", C.c_int32), ("reserved", C.c_int32)]
 
     def ends(self):
         return [self.seg_end[i] for i in range(self.n_seg)]
 
     def as_dict(self):
-        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "seg_end"}
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("seg_end", "reserved")}
         d["seg_end"] = self.ends()
         return d
 
 
 def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 10 ** 12, d2h_bw=0,
              state_budget=0, cost_table=None, forced_ends=None, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8,
-             weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0):
+             weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0, n_recompute=0):
     """atom_model_cfg from a synth.GPTConfig-like object (keeps ctypes arrays alive on the struct)."""
     c = ModelCfg()
     c.n_layer, c.d_model, c.n_head, c.seq_len, c.vocab, c.micro_batch = (
@@ -116,7 +116,7 @@ def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 1
         c.forced_ends = C.cast(arr, C.POINTER(C.c_int32))
         c.n_forced = len(forced_ends)
     c.lr, c.beta1, c.beta2, c.eps, c.weight_decay = lr, beta1, beta2, eps, weight_decay
-    c.warmup_steps, c.sync_every = warmup_steps, sync_every
+    c.warmup_steps, c.sync_every, c.n_recompute = warmup_steps, sync_every, n_recompute
     return c
 
 

@@ -88,6 +88,7 @@ atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan,
   p->C = plan->C;
   p->nranks = nranks;
   p->policy = plan->act_policy;
+  p->n_recompute = plan->n_recompute;
   p->rank = rank;
   p->seg_of_node.assign(dm.n_nodes, 0);
   int lo = 0;

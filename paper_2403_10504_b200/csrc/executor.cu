@@ -608,14 +608,17 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   // ACT_RECOMPUTE, C input checkpoints; then the re-forward entry; then the boundary buffers
   p->stash = a;
   int64_t off = 0;
-  const bool rc = p->policy == ATOM_ACT_RECOMPUTE;
+  // blocks 1..n_recompute (never the last segment's) are re-forwarded: input checkpoints only
+  bool any_rc = false;
   for (int l = 0; l < dm.L; ++l) {
     const bool last = p->seg_of_node[l + 1] == p->S;
+    const bool rc = !last && l < p->n_recompute;
+    any_rc |= rc;
     p->blk_off.push_back(off);
-    p->blk_full.push_back(!rc || last);
-    off += (!rc || last) ? (last ? 1 : p->C) * stash_blk_bytes(dm) : (int64_t)p->C * hfin_bytes(dm);
+    p->blk_full.push_back(!rc);
+    off += !rc ? (last ? 1 : p->C) * stash_blk_bytes(dm) : (int64_t)p->C * hfin_bytes(dm);
   }
-  if (rc && dm.L > p->nb_last) {
+  if (any_rc) {
     p->rc_off = off;
     off += stash_blk_bytes(dm);
   }

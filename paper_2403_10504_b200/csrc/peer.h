@@ -31,6 +31,7 @@ struct atom_peer {
   std::map<uint8_t*, cudaEvent_t> rel_of;
   uint8_t* stash = nullptr;
   int policy = ATOM_ACT_STASH;          // resolved activation policy of the plan
+  int n_recompute = 0;                  // blocks 1..n_recompute re-forward inside their backward
   std::vector<int64_t> blk_off;         // per block: byte offset (from stash) of its first stash entry
   std::vector<char> blk_full;           // per block: full entries (1) or input checkpoints only (0)
   int64_t rc_off = -1;                  // byte offset of the entry the backward re-forward fills

@@ -118,13 +118,15 @@ int64_t stash_blk_bytes(const ModelDims& dm) {
          al256(8 * M) + al256(8 * M) + al256(4LL * dm.b * dm.h * dm.T);
 }
 int64_t hfin_bytes(const ModelDims& dm) { return al256((int64_t)dm.wb * dm.M * dm.d); }
-int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int policy) {
+int n_rc(const ModelDims& dm, int R, int nb_last) { return std::min(R, dm.L - nb_last); }
+// re-forwarded blocks (1..R, none of the last segment) keep C input checkpoints and share one
+// entry their backward re-forward fills; the others keep C full entries (1 in the last segment)
+int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int R) {
   const int64_t nh = S == 1 ? 1 : (nb_last == 0 ? C : C + 1);
   const int64_t nb_pre = dm.L - nb_last;
-  if (policy == ATOM_ACT_RECOMPUTE)  // block inputs only + one entry the re-forward fills
-    return hfin_bytes(dm) * C * nb_pre + stash_blk_bytes(dm) * nb_last + hfin_bytes(dm) * nh +
-           (nb_pre > 0 ? stash_blk_bytes(dm) : 0);
-  return stash_blk_bytes(dm) * ((int64_t)C * nb_pre + nb_last) + hfin_bytes(dm) * nh;
+  const int64_t r = n_rc(dm, R, nb_last);
+  return stash_blk_bytes(dm) * ((int64_t)C * (nb_pre - r) + nb_last) + hfin_bytes(dm) * C * r + hfin_bytes(dm) * nh +
+         (r > 0 ? stash_blk_bytes(dm) : 0);
 }
 int64_t work_bytes(const ModelDims& dm, int C) {
   const int64_t ab = dm.wb, d = dm.d, V = dm.V, T = dm.T, b = dm.b, h = dm.h, M = dm.M;
@@ -148,22 +150,24 @@ struct Eval {
   const atom_model_cfg& c;
   const ModelDims& dm;
   int64_t budget;
-  int policy;
+  int R;   // blocks 1..R are re-forwarded inside their backward (those before the last segment)
   Costs k;
   int n;
-  std::vector<int64_t> pP, ptf, ptb, ptbr, ptlf, ptlb, ptmv, pts;
-  Eval(const atom_model_cfg& c_, const ModelDims& dm_, int64_t budget_, int64_t link, int policy_)
-      : c(c_), dm(dm_), budget(budget_), policy(policy_), k(node_costs(c_, dm_, link)), n(dm_.n_nodes) {
+  std::vector<int64_t> pP, ptf, ptb, ptbx, ptlf, ptlb, ptmv, pts;
+  Eval(const atom_model_cfg& c_, const ModelDims& dm_, int64_t budget_, int64_t link, int R_)
+      : c(c_), dm(dm_), budget(budget_), R(R_), k(node_costs(c_, dm_, link)), n(dm_.n_nodes) {
     auto pre = [&](const std::vector<int64_t>& v, std::vector<int64_t>& p) {
       p.assign(v.size() + 1, 0);
       for (size_t i = 0; i < v.size(); ++i) p[i + 1] = p[i] + v[i];
     };
-    pre(k.P, pP); pre(k.tf, ptf); pre(k.tb, ptb); pre(k.tbr, ptbr); pre(k.tlf, ptlf); pre(k.tlb, ptlb);
+    std::vector<int64_t> tbx(k.tb);
+    for (int v = 1; v <= std::min(R, dm.L); ++v) tbx[v] = k.tbr[v];
+    pre(k.P, pP); pre(k.tf, ptf); pre(k.tb, ptb); pre(tbx, ptbx); pre(k.tlf, ptlf); pre(k.tlb, ptlb);
     pre(k.tmv, ptmv); pre(k.ts, pts);
   }
   static int64_t s(const std::vector<int64_t>& p, int i, int j) { return p[j + 1] - p[i]; }
-  // backward time of a segment that is not the last one (re-forward under recompute)
-  int64_t tbn(int i, int j) const { return s(policy == ATOM_ACT_RECOMPUTE ? ptbr : ptb, i, j); }
+  // backward time of a segment that is not the last one (its re-forwarded blocks included)
+  int64_t tbn(int i, int j) const { return s(ptbx, i, j); }
   int64_t need(int i, int j) const { return seg_need(dm, s(pP, i, j)); }
   int nblocks(int i, int j) const {
     int lo = std::max(i, 1), hi = std::min(j, dm.L);
@@ -193,7 +197,7 @@ struct Eval {
   int64_t device_bytes(int C, const std::vector<int>& ends) const {
     const int S = (int)ends.size();
     const int il = S == 1 ? 0 : ends[S - 2] + 1;
-    return r1(ends[0]) + nslot_for(S) * al256(slot_need(ends)) + stash_bytes(dm, C, nblocks(il, n - 1), S, policy) +
+    return r1(ends[0]) + nslot_for(S) * al256(slot_need(ends)) + stash_bytes(dm, C, nblocks(il, n - 1), S, R) +
            work_bytes(dm, C);
   }
   // nullptr if feasible, else the first violated constraint
@@ -244,7 +248,7 @@ bool dp_for_C(const Eval& ev, int C, std::vector<int>* best_out) {
       std::vector<char> term(n, 0);
       bool any = false;
       for (int il = e1 + 2; il < n; ++il)
-        if (ev.need(il, n - 1) <= Q && stash_bytes(ev.dm, C, ev.nblocks(il, n - 1), 3, ev.policy) <= rem) {
+        if (ev.need(il, n - 1) <= Q && stash_bytes(ev.dm, C, ev.nblocks(il, n - 1), 3, ev.R) <= rem) {
           term[il] = 1;
           any = true;
         }
@@ -417,7 +421,7 @@ static void simulate(const Eval& ev, const std::vector<int>& ends, const std::ve
     int64_t dur = 0;
     switch (o.kind) {
       case K_FWD: dur = seg(ev.ptf, o.seg); break;
-      case K_BWD: dur = o.seg == S ? seg(ev.ptb, o.seg) : seg(ev.ptbr.empty() || ev.policy != ATOM_ACT_RECOMPUTE ? ev.ptb : ev.ptbr, o.seg); break;
+      case K_BWD: dur = o.seg == S ? seg(ev.ptb, o.seg) : seg(ev.ptbx, o.seg); break;
       case K_LOAD_F: dur = seg(ev.ptlf, o.seg); break;
       case K_LOAD_B: dur = (o.seg == S && S >= 2) ? seg(ev.ptmv, o.seg) : seg(ev.ptlb, o.seg); break;
       case K_STORE: dur = seg(ev.pts, o.seg); break;
@@ -455,8 +459,10 @@ static void fill_plan(const Eval& ev, int C, const std::vector<int>& ends, int64
   p->cut_bytes = (int64_t)(S - 1) * dm.wb * dm.M * dm.d;
   p->r1_bytes = ev.r1(ends[0]);
   p->slot_bytes = al256(ev.slot_need(ends));
-  p->stash_bytes = stash_bytes(dm, C, ev.nblocks(il, ev.n - 1), S, ev.policy);
-  p->act_policy = ev.policy;
+  p->stash_bytes = stash_bytes(dm, C, ev.nblocks(il, ev.n - 1), S, ev.R);
+  const int r = n_rc(dm, ev.R, ev.nblocks(il, ev.n - 1));
+  p->n_recompute = r;
+  p->act_policy = r == 0 ? ATOM_ACT_STASH : (r == dm.L - ev.nblocks(il, ev.n - 1) ? ATOM_ACT_RECOMPUTE : ATOM_ACT_HYBRID);
   p->work_bytes = work_bytes(dm, C);
   p->device_bytes = p->r1_bytes + p->nslot * p->slot_bytes + p->stash_bytes + p->work_bytes;
   std::vector<int64_t> P;
@@ -494,15 +500,21 @@ bool check_plan(const atom_model_cfg& c, const atom_plan_t& p) {
       set_error("invalid plan: segment ends must ascend");
       return false;
     }
-  if (p.act_policy != ATOM_ACT_STASH && p.act_policy != ATOM_ACT_RECOMPUTE) {
-    set_error("invalid plan: act_policy");
-    return false;
-  }
-  Eval ev(c, dm, p.hbm_budget > 0 ? p.hbm_budget : 1, p.link_bw > 0 ? p.link_bw : 1, p.act_policy);
   const int S = p.n_seg;
   const int il = S == 1 ? 0 : ends[S - 2] + 1;
+  {
+    const int nb_last = std::max(0, dm.L - std::max(il, 1) + 1);   // blocks of the last segment
+    const int nb_pre = dm.L - nb_last;
+    const int r = p.n_recompute;
+    const int want = r == 0 ? ATOM_ACT_STASH : (r == nb_pre ? ATOM_ACT_RECOMPUTE : ATOM_ACT_HYBRID);
+    if (r < 0 || r > nb_pre || p.act_policy != want) {
+      set_error("invalid plan: act_policy / n_recompute");
+      return false;
+    }
+  }
+  Eval ev(c, dm, p.hbm_budget > 0 ? p.hbm_budget : 1, p.link_bw > 0 ? p.link_bw : 1, p.n_recompute);
   if (ev.r1(ends[0]) != p.r1_bytes || al256(ev.slot_need(ends)) != p.slot_bytes || nslot_for(S) != p.nslot ||
-      stash_bytes(dm, p.C, ev.nblocks(il, n - 1), S, p.act_policy) != p.stash_bytes || work_bytes(dm, p.C) != p.work_bytes ||
+      stash_bytes(dm, p.C, ev.nblocks(il, n - 1), S, p.n_recompute) != p.stash_bytes || work_bytes(dm, p.C) != p.work_bytes ||
       p.r1_bytes + p.nslot * p.slot_bytes + p.stash_bytes + p.work_bytes != p.device_bytes) {
     set_error("invalid plan: arena sizes do not match this configuration (plan made for another cfg?)");
     return false;
@@ -522,8 +534,9 @@ bool make_plan(const atom_model_cfg& c, int64_t budget, int64_t link, atom_plan_
     set_error("invalid config: C / max_C out of range");
     return false;
   }
-  if (c.act_policy != ATOM_ACT_AUTO && c.act_policy != ATOM_ACT_STASH && c.act_policy != ATOM_ACT_RECOMPUTE) {
-    set_error("invalid config: act_policy");
+  if (c.act_policy < ATOM_ACT_AUTO || c.act_policy > ATOM_ACT_HYBRID ||
+      (c.act_policy == ATOM_ACT_HYBRID && (c.n_recompute < 0 || c.n_recompute > dm.L))) {
+    set_error("invalid config: act_policy / n_recompute");
     return false;
   }
   std::vector<int> forced;
@@ -540,10 +553,13 @@ bool make_plan(const atom_model_cfg& c, int64_t budget, int64_t link, atom_plan_
   const int c_lo = c.C > 0 ? c.C : 1, c_hi = c.C > 0 ? c.C : maxC;
   const char* first_violation = nullptr;
   int bad_pair = 0;
-  // ACT_AUTO: the full stash if any plan is feasible, else re-forward inside the backward
+  // re-forward counts R to try: ACT_AUTO the fewest (0 = full stash, ..., L = every block before
+  // the last segment), each over C ascending (R35)
   std::vector<int> pols;
-  if (c.act_policy == ATOM_ACT_AUTO) pols = {ATOM_ACT_STASH, ATOM_ACT_RECOMPUTE};
-  else pols = {c.act_policy};
+  if (c.act_policy == ATOM_ACT_AUTO)
+    for (int r = 0; r <= dm.L; ++r) pols.push_back(r);
+  else
+    pols = {c.act_policy == ATOM_ACT_STASH ? 0 : (c.act_policy == ATOM_ACT_RECOMPUTE ? dm.L : c.n_recompute)};
   for (int pol : pols) {
     Eval ev(c, dm, budget, link, pol);
     for (int C = c_lo; C <= c_hi; ++C) {

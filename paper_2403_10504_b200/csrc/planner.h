@@ -53,7 +53,8 @@ Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw);
 int64_t seg_need(const ModelDims& dm, int64_t P_seg);
 int64_t stash_blk_bytes(const ModelDims& dm);
 int64_t hfin_bytes(const ModelDims& dm);
-int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int policy);
+int n_rc(const ModelDims& dm, int R, int nb_last);
+int64_t stash_bytes(const ModelDims& dm, int C, int nb_last, int S, int R);
 int64_t work_bytes(const ModelDims& dm, int C);
 int nslot_for(int S);
 

@@ -36,17 +36,12 @@ def compute_span_ms(trace: str) -> float:
 
 def executed_flops(g, plan) -> float:
     """FLOPs one step executes: 6 N-style model FLOPs per token (plan.pred_flops) plus the
-    re-forward of every block outside the last segment under ACT_RECOMPUTE (R28:
-    the QKV, attention-projection and fc GEMMs, 16 d^2 per token, and the attention forward,
+    re-forward of the plan's n_recompute blocks (R28, R35: the QKV,
+    attention-projection and fc GEMMs, 16 d^2 per token, and the attention forward,
     2 d (T + 1) per token)."""
-    fl = float(plan.pred_flops)
-    if plan.act_policy == atom.ACT_RECOMPUTE:
-        ends = plan.ends()
-        L, d, T = g.n_layer, g.d_model, g.seq_len
-        nb_last = L - ends[-2] if len(ends) >= 2 and ends[-2] < L else 0
-        tokens = plan.C * g.micro_batch * T
-        fl += (L - nb_last) * tokens * (16.0 * d * d + 2.0 * d * (T + 1))
-    return fl
+    d, T = g.d_model, g.seq_len
+    tokens = plan.C * g.micro_batch * T
+    return float(plan.pred_flops) + plan.n_recompute * tokens * (16.0 * d * d + 2.0 * d * (T + 1))
 
 
 def lane_ms(trace: str, lane: str) -> float:
@@ -71,8 +66,8 @@ def cost_table_from_trace(trace: str, plan, n_layer: int) -> list:
     FWD / BWD op of every segment (execution time per layer, profiled).
 
     Node order E, B_0..B_{L-1}, H. Blocks share one cost: the blocks-only segments' times divided
-    by their block counts (the backward without the re-forward, which the planner adds back under
-    ACT_RECOMPUTE, R28). E and H get what is left of their segments: FWD(1) / BWD(1)
+    by their block counts (the backward without the re-forwards of the plan's n_recompute blocks,
+    which the planner adds back, R28, R35). E and H get what is left of their segments: FWD(1) / BWD(1)
     minus its blocks; FWD(S) carries the head's forward and backward (run back to back per
     micro-batch), split 1 : 2 as their FLOPs are. Returns [] when no segment holds only
     blocks (the caller falls back to the single measured rate)."""
@@ -81,16 +76,18 @@ def cost_table_from_trace(trace: str, plan, n_layer: int) -> list:
     S, L = len(ends), n_layer
     lo = [0] + [e + 1 for e in ends[:-1]]
     nblk = [sum(1 for v in range(lo[k], ends[k] + 1) if 1 <= v <= L) for k in range(S)]
-    rc = plan.act_policy == atom.ACT_RECOMPUTE
+    # re-forwarded blocks per segment: blocks 1..n_recompute
+    nrc = [sum(1 for v in range(lo[k], ends[k] + 1) if 1 <= v <= plan.n_recompute) if k < S - 1 else 0
+           for k in range(S)]
     mids = [k for k in range(S) if all(1 <= v <= L for v in range(lo[k], ends[k] + 1))
             and ("FWD", k + 1) in ops and ("BWD", k + 1) in ops and k < S - 1]
     if not mids:
         return []
     nb = sum(nblk[k] for k in mids)
     tf_b = sum(ops[("FWD", k + 1)] for k in mids) / nb
-    tb_b = sum(ops[("BWD", k + 1)] for k in mids) / nb - (tf_b if rc else 0.0)
+    tb_b = (sum(ops[("BWD", k + 1)] for k in mids) - tf_b * sum(nrc[k] for k in mids)) / nb
     tf_e = max(ops.get(("FWD", 1), 0.0) - nblk[0] * tf_b, 0.0) if lo[0] == 0 else 0.0
-    tb_e = max(ops.get(("BWD", 1), 0.0) - nblk[0] * (tb_b + (tf_b if rc and S > 1 else 0.0)), 0.0)
+    tb_e = max(ops.get(("BWD", 1), 0.0) - nblk[0] * tb_b - nrc[0] * tf_b, 0.0)
     head = max(ops.get(("FWD", S), 0.0) - nblk[S - 1] * tf_b, 0.0)
     ns = lambda us: max(int(round(us * 1000.0)), 1)
     table = [ns(tf_e), ns(tb_e)]

@@ -23,10 +23,10 @@ MINI = synth.GPTConfig("mini", n_layer=3, d_model=128, n_head=2, seq_len=128, vo
 HYPER = oadamw.AdamWHyper(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, warmup_steps=0)
 
 
-def make_peer(g, dtype, C, ends=None, init=None, seed=0, sync_every=0, policy=0):
+def make_peer(g, dtype, C, ends=None, init=None, seed=0, sync_every=0, policy=0, n_recompute=0):
     cfg = atom.make_cfg(g, dtype=dtype, C_=C, overlap_check=0, forced_ends=ends, lr=HYPER.lr, beta1=HYPER.beta1,
                         beta2=HYPER.beta2, eps=HYPER.eps, weight_decay=HYPER.weight_decay, warmup_steps=0,
-                        sync_every=sync_every, act_policy=policy)
+                        sync_every=sync_every, act_policy=policy, n_recompute=n_recompute)
     plan = atom.atom_plan(cfg, 10 ** 11, 10 ** 10)
     if ends is not None:
         assert plan.ends() == list(ends)
@@ -51,14 +51,18 @@ def per_tensor_rel(a, b, g):
     return out
 
 
-@pytest.mark.parametrize("g,ends,pol", [(TINY, None, 0), (TINY, [2, 5], 0), (TINY, [1, 2, 3, 4, 5], 0),
-                                         (MINI, [1, 2, 4], 0), (MINI, [0, 2, 4], 2)],
-                         ids=["tiny-resident", "tiny-2seg", "tiny-5seg", "mini-3seg", "mini-3seg-recompute"])
-def test_fp32_step_matches_oracle(g, ends, pol):
+@pytest.mark.parametrize("g,ends,pol,nrc", [(TINY, None, 0, 0), (TINY, [2, 5], 0, 0), (TINY, [1, 2, 3, 4, 5], 0, 0),
+                                             (MINI, [1, 2, 4], 0, 0), (MINI, [0, 2, 4], 2, 0),
+                                             (MINI, [0, 2, 4], 3, 1)],
+                         ids=["tiny-resident", "tiny-2seg", "tiny-5seg", "mini-3seg", "mini-3seg-recompute",
+                              "mini-3seg-hybrid"])
+def test_fp32_step_matches_oracle(g, ends, pol, nrc):
     C = 2
     init = synth.init_params(g, seed=1234, perturb=True)
     toks = batches(g, C, 2)
-    peer = make_peer(g, atom.FP32, C, ends, init, policy=pol)
+    peer = make_peer(g, atom.FP32, C, ends, init, policy=pol, n_recompute=nrc)
+    if pol == atom.ACT_HYBRID:
+        assert peer.plan.n_recompute == nrc
     ref = opeers.Peer(g, init.astype(np.float64), HYPER)
     for s in range(2):
         loss = peer.step(toks[s])
@@ -86,9 +90,12 @@ def test_swapped_equals_resident_bit_exact(dtype, g, plans):
     base_losses = [res.step(t) for t in toks]
     base = res.params()
     res.destroy()
-    # every plan with the full stash, and with block re-forward in the backward (ACT_RECOMPUTE)
-    for ends, pol in [(e, atom.ACT_STASH) for e in plans] + [(e, atom.ACT_RECOMPUTE) for e in plans]:
-        p = make_peer(g, dt, C, ends, init, policy=pol)
+    # every plan with the full stash, with block re-forward in the backward (ACT_RECOMPUTE), and
+    # with the re-forward of block 1 only (ACT_HYBRID, when the plan has another earlier block)
+    runs = [(e, atom.ACT_STASH, 0) for e in plans] + [(e, atom.ACT_RECOMPUTE, 0) for e in plans]
+    runs += [(e, atom.ACT_HYBRID, 1) for e in plans if e[-2] >= 2]
+    for ends, pol, nrc in runs:
+        p = make_peer(g, dt, C, ends, init, policy=pol, n_recompute=nrc)
         losses = [p.step(t) for t in toks]
         got = p.params()
         assert losses == base_losses, (ends, pol, losses, base_losses)

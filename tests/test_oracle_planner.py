@@ -6,6 +6,7 @@
 * Algorithm 1 (literal) = brute force on >= 200 random chains.
 * The exact DP = brute force over all partitions x all C.
 """
+import dataclasses
 import os
 import random
 
@@ -139,7 +140,8 @@ def _rand_plan_cfg(rng):
                    max_C=rng.randint(1, 6), overlap_check=rng.choice([0, 1, 1, 1]))
     if rng.random() < 0.4:
         c.state_budget = rng.randint(10 ** 4, 10 ** 7)
-    c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE])
+    c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE, pl.ACT_HYBRID])
+    c.n_recompute = rng.randint(0, L)
     if rng.random() < 0.7:
         tf = [0] + [rng.randint(1, 400) for _ in range(n - 1)]
         c.cost_table = sum(([t, 2 * t + rng.randint(0, 50)] for t in tf), [])
@@ -225,9 +227,17 @@ def test_full_stash_2p7b_needs_more_link_than_pcie():
     assert pl.dp_plan(c, 178 * 10 ** 9, 50 * 10 ** 9) is None
     # ACT_AUTO falls back to re-forwarding blocks inside the backward (reading R28)
     c.act_policy = pl.ACT_AUTO
+    c.act_policy = pl.ACT_RECOMPUTE
     p = pl.dp_plan(c, 178 * 10 ** 9, 50 * 10 ** 9)
     assert p is not None and p.act_policy == pl.ACT_RECOMPUTE and p.n_seg >= 3
-    ev = pl.Evaluator(c, 178 * 10 ** 9, 50 * 10 ** 9, pl.ACT_RECOMPUTE)
+    ev = pl.Evaluator(c, 178 * 10 ** 9, 50 * 10 ** 9, c.n_layer)
     assert ev.violation(p.C, p.seg_end) is None
     # the stash keeps block inputs only: far below the full stash at the same C
-    assert p.stash_bytes < pl.stash_bytes(c, p.C, 0, p.n_seg, pl.ACT_STASH) / 4
+    assert p.stash_bytes < pl.stash_bytes(c, p.C, 0, p.n_seg, 0) / 4
+    # ACT_AUTO re-forwards the fewest blocks that make a plan feasible (reading R35): some, not all
+    c.act_policy = pl.ACT_AUTO
+    q = pl.dp_plan(c, 178 * 10 ** 9, 50 * 10 ** 9)
+    assert q is not None and q.act_policy == pl.ACT_HYBRID and 0 < q.n_recompute < c.n_layer
+    assert pl.Evaluator(c, 178 * 10 ** 9, 50 * 10 ** 9, q.n_recompute - 1).violation(q.C, q.seg_end) is not None
+    assert pl.dp_plan(dataclasses.replace(c, act_policy=pl.ACT_HYBRID, n_recompute=q.n_recompute - 1),
+                      178 * 10 ** 9, 50 * 10 ** 9) is None

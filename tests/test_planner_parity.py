@@ -17,7 +17,8 @@ def _both(c: pl.PlanCfg, budget, link):
     g = synth.GPTConfig("x", c.n_layer, c.d_model, c.n_head, c.seq_len, c.vocab, c.micro_batch)
     ac = atom.make_cfg(g, dtype=c.dtype, C_=c.C, max_C=c.max_C, overlap_check=c.overlap_check,
                        peak_flops=c.peak_flops, d2h_bw=c.d2h_bw, state_budget=c.state_budget,
-                       cost_table=c.cost_table, forced_ends=c.forced_ends, act_policy=c.act_policy)
+                       cost_table=c.cost_table, forced_ends=c.forced_ends, act_policy=c.act_policy,
+                       n_recompute=c.n_recompute)
     want = pl.plan(c, budget, link)
     try:
         got = atom.atom_plan(ac, budget, link)
@@ -31,7 +32,7 @@ def _both(c: pl.PlanCfg, budget, link):
 
 def _same(want: pl.Plan, got: atom.Plan):
     assert got.ends() == want.seg_end and got.C == want.C and got.n_seg == want.n_seg
-    for f in ("nslot", "act_policy", "cut_bytes", "r1_bytes", "slot_bytes", "stash_bytes", "work_bytes", "device_bytes",
+    for f in ("nslot", "act_policy", "n_recompute", "cut_bytes", "r1_bytes", "slot_bytes", "stash_bytes", "work_bytes", "device_bytes",
               "pred_h2d_B", "pred_d2h_B", "pred_flops", "pred_step_ns", "pred_hidden_ppm"):
         assert getattr(got, f) == getattr(want, f), f
 
@@ -54,7 +55,8 @@ def test_random_configs_bit_exact():
             c.state_budget = rng.randint(10 ** 4, 10 ** 8)
         if rng.random() < 0.1:
             c.C = rng.randint(1, 6)
-        c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE])
+        c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE, pl.ACT_HYBRID])
+        c.n_recompute = rng.randint(0, L)
         link = rng.choice([10 ** 8, 10 ** 9, 10 ** 10])
         hi = pl.Evaluator(c, 10 ** 18, link).device_bytes(1, [L + 1])
         budget = rng.randint(hi // 4, int(hi * 1.5))

@@ -37,8 +37,8 @@ def test_executed_flops_counts_the_reforward():
 
 
 class _Plan:
-    def __init__(self, ends, policy):
-        self._ends, self.act_policy = ends, policy
+    def __init__(self, ends, policy, n_recompute=0):
+        self._ends, self.act_policy, self.n_recompute = ends, policy, n_recompute
 
     def ends(self):
         return self._ends
@@ -64,5 +64,11 @@ def test_cost_table_from_trace_blocks_embed_head():
     lines_rc = [l.replace(f"BWD 2 ", "BWD 2 ") for l in lines]
     lines_rc = [(f"compute BWD 2 {l.split()[3]} - 0 {2 * (tb + tf)}" if l.split()[1:3] == ["BWD", "2"] else l)
                 for l in lines_rc]
-    t_rc = aprof.cost_table_from_trace("\n".join(lines_rc), _Plan([1, 3, 5], atom.ACT_RECOMPUTE), 4)
+    t_rc = aprof.cost_table_from_trace("\n".join(lines_rc), _Plan([1, 3, 5], atom.ACT_HYBRID, 3), 4)
     assert abs(t_rc[3] / 1000.0 - tb) < 1e-6
+    # hybrid: only blocks 1..2 re-forwarded -> segment 2 holds one of them (B1), segment 1 one (B0)
+    lines_h = [(f"compute BWD 2 {l.split()[3]} - 0 {2 * tb + tf}" if l.split()[1:3] == ["BWD", "2"] else
+                (f"compute BWD 1 {l.split()[3]} - 0 {emb_b + tb + tf}" if l.split()[1:3] == ["BWD", "1"] else l))
+               for l in lines]
+    t_h = aprof.cost_table_from_trace("\n".join(lines_h), _Plan([1, 3, 5], atom.ACT_HYBRID, 2), 4)
+    assert abs(t_h[3] / 1000.0 - tb) < 1e-6 and abs(t_h[1] / 1000.0 - emb_b) < 1e-6
