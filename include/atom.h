@@ -152,6 +152,27 @@ atom_status atom_step_device(atom_peer* peer, const int32_t* tokens_dev, float* 
  * (standalone pass over all sub-models).  Returns after enqueueing (flush == 0) or completion. */
 atom_status atom_sync(atom_peer* const* peers, int32_t n_local, int32_t flush);
 
+/* Membership changes ("peers join and leave"; P:563 GPUs killed mid-training).
+ * The host-side registry (paper_2403_10504_b200/elastic.py) decides who is a member; these calls
+ * only rebuild the averaging communicator and bring a joiner up to date.  All are collective over
+ * the members of the NEW membership and must be called between steps (no sync step in flight).
+ *
+ * atom_comm_reset: drop the current communicator (aborted: members that died cannot answer) and
+ *   join a new one from a fresh 128-byte id (atom_nccl_unique_id on one member, shared through the
+ *   registry); nranks == 1 leaves the peer without a communicator (sync steps become local no-ops).
+ * atom_comm_shrink: ncclCommShrink of the current communicator without the listed ranks (failed or
+ *   leaving peers; abort_ops != 0 first terminates operations of the parent that cannot complete);
+ *   the peer's rank / nranks become its position in the shrunk communicator.
+ * atom_broadcast_state: root sends its fp32 master, AdamW m, v and optimizer step count; members
+ *   with adopt != 0 (joiners: "fetch the current model") overwrite theirs, the others only
+ *   take part.  Root's state is unchanged.
+ * Errors: ATOM_E_INVALID, ATOM_E_STATE (poisoned peer), ATOM_E_NCCL, ATOM_E_CUDA. */
+atom_status atom_comm_reset(atom_peer* peer, const void* nccl_id, int32_t nranks, int32_t rank);
+atom_status atom_comm_shrink(atom_peer* peer, const int32_t* exclude_ranks, int32_t n_exclude, int32_t abort_ops);
+atom_status atom_broadcast_state(atom_peer* peer, int32_t root, int32_t adopt);
+/* The peer's averaging rank / size and optimizer step count. */
+atom_status atom_peer_info(atom_peer* peer, int32_t* rank, int32_t* nranks, int64_t* step);
+
 /* Copy the peer's fp32 master parameters and AdamW moments (canonical order, [N] each) to host
  * buffers; NULL skips one.  Waits for all outstanding work of the peer. */
 atom_status atom_get_params(atom_peer* peer, float* master_out, float* m_out, float* v_out);

@@ -176,6 +176,16 @@ lib.atom_peer_destroy.restype = C.c_int
 lib.atom_peer_destroy.argtypes = [_P]
 
 
+lib.atom_comm_reset.restype = C.c_int
+lib.atom_comm_reset.argtypes = [_P, C.c_void_p, C.c_int32, C.c_int32]
+lib.atom_comm_shrink.restype = C.c_int
+lib.atom_comm_shrink.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32, C.c_int32]
+lib.atom_broadcast_state.restype = C.c_int
+lib.atom_broadcast_state.argtypes = [_P, C.c_int32, C.c_int32]
+lib.atom_peer_info.restype = C.c_int
+lib.atom_peer_info.argtypes = [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+
+
 def atom_nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib.atom_nccl_unique_id(buf))
@@ -248,6 +258,26 @@ class Peer:
             f = line.split()
             out.append({k: (float(v) if k in ("ms", "tflops") else int(v)) for k, v in zip(keys, f)})
         return out
+
+    def comm_reset(self, nccl_id: bytes, nranks: int, rank: int):
+        """atom_comm_reset: leave the current averaging communicator, join a new one."""
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        check(lib.atom_comm_reset(self.h, idbuf, nranks, rank))
+
+    def comm_shrink(self, exclude_ranks, abort_ops=False):
+        """atom_comm_shrink: ncclCommShrink without the given (failed / leaving) ranks."""
+        ex = (C.c_int32 * max(len(exclude_ranks), 1))(*exclude_ranks)
+        check(lib.atom_comm_shrink(self.h, ex, len(exclude_ranks), int(abort_ops)))
+
+    def broadcast_state(self, root: int, adopt: bool):
+        """atom_broadcast_state (collective): root sends master, m, v and step count; adopt=True
+        overwrites this peer's state with root's (a joiner)."""
+        check(lib.atom_broadcast_state(self.h, root, int(adopt)))
+
+    def info(self) -> dict:
+        r, n, t = C.c_int32(), C.c_int32(), C.c_int64()
+        check(lib.atom_peer_info(self.h, C.byref(r), C.byref(n), C.byref(t)))
+        return {"rank": r.value, "nranks": n.value, "step": t.value}
 
     def stats(self) -> dict:
         s = Stats()

@@ -9,6 +9,9 @@ namespace atom {
 bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const void* nccl_id);
 bool peer_step(atom_peer* p, const int32_t* tokens, bool on_device, float* loss);
 bool peer_flush_average(atom_peer* p);
+bool peer_broadcast_state(atom_peer* p, int root, bool adopt);
+bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank);
+bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abort_ops);
 bool peer_get_params(atom_peer* p, float* master, float* m, float* v);
 bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms);
 bool peer_stats(atom_peer* p, atom_stats_t* s);
@@ -160,6 +163,49 @@ atom_status atom_sync(atom_peer* const* peers, int32_t n_local, int32_t flush) {
       return fail(peers[i], cuda_or_nccl());
     }
   if (n_local > 1) ncclGroupEnd();
+  return ATOM_OK;
+}
+
+atom_status atom_comm_reset(atom_peer* p, const void* nccl_id, int32_t nranks, int32_t rank) {
+  if (!p || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_id)) {
+    set_error("atom_comm_reset: invalid arguments");
+    return ATOM_E_INVALID;
+  }
+  if (p->poisoned) { set_error("peer poisoned"); return ATOM_E_STATE; }
+  if (!peer_comm_reset(p, nccl_id, nranks, rank)) return fail(p, cuda_or_nccl());
+  return ATOM_OK;
+}
+
+atom_status atom_comm_shrink(atom_peer* p, const int32_t* exclude, int32_t n_exclude, int32_t abort_ops) {
+  if (!p || n_exclude < 0 || (n_exclude > 0 && !exclude)) {
+    set_error("atom_comm_shrink: invalid arguments");
+    return ATOM_E_INVALID;
+  }
+  if (p->poisoned) { set_error("peer poisoned"); return ATOM_E_STATE; }
+  for (int i = 0; i < n_exclude; ++i)
+    if (exclude[i] < 0 || exclude[i] >= p->nranks || exclude[i] == p->rank) {
+      set_error("atom_comm_shrink: rank %d cannot be excluded (own rank %d of %d)", exclude[i], p->rank, p->nranks);
+      return ATOM_E_INVALID;
+    }
+  if (!peer_comm_shrink(p, exclude, n_exclude, abort_ops != 0)) return fail(p, cuda_or_nccl());
+  return ATOM_OK;
+}
+
+atom_status atom_broadcast_state(atom_peer* p, int32_t root, int32_t adopt) {
+  if (!p || root < 0 || root >= p->nranks) {
+    set_error("atom_broadcast_state: invalid root");
+    return ATOM_E_INVALID;
+  }
+  if (p->poisoned) { set_error("peer poisoned"); return ATOM_E_STATE; }
+  if (!peer_broadcast_state(p, root, adopt != 0)) return fail(p, cuda_or_nccl());
+  return ATOM_OK;
+}
+
+atom_status atom_peer_info(atom_peer* p, int32_t* rank, int32_t* nranks, int64_t* step) {
+  if (!p) { set_error("atom_peer_info: NULL peer"); return ATOM_E_INVALID; }
+  if (rank) *rank = p->rank;
+  if (nranks) *nranks = p->nranks;
+  if (step) *step = p->t;
   return ATOM_OK;
 }
 

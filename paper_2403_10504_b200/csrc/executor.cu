@@ -629,6 +629,8 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   p->dh = a; a += al256(ab * p->C * M * d);
   p->losses = (float*)a; a += al256(4LL * p->C * M);
   p->scratch = a;
+  p->scratch_bytes = std::max(al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T),
+                              al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
   a += std::max(al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T),
                 al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
   p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);
@@ -732,6 +734,107 @@ bool peer_flush_average(atom_peer* p) {
     } else {
       PEER_OK(cast_params<float>(sv.master, (float*)sv.W, P, p->s_comp));
     }
+  }
+  PEER_OK(peer_stream_sync(p));
+  return true;
+}
+
+// membership change: abort the old communicator, join a new one (P:410 peers join and leave)
+bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank) {
+  PEER_OK(peer_stream_sync(p));
+  if (p->comm) {
+    ncclCommAbort(p->comm);
+    p->comm = nullptr;
+  }
+  p->nranks = nranks;
+  p->rank = rank;
+  if (nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&p->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      p->comm = nullptr;
+      p->nranks = 1;
+      p->rank = 0;
+      set_error("ncclCommInitRank failed: %s", ncclGetErrorString(r));
+      return false;
+    }
+  }
+  return true;
+}
+
+// failed / leaving ranks dropped from the communicator without a new bootstrap (ncclCommShrink)
+bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abort_ops) {
+  PEER_OK(peer_stream_sync(p));
+  if (!p->comm || n_exclude == 0) return true;
+  ncclComm_t nc = nullptr;
+  std::vector<int> ex(exclude, exclude + n_exclude);
+  ncclResult_t r = ncclCommShrink(p->comm, ex.data(), n_exclude, &nc, nullptr,
+                                  abort_ops ? NCCL_SHRINK_ABORT : NCCL_SHRINK_DEFAULT);
+  if (r != ncclSuccess) {
+    set_error("ncclCommShrink failed: %s", ncclGetErrorString(r));
+    return false;
+  }
+  ncclCommAbort(p->comm);   // the parent may still reference dead ranks: abort, not destroy
+  p->comm = nc;
+  int n = 1, rk = 0;
+  if (ncclCommCount(nc, &n) != ncclSuccess || ncclCommUserRank(nc, &rk) != ncclSuccess) {
+    set_error("nccl: shrunk communicator query failed");
+    return false;
+  }
+  p->nranks = n;
+  p->rank = rk;
+  if (n == 1) {   // alone: keep no communicator (sync steps are local no-ops)
+    ncclCommDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  return true;
+}
+
+// a joiner adopts root's model: fp32 master, AdamW m and v and the optimizer step count (AdamW
+// bias correction, learning-rate warm-up). Everything travels through the working scratch (idle
+// between steps) in chunks; only members with adopt set overwrite their state (the resident
+// segment 1 in place, whose compute weights are then re-derived; the others in the host arena).
+bool peer_broadcast_state(atom_peer* p, int root, bool adopt) {
+  PEER_OK(peer_stream_sync(p));
+  if (p->nranks <= 1) return true;
+  const bool is_root = p->rank == root;
+  float* buf = (float*)p->scratch;
+  const int64_t chunk = p->scratch_bytes / 4;
+  auto bcast = [&](void* b, size_t n, ncclDataType_t ty) -> bool {
+    ncclResult_t r = ncclBroadcast(b, b, n, ty, root, p->comm, p->s_comm);
+    if (r != ncclSuccess) {
+      set_error("ncclBroadcast failed: %s", ncclGetErrorString(r));
+      return false;
+    }
+    PEER_CUDA(cudaStreamSynchronize(p->s_comm));
+    return true;
+  };
+  SegView r1 = seg_view(p, 1, p->r1);
+  const int64_t P1 = p->seg_P[0];
+  // [0, P1) lives on the device (segment 1), [P1, N_pad) in the host arena (padded layout)
+  auto src = [&](int a, int64_t i) -> float* {
+    float* dev[3] = {r1.master, r1.m, r1.v};
+    float* host[3] = {p->h_master, p->h_m, p->h_v};
+    return i < P1 ? dev[a] + i : host[a] + i;
+  };
+  for (int a = 0; a < 3; ++a)
+    for (int64_t i0 = 0; i0 < p->dm.N_pad;) {
+      const int64_t n = std::min(chunk, (i0 < P1 ? P1 : p->dm.N_pad) - i0);
+      if (is_root) PEER_CUDA(cudaMemcpy(buf, src(a, i0), 4 * (size_t)n, cudaMemcpyDefault));
+      PEER_OK(bcast(buf, (size_t)n, ncclFloat32));
+      if (adopt && !is_root) PEER_CUDA(cudaMemcpy(src(a, i0), buf, 4 * (size_t)n, cudaMemcpyDefault));
+      i0 += n;
+    }
+  int64_t* dt = (int64_t*)buf;
+  PEER_CUDA(cudaMemcpy(dt, &p->t, sizeof(int64_t), cudaMemcpyHostToDevice));
+  PEER_OK(bcast(dt, 1, ncclInt64));
+  if (adopt) PEER_CUDA(cudaMemcpy(&p->t, dt, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (adopt && !is_root) {
+    if (p->dm.dtype == ATOM_BF16)
+      PEER_OK(cast_params<bf16>(r1.master, (bf16*)r1.W, P1, p->s_comp));
+    else
+      PEER_OK(cast_params<float>(r1.master, (float*)r1.W, P1, p->s_comp));
   }
   PEER_OK(peer_stream_sync(p));
   return true;

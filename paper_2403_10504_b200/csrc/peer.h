@@ -41,6 +41,7 @@ struct atom_peer {
   uint8_t* dh = nullptr;                // [C][M][d] boundary gradient
   float* losses = nullptr;              // [C*M]
   uint8_t* scratch = nullptr;
+  int64_t scratch_bytes = 0;
   float* red = nullptr;
   int* emb = nullptr;
   float* loss_dev = nullptr;

@@ -1,0 +1,148 @@
+"""Elastic peers on B200s (PAPER P:410 peers join and leave, P:563 GPUs killed
+mid-training): real atom peers average over NCCL on sync steps chosen by the global-batch
+trigger (paper_2403_10504_b200/elastic.py); one peer dies abruptly, the survivors drop it with
+ncclCommShrink (atom_comm_shrink) and train on; a joiner takes the dead peer's GPU, gets a fresh
+communicator (atom_comm_reset) and adopts the leader's state (atom_broadcast_state).
+
+Checked through the C-ABI: every sync step leaves all members with bit-identical fp32 masters;
+right after admission the joiner's master, m, v and step count equal the leader's; training
+completes every step on every survivor.  Needs >= 2 GPUs (gpurun --gpus 2 or 4).
+"""
+import datetime
+import hashlib
+import json
+import multiprocessing as mp
+import os
+import socket
+import time
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEPS, GLOBAL_BATCH, TTL, KILL_AT, JOINER = 10, 12, 4.0, 2, 10
+
+
+def _ngpu():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _digest(peer):
+    p = peer.params()
+    return {k: hashlib.sha256(v.tobytes()).hexdigest() for k, v in p.items()}
+
+
+def _peer(pid, n0, port, q):
+    import torch
+    import torch.distributed as dist
+    store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=datetime.timedelta(seconds=300))
+    victim = n0 - 1
+    gpu = pid if pid != JOINER else victim
+    if pid == JOINER:   # wait until the victim's failure has been handled (its GPU is free)
+        while not store.check([f"dec/{KILL_AT + 2}"]):
+            time.sleep(0.01)
+    torch.cuda.set_device(gpu)
+    import synth
+    from paper_2403_10504_b200 import atom, elastic
+    g = synth.CONFIGS["tiny"]
+    C = 2
+    cfg = atom.make_cfg(g, dtype=atom.BF16, C_=C, overlap_check=0, forced_ends=[2, 5], lr=1e-3, warmup_steps=0)
+    plan = atom.atom_plan(cfg, 10 ** 11, 10 ** 10)
+    init = synth.init_params(g, seed=1234, perturb=True)
+    co = elastic.Coordinator(store, pid, GLOBAL_BATCH, ttl=TTL, make_id=atom.atom_nccl_unique_id)
+    log = {"pid": pid, "decs": [], "hash": {}, "info": {}}
+    if pid == JOINER:
+        peer = atom.Peer(cfg, plan, device=gpu, init_params=synth.init_params(g, seed=99), seed=0)
+        d = co.join()
+        co.apply(d, peer, atom.atom_sync)
+        log["decs"].append(d.to_json())
+        log["hash"][f"admit{d.s}"] = _digest(peer)
+        log["info"][f"admit{d.s}"] = peer.info()
+    else:
+        if pid == 0:
+            store.set("nccl0", atom.atom_nccl_unique_id().hex())
+        nid = bytes.fromhex(store.get("nccl0").decode())
+        peer = atom.Peer(cfg, plan, device=gpu, init_params=init, seed=0, nccl_id=nid, nranks=n0, rank=pid)
+        co.start(list(range(n0)))
+    while co.s < STEPS - 1:
+        toks = synth.tokens(g, C * g.micro_batch, synth.step_seed(pid, co.s + 1))
+        peer.step(toks)
+        torch.cuda.synchronize()
+        was_sync = co.sync_step
+        d = co.after_step(C * g.micro_batch)
+        if was_sync:
+            log["hash"][f"sync{d.s}"] = _digest(peer)
+        co.apply(d, peer, atom.atom_sync)
+        if d.joiners:
+            log["hash"][f"admit{d.s}"] = _digest(peer)
+            log["info"][f"admit{d.s}"] = peer.info()
+        log["decs"].append(d.to_json())
+        if pid == victim and d.s >= KILL_AT and not d.sync:
+            q.put(json.dumps(log))
+            q.close()
+            q.join_thread()
+            os._exit(0)    # abrupt failure between steps: no leave, no destroy
+    log["info"]["end"] = peer.info()
+    q.put(json.dumps(log))
+    peer.destroy()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_failure_shrink_join_and_averaging():
+    import torch.distributed as dist
+    n0 = min(_ngpu(), 3)
+    victim = n0 - 1
+    port = _free_port()
+    server = dist.TCPStore("127.0.0.1", port, is_master=True, wait_for_workers=False,
+                           timeout=datetime.timedelta(seconds=300))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pids = list(range(n0)) + [JOINER]
+    procs = [ctx.Process(target=_peer, args=(pid, n0, port, q)) for pid in pids]
+    for p in procs:
+        p.start()
+    logs = {}
+    for _ in procs:
+        lg = json.loads(q.get(timeout=600))
+        logs[lg["pid"]] = lg
+    for p in procs:
+        p.join(timeout=60)
+    del server
+    decs = {}
+    for lg in logs.values():
+        for d in lg["decs"]:
+            d = json.loads(d)
+            assert decs.setdefault(d["s"], d) == d
+    assert sorted(decs) == list(range(STEPS))
+    s_kill = json.loads(logs[victim]["decs"][-1])["s"]
+    assert decs[s_kill + 1]["dead"] == [victim]
+    adm = [d for d in decs.values() if d["joiners"]]
+    assert len(adm) == 1 and adm[0]["joiners"] == [JOINER]
+    a = adm[0]
+    leader = a["leader"]
+    # the joiner adopted the leader's master, m, v and step count, bit for bit
+    key = f"admit{a['s']}"
+    assert logs[JOINER]["hash"][key] == logs[leader]["hash"][key]
+    assert logs[JOINER]["info"][key]["step"] == logs[leader]["info"][key]["step"]
+    assert logs[JOINER]["info"][key]["nranks"] == len(a["members"])
+    # every sync step left the members with identical masters (m, v stay local, R16)
+    syncs = [s for s in decs if decs[s]["sync"] and s + 1 in decs and len(decs[s]["members"]) > 1]
+    assert syncs, decs
+    for s in syncs:
+        hs = [logs[m]["hash"][f"sync{s + 1}"]["master"] for m in decs[s]["members"]]
+        assert len(set(hs)) == 1, (s, decs[s]["members"])
+    # survivors and the joiner finished every step
+    for pid in [p for p in pids if p != victim]:
+        assert json.loads(logs[pid]["decs"][-1])["s"] == STEPS - 1
