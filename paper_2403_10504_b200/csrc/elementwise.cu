@@ -183,46 +183,56 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
 // Column sums over rows in a fixed order (bias gradients, LN gain / shift gradients):
 //   mode 0: out0[j] += sum_r a[r][j]
 //   mode 1: out0[j] += sum_r a[r][j] * xhat[r][j],  out1[j] += sum_r a[r][j]
-// One CTA per (column block of 128 x VW columns, chunk of RED_ROWS rows); its four thread groups
-// sum 32 rows each (CP_UNR 16-byte loads in flight per thread), combined in group order into one
-// partial per chunk. The last CTA of a column block to finish (atomic ticket; the ticket only
-// picks who, never the order) adds the chunk partials in chunk order and resets the ticket.
-constexpr int CP_UNR = 8, CP_GROUPS = 4, CP_GROWS = RED_ROWS / CP_GROUPS;
+//   mode 2: a[r][j] <- T(a[r][j] * gelu'(x[r][j])) in place, out0[j] += sum_r of the stored values
+// Grid (column blocks of 64 x VW columns) x (G row ranges), sized by the host to one wave of
+// resident CTAs (CP_PER_SM per SM): a CTA's four thread groups sum contiguous quarters of its row range
+// (UNR 16-byte loads in flight per thread), combined in group order into one partial per range.
+// The last CTA of a column block to finish (atomic ticket; the ticket only picks who, never the
+// order) adds the range partials in range order and resets the ticket: deterministic for a given
+// (rows, columns, SM count).
+constexpr int CP_GROUPS = 4, CP_TX = 64, CP_PER_SM = 3;
 template <typename T, int MODE>
-__global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __restrict__ a, long lda,
-                                                                   const T* __restrict__ x,
-                                                                   const float* __restrict__ stats, long rows,
-                                                                   int ncols, float* __restrict__ part0,
-                                                                   float* __restrict__ part1, float* __restrict__ out0,
-                                                                   float* __restrict__ out1, int* __restrict__ ticket) {
+__global__ void __launch_bounds__(CP_TX * CP_GROUPS, CP_PER_SM) col_sums_kernel(const T* __restrict__ a, long lda,
+                                                                        const T* __restrict__ x,
+                                                                        const float* __restrict__ stats, long rows,
+                                                                        int ncols, float* __restrict__ part0,
+                                                                        float* __restrict__ part1,
+                                                                        float* __restrict__ out0,
+                                                                        float* __restrict__ out1,
+                                                                        int* __restrict__ ticket) {
   constexpr int VW = Vec<T>::N;
-  __shared__ float sh[CP_GROUPS][MODE == 1 ? 2 : 1][128 * VW];
+  constexpr int UNR = MODE == 0 ? 8 : 4;
+  constexpr int NS = MODE == 1 ? 2 : 1;
+  __shared__ float sh[CP_GROUPS][NS][CP_TX * VW];
   __shared__ int last;
   const int tx = threadIdx.x, g = threadIdx.y;
-  const int j = (blockIdx.x * 128 + tx) * VW;
+  const int j = (blockIdx.x * CP_TX + tx) * VW;
   const int c = blockIdx.y, nch = gridDim.y;
   float s0[VW], s1[VW];
 #pragma unroll
   for (int i = 0; i < VW; ++i) s0[i] = s1[i] = 0.f;
+  // this CTA's rows [c*R, (c+1)*R) in four contiguous group quarters
+  const long R = (rows + nch - 1) / nch, Rg = (R + CP_GROUPS - 1) / CP_GROUPS;
+  const long cr1 = min(rows, (long)(c + 1) * R);
+  const long r0 = (long)c * R + g * Rg, r1 = min(cr1, r0 + Rg);
   if (j < ncols) {
-    const long r0 = (long)c * RED_ROWS + g * CP_GROWS, r1 = min(rows, r0 + CP_GROWS);
-    for (long rb = r0; rb < r1; rb += CP_UNR) {
+    for (long rb = r0; rb < r1; rb += UNR) {
       // raw 16-byte loads first (all in flight), conversions after
-      uint4 ra[CP_UNR], rx[MODE != 0 ? CP_UNR : 1];
+      uint4 ra[UNR], rx[MODE != 0 ? UNR : 1];
 #pragma unroll
-      for (int u = 0; u < CP_UNR; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         const bool ok = rb + u < r1;
         ra[u] = ok ? *(const uint4*)(a + (rb + u) * lda + j) : make_uint4(0, 0, 0, 0);
         if constexpr (MODE != 0) rx[u] = ok ? *(const uint4*)(x + (rb + u) * ncols + j) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int u = 0; u < CP_UNR; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         if (rb + u < r1) {
           float v[VW];
           const T* ep = (const T*)&ra[u];
 #pragma unroll
           for (int i = 0; i < VW; ++i) v[i] = to_f(ep[i]);
-          if constexpr (MODE == 2) {   // a <- T(a * gelu'(x)) in place; sums of the stored values
+          if constexpr (MODE == 2) {
             const T* xp = (const T*)&rx[u];
             float o[VW];
 #pragma unroll
@@ -250,11 +260,11 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
 #pragma unroll
   for (int i = 0; i < VW; ++i) {
     sh[g][0][tx * VW + i] = s0[i];
-    if constexpr (MODE == 1) sh[g][MODE == 1 ? 1 : 0][tx * VW + i] = s1[i];
+    if constexpr (MODE == 1) sh[g][NS - 1][tx * VW + i] = s1[i];
   }
   __syncthreads();
   // combine the groups in group order: thread (tx, g) finishes columns tx * VW + e, e = g, g + CP_GROUPS, ...
-  const long cb = (long)blockIdx.x * 128 * VW;
+  const long cb = (long)blockIdx.x * CP_TX * VW;
   for (int e = g; e < VW; e += CP_GROUPS) {
     const int col = tx * VW + e;
     if (cb + col < ncols) {
@@ -262,8 +272,8 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
       for (int q = 1; q < CP_GROUPS; ++q) t0 += sh[q][0][col];
       part0[(long)c * ncols + cb + col] = t0;
       if constexpr (MODE == 1) {
-        float t1 = sh[0][MODE == 1 ? 1 : 0][col];
-        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][MODE == 1 ? 1 : 0][col];
+        float t1 = sh[0][NS - 1][col];
+        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][NS - 1][col];
         part1[(long)c * ncols + cb + col] = t1;
       }
     }
@@ -274,22 +284,22 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // final reduction of this column block over the chunks: thread (tx, g) sums its VW columns over
-  // chunks g, g + CP_GROUPS, ... (16-byte loads, several in flight), then the groups are added in
+  // final reduction of this column block over the ranges: thread (tx, g) sums its VW columns over
+  // ranges g, g + CP_GROUPS, ... (16-byte loads, several in flight), then the groups are added in
   // group order -- a fixed order, so the result is deterministic
-  float r0[VW], r1[VW];
+  float q0[VW], q1[VW];
 #pragma unroll
-  for (int i = 0; i < VW; ++i) r0[i] = r1[i] = 0.f;
+  for (int i = 0; i < VW; ++i) q0[i] = q1[i] = 0.f;
   if (j < ncols) {
 #pragma unroll 4
     for (int q = g; q < nch; q += CP_GROUPS) {
 #pragma unroll
       for (int i4 = 0; i4 < VW; i4 += 4) {
         const float4 a4 = __ldcg((const float4*)(part0 + (long)q * ncols + j + i4));
-        r0[i4] += a4.x; r0[i4 + 1] += a4.y; r0[i4 + 2] += a4.z; r0[i4 + 3] += a4.w;
+        q0[i4] += a4.x; q0[i4 + 1] += a4.y; q0[i4 + 2] += a4.z; q0[i4 + 3] += a4.w;
         if constexpr (MODE == 1) {
           const float4 b4 = __ldcg((const float4*)(part1 + (long)q * ncols + j + i4));
-          r1[i4] += b4.x; r1[i4 + 1] += b4.y; r1[i4 + 2] += b4.z; r1[i4 + 3] += b4.w;
+          q1[i4] += b4.x; q1[i4 + 1] += b4.y; q1[i4 + 2] += b4.z; q1[i4 + 3] += b4.w;
         }
       }
     }
@@ -297,8 +307,8 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
   __syncthreads();   // the group-combine reads of sh above are done
 #pragma unroll
   for (int i = 0; i < VW; ++i) {
-    sh[g][0][tx * VW + i] = r0[i];
-    if constexpr (MODE == 1) sh[g][MODE == 1 ? 1 : 0][tx * VW + i] = r1[i];
+    sh[g][0][tx * VW + i] = q0[i];
+    if constexpr (MODE == 1) sh[g][NS - 1][tx * VW + i] = q1[i];
   }
   __syncthreads();
   for (int e = g; e < VW; e += CP_GROUPS) {
@@ -308,8 +318,8 @@ __global__ void __launch_bounds__(128 * CP_GROUPS) col_sums_kernel(const T* __re
       for (int q = 1; q < CP_GROUPS; ++q) t0 += sh[q][0][col];
       out0[cb + col] += t0;
       if constexpr (MODE == 1) {
-        float t1 = sh[0][MODE == 1 ? 1 : 0][col];
-        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][MODE == 1 ? 1 : 0][col];
+        float t1 = sh[0][NS - 1][col];
+        for (int q = 1; q < CP_GROUPS; ++q) t1 += sh[q][NS - 1][col];
         out1[cb + col] += t1;
       }
     }
@@ -555,6 +565,22 @@ static inline int grid_for(long n, int threads = 256) {
   return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
 }
 
+// row ranges of the column sums: one wave of resident CTAs (CP_PER_SM per SM) over the column blocks,
+// at least 32 rows per range, and no more ranges than the partial buffer's ceil(rows / RED_ROWS)
+static int cs_ranges(long rows, int col_blocks) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  long g = (long)sms * CP_PER_SM / (col_blocks > 0 ? col_blocks : 1);
+  g = std::min(g, (rows + 31) / 32);
+  g = std::min(g, (rows + RED_ROWS - 1) / RED_ROWS);
+  return (int)std::max(1L, g);
+}
+
 #define LAUNCH_OK()                      \
   do {                                   \
     count_launch();                      \
@@ -597,13 +623,14 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
 #undef LN_BWD_CASE
   }
   LAUNCH_OK();
-  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   constexpr int VW = Vec<T>::N;
-  if ((d / VW + 127) / 128 > CS_TICKETS) {
+  const int nb = (d / VW + CP_TX - 1) / CP_TX;
+  if (nb > CS_TICKETS) {
     set_error("ln_bwd: %d columns exceed the column-sum ticket slots", d);
     return false;
   }
-  col_sums_kernel<T, 1><<<dim3((d / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+  const int nch = cs_ranges(rows, nb);
+  col_sums_kernel<T, 1><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
       dy, d, x, stats, rows, d, part, part + (long)nch * d, dg, db, ticket);
   LAUNCH_OK();
   return true;
@@ -612,30 +639,32 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
 // the result: the fc pre-activation gradient and its bias gradient in one pass
 template <typename T>
 bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
-  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   constexpr int VW = Vec<T>::N;
-  if (n % VW || (n / VW + 127) / 128 > CS_TICKETS) {
+  const int nb = (n / VW + CP_TX - 1) / CP_TX;
+  if (n % VW || nb > CS_TICKETS) {
     set_error("dgelu_bias_grad: %d columns (multiple of %d, at most %d blocks)", n, VW, CS_TICKETS);
     return false;
   }
-  col_sums_kernel<T, 2><<<dim3((n / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+  const int nch = cs_ranges(rows, nb);
+  col_sums_kernel<T, 2><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
       dy, n, u, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
   LAUNCH_OK();
   return true;
 }
 template <typename T>
 bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
-  const int nch = (int)((rows + RED_ROWS - 1) / RED_ROWS);
   constexpr int VW = Vec<T>::N;
   if (n % VW || ld % VW) {
     set_error("bias_grad: columns and pitch must be multiples of %d", VW);
     return false;
   }
-  if ((n / VW + 127) / 128 > CS_TICKETS) {
+  const int nb = (n / VW + CP_TX - 1) / CP_TX;
+  if (nb > CS_TICKETS) {
     set_error("bias_grad: %d columns exceed the column-sum ticket slots", n);
     return false;
   }
-  col_sums_kernel<T, 0><<<dim3((n / VW + 127) / 128, nch), dim3(128, CP_GROUPS), 0, st>>>(
+  const int nch = cs_ranges(rows, nb);
+  col_sums_kernel<T, 0><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
       dy, ld, nullptr, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
   LAUNCH_OK();
   return true;

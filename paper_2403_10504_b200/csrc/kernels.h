@@ -20,8 +20,8 @@ bool gemm_simt(int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
 template <typename T> bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st,
                                   const T* res = nullptr);
 template <typename T> bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st);
-// part: fp32 chunk partials (2 x ceil(rows / RED_ROWS) x d for ln_bwd); ticket: CS_TICKETS zeroed
-// ints, one per block of 128 x (16 / sizeof(T)) columns, returned to zero by the kernel
+// part: fp32 range partials (at most 2 x ceil(rows / RED_ROWS) x d for ln_bwd); ticket: CS_TICKETS zeroed
+// ints, one per block of 64 x (16 / sizeof(T)) columns, returned to zero by the kernel
 constexpr int CS_TICKETS = 48;
 template <typename T> bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dres, T* dx, float* dg,
                                   float* db, float* part, int* ticket, long rows, int d, cudaStream_t st);
