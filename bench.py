@@ -263,6 +263,14 @@ def gemm_traffic():
                                "algorithmic_bytes": alg, "source": os.path.relpath(GEMM_NCU, os.path.dirname(GEMM_NCU) + "/..")}}
 
 
+def host_link(trace, plan, probe_gbs):
+    from paper_2403_10504_b200 import profile as aprof
+    h2d, d2h = aprof.lane_ms(trace, "h2d"), aprof.lane_ms(trace, "d2h")
+    return {"h2d_op_GBs": plan.pred_h2d_B / h2d / 1e6 if h2d > 0 else None,
+            "d2h_op_GBs": plan.pred_d2h_B / d2h / 1e6 if d2h > 0 else None,
+            "probe_bidir_GBs": probe_gbs, "solo_h2d_GBs": H2D_GBS, "solo_d2h_GBs": D2H_GBS}
+
+
 def compute_busy_pct(trace, step_ms):
     """Share of the compute lane's span in the last step (its first op start -> last op end) in
     which it runs an op (union of the traced intervals): what is left is the compute stream waiting
@@ -297,6 +305,8 @@ def main():
     ap.add_argument("--trace-out", default="", help="write the last step's per-op trace here (rank 0)")
     ap.add_argument("--planner-tflops", type=float, default=0.0,
                     help="compute rate the planner's cost model assumes (default: measured by a profile run)")
+    ap.add_argument("--grad-rounds", type=int, default=0,
+                    help="host update placement (P:563 CPU AdamW): gradient rounds per update (0 = GPU AdamW every step)")
     ap.add_argument("--no-profile", action="store_true",
                     help="plan with the measured bf16 peak instead of a profiled compute rate")
     args = ap.parse_args()
@@ -333,7 +343,7 @@ def main():
     # peer averaging cadence from a global batch of 512 sequences (reading R17)
     plan_tf = args.planner_tflops or pk["bf16_tflops"]
     cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(plan_tf * 1e12),
-                        state_budget=state_cap, lr=1e-4, warmup_steps=3000)
+                        state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
     profiled = None
     if not args.planner_tflops and not args.no_profile:
@@ -369,7 +379,7 @@ def main():
         link_bw = int(min(rates[1], args.link_gbs * 1e9))
         cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(rates[0]), state_budget=state_cap,
                             lr=1e-4, warmup_steps=3000, cost_table=table or None,
-                            d2h_bw=int(min(rates[2], args.link_gbs * 1e9)))
+                            d2h_bw=int(min(rates[2], args.link_gbs * 1e9)), grad_rounds=args.grad_rounds)
         plan = atom.atom_plan(cfg, hbm_budget, link_bw)
     tok_step = plan.C * g.micro_batch * g.seq_len
     cfg.sync_every = adist.sync_every(world, plan.C, g.micro_batch)     # global batch 512
@@ -415,8 +425,11 @@ def main():
     gemm_tf = st["gemm_flops"] / (st["gemm_ms"] / 1000.0) / 1e12 if st["gemm_ms"] > 0 else None
     peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     ms_step = ms / args.steps
+    # the slower of the FLOPs at tensor peak and the plan's swapped bytes over the host link (per
+    # direction, the link alone): ~14 N in / 12 N out with the GPU AdamW (less the resident
+    # sub-model 1), 12 N / 4 N with host gradient sums (--grad-rounds)
     t_roof = max(tok_step * f_alg_per_token(g) / (pk["bf16_tflops"] * 1e12),
-                 14 * synth.n_params(g) / (H2D_GBS * 1e9), 12 * synth.n_params(g) / (D2H_GBS * 1e9))
+                 plan.pred_h2d_B / (H2D_GBS * 1e9), plan.pred_d2h_B / (D2H_GBS * 1e9))
     trace = peer.trace()
     if rank == 0 and args.trace_out:
         with open(args.trace_out, "w") as f:
@@ -437,6 +450,8 @@ def main():
                        "planner_tflops": plan_tf, "profile": profiled,
                        "state_budget_bytes": state_cap, "device_arena_bytes": plan.device_bytes,
                        "parallelism": f"peers{world}", "sync_every": cfg.sync_every,
+                       "update": (f"host: CPU AdamW every {args.grad_rounds} gradient rounds (a step = one round)"
+                                  if args.grad_rounds else "GPU AdamW on every swapped-in sub-model, every step"),
                        "link_GBs_bidir_probe": args.link_gbs, "numa_cpus": numa_cpus,
                        "l2": "inputs larger than L2 (weights/activations stream through HBM every step)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 4 * n_seq * (g.seq_len + 1),
@@ -454,11 +469,14 @@ def main():
                               "flops_per_token": f_alg_per_token(g),
                               # the same bound with the host link as all ranks see it at once
                               # (link_probe: host DRAM shared by the peers of one socket)
-                              "t_roof_contended_ms": 1000.0 * max(t_roof, 12 * synth.n_params(g) / (args.link_gbs * 1e9)),
-                              "frac_contended": 1000.0 * max(t_roof, 12 * synth.n_params(g) / (args.link_gbs * 1e9)) / ms_step},
+                              "t_roof_contended_ms": 1000.0 * max(t_roof, plan.pred_d2h_B / (args.link_gbs * 1e9)),
+                              "frac_contended": 1000.0 * max(t_roof, plan.pred_d2h_B / (args.link_gbs * 1e9)) / ms_step},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
             "compute_busy_pct": compute_busy_pct(trace, st["step_ms"]),
             "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
+            # while a copy runs (planned bytes of the last step / busy time of its copy lane) vs the
+            # link as every rank sees it at once (link_probe) and alone (profiles/box_probe_r01.json)
+            "host_link": host_link(trace, plan, args.link_gbs),
             "loss_first_last": [losses[0], losses[-1]],
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -81,6 +81,15 @@ typedef struct {
   int32_t warmup_steps;   /* linear warm-up length in steps (3000)                                    */
   int32_t sync_every;     /* average parameters every K steps; 0 = only when atom_sync() asks               */
   int32_t n_recompute;    /* ATOM_ACT_HYBRID: blocks 1..n_recompute (0..L) are re-forwarded in the backward */
+  int32_t grad_rounds;    /* 0: fused GPU AdamW on every swapped-in sub-model, every step (north star).
+                             R >= 1: the paper's update placement (P:563 CPU AdamW; R37): each
+                             atom_step is one gradient round; sub-models 2..S accumulate their fp32
+                             gradients in a host arena across R rounds (the backward loads the running sum
+                             with the master and stores it back: 8 + 4 B/param per round instead of 12 + 12)
+                             and every R-th round a multi-threaded CPU AdamW updates their host master,
+                             m and v with the mean gradient; the resident sub-model 1 accumulates on the
+                             device and takes the same update on the GPU                                 */
+  int32_t cpu_threads;    /* CPU AdamW threads (0 = all online cores)                                       */
 } atom_model_cfg;
 
 /* The plan: plain data, fixed capacity, no pointers.  Produced by atom_plan. */

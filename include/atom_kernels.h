@@ -43,6 +43,12 @@ int atom_k_attn_fwd(int impl, int dtype, const void* qkv, void* o, float* lse, i
 int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
                     float* dsum, void* dqkv, int B, int T, int h, int dh, void* stream);
 
+/* The CPU AdamW of the host update placement ("CPU AdamW"; R37) on host fp32
+ * arrays p, m, v (updated in place) and g (read, scaled by gscale first): lr_t the step's learning
+ * rate, t the 1-based update count, threads 0 = all cores.  Pure host code: runs without a GPU. */
+int atom_k_cpu_adamw(float* p, const float* g, float* m, float* v, long n, float lr_t, float b1, float b2, float eps,
+                     float wd, long t, float gscale, int threads);
+
 /* Number of kernels libatom launched in this process. */
 unsigned long long atom_k_launch_count(void);
 

@@ -11,6 +11,10 @@ micro-batches (one flat batch of C*b sequences, loss = mean over all step
 tokens) followed by AdamW; on a sync step the fp32 master
 parameters (only) are replaced by their arithmetic mean over peers, after
 that step's update.  m and v stay local.
+
+Host update placement (R37; "CPU AdamW", Hivemind accumulating
+gradients up to the target batch): with grad_rounds = R >= 1 a step is one gradient round; the
+gradients of R rounds are summed and every R-th round AdamW takes one step with their mean.
 """
 from __future__ import annotations
 
@@ -25,19 +29,31 @@ def average(params_list):
 
 
 class Peer:
-    def __init__(self, cfg, init_params, hyper: adamw.AdamWHyper):
+    def __init__(self, cfg, init_params, hyper: adamw.AdamWHyper, grad_rounds: int = 0):
         self.cfg = cfg
         self.h = hyper
         self.p = np.asarray(init_params, dtype=np.float64).copy()
         self.m = np.zeros_like(self.p)
         self.v = np.zeros_like(self.p)
         self.t = 0
+        self.R = grad_rounds
+        self.gsum = np.zeros_like(self.p)
+        self.rounds = 0
 
     def step(self, tokens):
-        """One training step on tokens [C*b, T+1]; returns the step loss."""
+        """One training step (or gradient round) on tokens [C*b, T+1]; returns the loss."""
         loss, g = gpt.loss_and_grad(self.cfg, self.p, tokens)
-        self.t += 1
-        self.p, self.m, self.v = adamw.adamw_step(self.h, self.t, self.p, g, self.m, self.v)
+        if self.R <= 0:
+            self.t += 1
+            self.p, self.m, self.v = adamw.adamw_step(self.h, self.t, self.p, g, self.m, self.v)
+            return loss, g
+        self.gsum = self.gsum + g
+        self.rounds += 1
+        if self.rounds == self.R:
+            self.t += 1
+            self.p, self.m, self.v = adamw.adamw_step(self.h, self.t, self.p, self.gsum / self.R, self.m, self.v)
+            self.gsum = np.zeros_like(self.p)
+            self.rounds = 0
         return loss, g
 
 

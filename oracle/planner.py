@@ -174,6 +174,7 @@ class PlanCfg:
     act_policy: int = ACT_AUTO    # AUTO: fewest re-forwarded blocks R = 0 (stash), 1, ..., L (reading R35)
     forced_ends: Optional[List[int]] = None
     n_recompute: int = 0          # ACT_HYBRID: re-forward blocks 1..n_recompute (those before the last segment)
+    grad_rounds: int = 0          # > 0: host gradient sums + CPU AdamW (reading R37): bwd loads 8 B, stores 4 B
 
     @classmethod
     def from_gpt(cls, g, **kw):
@@ -236,9 +237,12 @@ def node_costs(c: PlanCfg, link_bw: int) -> Costs:
         tbr = [ceil_div((2 * f + r) * 10 ** 9, c.peak_flops) for f, r in zip(ff, fr)]
     d2h = c.d2h_bw if c.d2h_bw > 0 else link_bw
     tlf = [ceil_div(4 * p * 10 ** 9, link_bw) for p in P]
-    tlb = [ceil_div(12 * p * 10 ** 9, link_bw) for p in P]
-    tmv = [ceil_div(8 * p * 10 ** 9, link_bw) for p in P]
-    ts = [ceil_div(12 * p * 10 ** 9, d2h) for p in P]
+    # host update placement (R37): the backward loads master + gradient sum (last segment: the sum)
+    # and stores the sum; else master + m + v in (m + v), all three out
+    hu = c.grad_rounds > 0
+    tlb = [ceil_div((8 if hu else 12) * p * 10 ** 9, link_bw) for p in P]
+    tmv = [ceil_div((4 if hu else 8) * p * 10 ** 9, link_bw) for p in P]
+    ts = [ceil_div((4 if hu else 12) * p * 10 ** 9, d2h) for p in P]
     return Costs(P, tf, tb, tlf, tlb, tmv, ts, ff, tbr)
 
 
@@ -454,8 +458,11 @@ class Evaluator:
         M = c.micro_batch * c.seq_len
         P = [self.s("P", i, j) for i, j in segs]
         # forward loads fp32 masters of 2..S; backward loads master+m+v of 2..S-1 and m+v of S
-        h2d = (sum(4 * p for p in P[1:]) + sum(12 * p for p in P[1:-1]) + 8 * P[-1]) if S >= 2 else 0
-        d2h = sum(12 * p for p in P[1:])
+        # (host update placement: master + gradient sum, and the sum of S; stores the sum)
+        hu = c.grad_rounds > 0
+        h2d = (sum(4 * p for p in P[1:]) + sum((8 if hu else 12) * p for p in P[1:-1])
+               + (4 if hu else 8) * P[-1]) if S >= 2 else 0
+        d2h = sum((4 if hu else 12) * p for p in P[1:])
         return Plan(S, list(ends), C, nslot(S), (S - 1) * wbytes(c) * M * c.d_model, r1, al256(Q), st, wk,
                     r1 + nslot(S) * al256(Q) + st + wk, h2d, d2h,
                     C * sum(3 * f for f in self.k.ff), pol, r)

@@ -54,6 +54,19 @@ lib.atom_k_gemm.restype = C.c_int
 lib.atom_k_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_long, C.c_int,
                             C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_void_p, C.c_long, C.c_void_p, C.c_long,
                             C.c_void_p, C.c_void_p, C.c_long, C.c_void_p, C.c_long, C.c_int, C.c_void_p]
+lib.atom_k_cpu_adamw.restype = C.c_int
+lib.atom_k_cpu_adamw.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_float, C.c_float,
+                                 C.c_float, C.c_float, C.c_float, C.c_long, C.c_float, C.c_int]
+
+
+def k_cpu_adamw(p, g, m, v, lr_t, b1, b2, eps, wd, t, gscale=1.0, threads=0):
+    """atom_k_cpu_adamw on float32 numpy arrays (p, m, v updated in place)."""
+    for a in (p, g, m, v):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    return check(lib.atom_k_cpu_adamw(p.ctypes.data, g.ctypes.data, m.ctypes.data, v.ctypes.data, p.size, lr_t, b1,
+                                      b2, eps, wd, t, gscale, threads))
+
+
 lib.atom_k_launch_count.restype = C.c_ulonglong
 
 
@@ -77,7 +90,8 @@ class ModelCfg(C.Structure):
                 ("cost_table", C.POINTER(C.c_int64)), ("forced_ends", C.POINTER(C.c_int32)),
                 ("n_forced", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("eps", C.c_float), ("weight_decay", C.c_float), ("warmup_steps", C.c_int32),
-                ("sync_every", C.c_int32), ("n_recompute", C.c_int32)]
+                ("sync_every", C.c_int32), ("n_recompute", C.c_int32), ("grad_rounds", C.c_int32),
+                ("cpu_threads", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -99,7 +113,8 @@ class Plan(C.Structure):
 
 def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 10 ** 12, d2h_bw=0,
              state_budget=0, cost_table=None, forced_ends=None, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8,
-             weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0, n_recompute=0):
+             weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0, n_recompute=0, grad_rounds=0,
+             cpu_threads=0):
     """atom_model_cfg from a synth.GPTConfig-like object (keeps ctypes arrays alive on the struct)."""
     c = ModelCfg()
     c.n_layer, c.d_model, c.n_head, c.seq_len, c.vocab, c.micro_batch = (
@@ -117,6 +132,7 @@ def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 1
         c.n_forced = len(forced_ends)
     c.lr, c.beta1, c.beta2, c.eps, c.weight_decay = lr, beta1, beta2, eps, weight_decay
     c.warmup_steps, c.sync_every, c.n_recompute = warmup_steps, sync_every, n_recompute
+    c.grad_rounds, c.cpu_threads = grad_rounds, cpu_threads
     return c
 
 

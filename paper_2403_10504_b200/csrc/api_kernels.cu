@@ -66,4 +66,14 @@ int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const v
 
 unsigned long long atom_k_launch_count(void) { return g_launch_count; }
 
+int atom_k_cpu_adamw(float* p, const float* g, float* m, float* v, long n, float lr_t, float b1, float b2, float eps,
+                     float wd, long t, float gscale, int threads) {
+  if (!p || !g || !m || !v || n < 0 || t < 1) {
+    set_error("atom_k_cpu_adamw: invalid arguments");
+    return ATOM_E_INVALID;
+  }
+  cpu_adamw(p, g, m, v, n, adam_consts(lr_t, b1, b2, eps, wd, t, gscale), threads);
+  return ATOM_OK;
+}
+
 }  // extern "C"

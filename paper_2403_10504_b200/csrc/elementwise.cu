@@ -484,21 +484,24 @@ __global__ void gelu_kernel(const T* __restrict__ u, T* __restrict__ g, long n) 
 //   p <- p - (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps);  w <- T(p) (optional)
 template <typename T>
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                             float* __restrict__ v, T* __restrict__ w, long n, float lr, float b1, float b2, float eps,
-                             float wd, float bc1, float sbc2) {
-  const float decay = 1.f - lr * wd, step = lr / bc1;
+                             float* __restrict__ v, T* __restrict__ w, long n, AdamConsts c) {
+  // every product and quotient rounded on its own (__fmul_rn / __fdiv_rn: no contraction), the
+  // two explicit fmaf as written: cpu_adam.cpp applies the same operations in the same order
+  const float omb1 = 1.f - c.b1, omb2 = 1.f - c.b2;
+  auto upd = [&](float& pk, float gk, float& mk, float& vk) {
+    gk = __fmul_rn(gk, c.gscale);
+    const float pd = __fmul_rn(pk, c.decay);
+    mk = fmaf(omb1, gk - mk, mk);
+    vk = fmaf(c.b2, vk, __fmul_rn(__fmul_rn(omb2, gk), gk));
+    const float den = __fadd_rn(__fdiv_rn(sqrtf(vk), c.sbc2), c.eps);
+    pk = pd - __fdiv_rn(__fmul_rn(c.step, mk), den);
+  };
   const long n4 = n / 4;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
     float4 pp = ((float4*)p)[i], gg = ((const float4*)g)[i], mm = ((float4*)m)[i], vv = ((float4*)v)[i];
     float* pa = &pp.x; const float* ga = &gg.x; float* ma = &mm.x; float* va = &vv.x;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float pk = pa[k] * decay;
-      ma[k] = fmaf(1.f - b1, ga[k] - ma[k], ma[k]);
-      va[k] = fmaf(b2, va[k], (1.f - b2) * ga[k] * ga[k]);
-      const float den = sqrtf(va[k]) / sbc2 + eps;
-      pa[k] = pk - step * ma[k] / den;
-    }
+    for (int k = 0; k < 4; ++k) upd(pa[k], ga[k], ma[k], va[k]);
     ((float4*)p)[i] = pp; ((float4*)m)[i] = mm; ((float4*)v)[i] = vv;
     if (w) {
 #pragma unroll
@@ -506,11 +509,9 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     }
   }
   for (long i = 4 * n4 + blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    float pk = p[i] * decay;
-    m[i] = fmaf(1.f - b1, g[i] - m[i], m[i]);
-    v[i] = fmaf(b2, v[i], (1.f - b2) * g[i] * g[i]);
-    pk = pk - step * m[i] / (sqrtf(v[i]) / sbc2 + eps);
-    p[i] = pk;
+    float pk = p[i], mk = m[i], vk = v[i];
+    upd(pk, g[i], mk, vk);
+    p[i] = pk; m[i] = mk; v[i] = vk;
     if (w) w[i] = from_f<T>(pk);
   }
 }
@@ -718,11 +719,8 @@ bool gelu_apply(const T* u, T* g, long n, cudaStream_t st) {
   return true;
 }
 template <typename T>
-bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, float lr, float b1, float b2, float eps,
-           float wd, int t, cudaStream_t st) {
-  const double bc1 = 1.0 - pow((double)b1, t), bc2 = 1.0 - pow((double)b2, t);
-  adamw_kernel<T><<<grid_for(n / 4 + 1), 256, 0, st>>>(p, g, m, v, w, n, lr, b1, b2, eps, wd, (float)bc1,
-                                                       (float)sqrt(bc2));
+bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, const AdamConsts& k, cudaStream_t st) {
+  adamw_kernel<T><<<grid_for(n / 4 + 1), 256, 0, st>>>(p, g, m, v, w, n, k);
   LAUNCH_OK();
   return true;
 }
@@ -755,8 +753,7 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
   template bool embed_bwd<T>(const int32_t*, long, int, int, const T*, int, int, float*, float*, int*,         \
                              cudaStream_t);                                                                     \
   template bool gelu_apply<T>(const T*, T*, long, cudaStream_t);                                                \
-  template bool adamw<T>(float*, const float*, float*, float*, T*, long, float, float, float, float, float, int, \
-                         cudaStream_t);                                                                         \
+  template bool adamw<T>(float*, const float*, float*, float*, T*, long, const AdamConsts&, cudaStream_t);     \
   template bool cast_params<T>(const float*, T*, long, cudaStream_t);
 INST(float)
 INST(bf16)

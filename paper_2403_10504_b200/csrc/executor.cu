@@ -19,6 +19,7 @@ using namespace atom;
 
 namespace atom {
 extern unsigned long long g_launch_count;
+bool peer_flush_average(atom_peer* p);
 }
 
 #define PEER_CUDA(expr)                                                                                      \
@@ -377,7 +378,10 @@ bool embed_backward(atom_peer* p, int mb, const SegView& sv) {
 
 template <typename T>
 bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
-  if (k == p->S && mb == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  // the gradient buffer starts each step at zero; under gradient rounds (R37) only the first round
+  // of an update starts at zero, later rounds continue the running sum (resident sub-model 1: kept
+  // on the device; sub-models 2..S: loaded from the host sum with the master)
+  if (k == p->S && mb == 0 && p->round == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
   for (int node = p->seg_lo[k - 1]; node <= p->seg_hi[k - 1]; ++node) {
     if (node == 0)
       PEER_OK(embed_forward<T>(p, mb, sv));
@@ -390,7 +394,7 @@ bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
 }
 template <typename T>
 bool run_bwd(atom_peer* p, int k, int mb, const SegView& sv) {
-  if (k < p->S && mb == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  if (k < p->S && mb == 0 && p->round == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
   for (int node = p->seg_hi[k - 1]; node >= p->seg_lo[k - 1]; --node) {
     if (node == 0)
       PEER_OK(embed_backward<T>(p, mb, sv));
@@ -427,16 +431,43 @@ bool copy_seg(atom_peer* p, int k, float* dev, float* host, bool h2d) {
   return true;
 }
 
+// AdamW constants of this step's update: lr warm-up on the update count t; under gradient rounds
+// (R37) the summed gradient of R rounds is scaled to their mean
+AdamConsts step_consts(const atom_peer* p) {
+  const float lr_t = p->cfg.warmup_steps > 0
+                         ? p->cfg.lr * (float)std::min(1.0, (double)p->t / (double)p->cfg.warmup_steps)
+                         : p->cfg.lr;
+  const float gscale = p->cfg.grad_rounds > 0 ? 1.f / (float)p->cfg.grad_rounds : 1.f;
+  return adam_consts(lr_t, p->cfg.beta1, p->cfg.beta2, p->cfg.eps, p->cfg.weight_decay, (long)p->t, gscale);
+}
+
+// one sub-model's CPU AdamW, run by the CUDA driver in copy-stream order (no CUDA calls inside)
+struct HostAdamJob {
+  float *p, *g, *m, *v;
+  int64_t n;
+  AdamConsts k;
+  int threads;
+};
+void CUDART_CB host_adam(void* arg) {
+  auto* j = (HostAdamJob*)arg;
+  cpu_adamw(j->p, j->g, j->m, j->v, (long)j->n, j->k, j->threads);
+  delete j;
+}
+
 template <typename T>
 bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
   cudaStream_t st = lane_stream(p, o.lane);
+  const bool hu = p->cfg.grad_rounds > 0;
   for (auto& w : o.waits) {
     if (w.kind == -1) {
       auto it = p->rel_of.find(p->slot_phys[w.seg]);
       if (it != p->rel_of.end() && it->second) PEER_CUDA(cudaStreamWaitEvent(st, it->second, 0));
     } else if (w.kind == -2) {
       // host arena of segment w.seg written by the previous step's STORE
-      if (p->t > 1) PEER_CUDA(cudaStreamWaitEvent(st, p->op_ev[{K_STORE, w.seg}], 0));
+      if (p->steps > 0) PEER_CUDA(cudaStreamWaitEvent(st, p->op_ev[{K_STORE, w.seg}], 0));
+      // ... and, under gradient rounds, updated by its last CPU AdamW
+      if (!p->cpu_ev_set.empty() && p->cpu_ev_set[w.seg - 1])
+        PEER_CUDA(cudaStreamWaitEvent(st, p->cpu_ev[w.seg - 1], 0));
     } else {
       PEER_CUDA(cudaStreamWaitEvent(st, p->op_ev[{w.kind, w.seg}], 0));
     }
@@ -459,16 +490,15 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
     case K_FREE:
       break;
     case K_ADAM: {
-      const float lr_t = p->cfg.warmup_steps > 0
-                             ? p->cfg.lr * (float)std::min(1.0, (double)p->t / (double)p->cfg.warmup_steps)
-                             : p->cfg.lr;
+      // host update placement: only the resident sub-model 1 updates on the GPU (at the last round
+      // of an update); the others update on the CPU after their gradient sum is stored
+      if (hu && (k != 1 || !p->upd_round)) break;
       T* wout = (k == 1 && !sync) ? (T*)sv.W : nullptr;
-      PEER_OK(adamw<T>(sv.master, sv.grad, sv.m, sv.v, wout, P, lr_t, p->cfg.beta1, p->cfg.beta2, p->cfg.eps,
-                       p->cfg.weight_decay, (int)p->t, st));
+      PEER_OK(adamw<T>(sv.master, sv.grad, sv.m, sv.v, wout, P, step_consts(p), st));
       break;
     }
     case K_AVG:
-      if (p->nranks > 1) {
+      if (p->nranks > 1 && !hu) {
         ncclResult_t r = ncclAllReduce(sv.master, sv.master, (size_t)P, ncclFloat32, ncclAvg, p->comm, st);
         if (r != ncclSuccess) {
           set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
@@ -481,13 +511,41 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
       break;
     case K_LOAD_F:
       PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
+      // the interleaved last sub-model accumulates inside its forward op: its running gradient
+      // sum comes with the forward load (R37)
+      if (hu && k == p->S && p->round > 0) PEER_OK(copy_seg(p, k, sv.grad, p->h_gacc, true));
       break;
     case K_LOAD_B:
+      if (hu) {
+        if (k < p->S) {
+          PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
+          if (p->round > 0) PEER_OK(copy_seg(p, k, sv.grad, p->h_gacc, true));
+        }
+        break;
+      }
       if (!(k == p->S && p->S >= 2)) PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
       PEER_OK(copy_seg(p, k, sv.m, p->h_m, true));
       PEER_OK(copy_seg(p, k, sv.v, p->h_v, true));
       break;
     case K_STORE:
+      if (hu) {
+        // the gradient sum out; at the last round the CPU AdamW of this sub-model runs after it on
+        // its own stream (host functions there do not hold up the copies); the next step's forward
+        // load of the sub-model waits for it (HOST:k)
+        PEER_OK(copy_seg(p, k, sv.grad, p->h_gacc, false));
+        if (p->upd_round) {
+          cudaEvent_t stored = p->cpu_ev[k - 1];
+          PEER_CUDA(cudaEventRecord(stored, st));
+          PEER_CUDA(cudaStreamWaitEvent(p->s_cpu, stored, 0));
+          auto* job = new HostAdamJob{p->h_master + p->seg_off[k - 1], p->h_gacc + p->seg_off[k - 1],
+                                      p->h_m + p->seg_off[k - 1], p->h_v + p->seg_off[k - 1], P, step_consts(p),
+                                      p->cfg.cpu_threads};
+          PEER_CUDA(cudaLaunchHostFunc(p->s_cpu, host_adam, job));
+          PEER_CUDA(cudaEventRecord(p->cpu_ev[k - 1], p->s_cpu));
+          p->cpu_ev_set[k - 1] = 1;
+        }
+        break;
+      }
       PEER_OK(copy_seg(p, k, sv.master, p->h_master, false));
       PEER_OK(copy_seg(p, k, sv.m, p->h_m, false));
       PEER_OK(copy_seg(p, k, sv.v, p->h_v, false));
@@ -508,10 +566,17 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
 
 template <typename T>
 bool run_step(atom_peer* p, float* loss_out) {
-  p->t += 1;
-  bool sync = (p->cfg.sync_every > 0 && p->t % p->cfg.sync_every == 0) || p->sync_next;
-  p->sync_next = false;
+  // gradient rounds (R37): step = round; the optimizer step count t advances on update rounds
+  const int R = p->cfg.grad_rounds;
+  p->round = R > 0 ? (int)(p->steps % R) : 0;
+  p->upd_round = R <= 0 || p->round == R - 1;
+  if (p->upd_round) p->t += 1;
+  bool sync = p->upd_round && ((p->cfg.sync_every > 0 && p->t % p->cfg.sync_every == 0) || p->sync_next);
+  if (p->upd_round) p->sync_next = false;
   if (p->nranks <= 1) sync = sync && false;
+  // host update placement averages the updated host masters after the step (standalone pass)
+  const bool flush_after = sync && R > 0;
+  if (flush_after) sync = false;
   const std::vector<Op>& ops = sync ? p->ops_sync : p->ops;
   const std::vector<int>& endq = sync ? p->endq_sync : p->endq;
   if (p->trace_ev.size() < 2 * ops.size()) {
@@ -531,6 +596,7 @@ bool run_step(atom_peer* p, float* loss_out) {
   p->steps++;
   PEER_CUDA(cudaEventSynchronize(p->ev_loss));
   *loss_out = *p->h_loss;
+  if (flush_after) PEER_OK(peer_flush_average(p));
   return true;
 }
 
@@ -541,7 +607,7 @@ namespace atom {
 
 bool peer_stream_sync(atom_peer* p) {
   PEER_CUDA(cudaSetDevice(p->device));
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn, p->s_cpu})
     if (s) PEER_CUDA(cudaStreamSynchronize(s));
   return true;
 }
@@ -572,6 +638,12 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_side, cudaStreamNonBlocking));
   PEER_CUDA(cudaStreamCreateWithFlags(&p->s_attn, cudaStreamNonBlocking));
+  if (p->cfg.grad_rounds > 0) {
+    PEER_CUDA(cudaStreamCreateWithFlags(&p->s_cpu, cudaStreamNonBlocking));
+    p->cpu_ev.assign(p->S, nullptr);
+    p->cpu_ev_set.assign(p->S, 0);
+    for (auto& ev : p->cpu_ev) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
   for (auto& ev : p->ev_side) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   {
     const char* e = getenv("ATOM_SIDE_WGRAD");   // 0: all block-backward kernels on one stream
@@ -594,6 +666,13 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   }
   memset(p->h_m, 0, nb);
   memset(p->h_v, 0, nb);
+  if (p->cfg.grad_rounds > 0) {   // host gradient sums (R37)
+    if (cudaHostAlloc((void**)&p->h_gacc, nb, cudaHostAllocPortable) != cudaSuccess) {
+      set_error("pinned host allocation of %zu bytes (gradient sums) failed", nb);
+      return false;
+    }
+    memset(p->h_gacc, 0, nb);
+  }
   PEER_CUDA(cudaHostAlloc((void**)&p->h_tokens, 4 * (size_t)p->C * dm.b * (dm.T + 1), cudaHostAllocPortable));
   PEER_CUDA(cudaHostAlloc((void**)&p->h_loss, 64, cudaHostAllocPortable));
   // carve the arena: r1 | slots | stash | hfin | work
@@ -955,19 +1034,21 @@ void peer_reset_stats(atom_peer* p, int timing) {
 
 void peer_free(atom_peer* p) {
   cudaSetDevice(p->device);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn, p->s_cpu})
     if (s) cudaStreamSynchronize(s);
   if (p->comm) ncclCommDestroy(p->comm);
   for (auto ev : p->ev_side)
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : p->cpu_ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& kv : p->op_ev) cudaEventDestroy(kv.second);
   for (auto ev : p->trace_ev) cudaEventDestroy(ev);
   for (auto ev : p->gemm_ev) cudaEventDestroy(ev);
   if (p->ev_loss) cudaEventDestroy(p->ev_loss);
   if (p->step_start) cudaEventDestroy(p->step_start);
-  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn})
+  for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn, p->s_cpu})
     if (s) cudaStreamDestroy(s);
-  for (float* h : {p->h_master, p->h_m, p->h_v, p->h_loss})
+  for (float* h : {p->h_master, p->h_m, p->h_v, p->h_loss, p->h_gacc})
     if (h) cudaFreeHost(h);
   if (p->h_tokens) cudaFreeHost(p->h_tokens);
 }

@@ -1,6 +1,7 @@
 // Internal (C++) declarations of libatom's kernel launchers.  The C-ABI lives in
 // include/atom.h (training step) and include/atom_kernels.h (per-kernel test entry points).
 #pragma once
+#include "adam.h"
 #include "common.cuh"
 #include "epilogue.cuh"
 
@@ -36,8 +37,8 @@ template <typename T> bool embed_fwd(const int32_t* tok, long tstride, int T_, l
 template <typename T> bool embed_bwd(const int32_t* tok, long tstride, int T_, int B, const T* dh, int V, int d, float* dwte,
                                      float* dwpe, int* scratch, cudaStream_t st);
 template <typename T> bool gelu_apply(const T* u, T* g, long n, cudaStream_t st);
-template <typename T> bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, float lr, float b1, float b2,
-                                 float eps, float wd, int t, cudaStream_t st);
+template <typename T> bool adamw(float* p, const float* g, float* m, float* v, T* w, long n, const AdamConsts& k,
+                                 cudaStream_t st);
 template <typename T> bool cast_params(const float* src, T* dst, long n, cudaStream_t st);
 bool init_normal(float* dst, long n, uint64_t seed, uint64_t base, float std, float fill, cudaStream_t st);
 bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st);

@@ -32,6 +32,11 @@ struct atom_peer {
   uint8_t* stash = nullptr;
   int policy = ATOM_ACT_STASH;          // resolved activation policy of the plan
   int n_recompute = 0;                  // blocks 1..n_recompute re-forward inside their backward
+  // host update placement (cfg.grad_rounds = R > 0, R37): this step's gradient round
+  // (0..R-1), whether it ends with an update, and the host gradient sums of sub-models 2..S
+  int round = 0;
+  bool upd_round = true;
+  float* h_gacc = nullptr;
   std::vector<int64_t> blk_off;         // per block: byte offset (from stash) of its first stash entry
   std::vector<char> blk_full;           // per block: full entries (1) or input checkpoints only (0)
   int64_t rc_off = -1;                  // byte offset of the entry the backward re-forward fills
@@ -61,6 +66,9 @@ struct atom_peer {
   // idle; ev_side[0] forks, ev_side[1..3] mark the WFC / WO / WQKV gradients done
   cudaStream_t s_side = nullptr;
   cudaStream_t s_attn = nullptr;        // the attention backward's dQ kernel, beside dK/dV
+  cudaStream_t s_cpu = nullptr;         // CPU AdamW host functions (R37), off the copy streams
+  std::vector<cudaEvent_t> cpu_ev;      // per segment: its last CPU AdamW finished (index k - 1)
+  std::vector<char> cpu_ev_set;
   cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
   bool side_wgrad = true;
   std::map<std::pair<int, int>, cudaEvent_t> op_ev;  // (kind, seg) -> completion event

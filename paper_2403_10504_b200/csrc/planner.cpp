@@ -103,9 +103,12 @@ Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw) 
     const i128 p = dm.P[i];
     k.P.push_back(dm.P[i]);
     k.tlf.push_back(ceil_ns(4 * p, link_bw));
-    k.tlb.push_back(ceil_ns(12 * p, link_bw));
-    k.tmv.push_back(ceil_ns(8 * p, link_bw));
-    k.ts.push_back(ceil_ns(12 * p, d2h));
+    // grad_rounds > 0 (host update placement, R37): the backward loads master + gradient sum
+    // (the last segment: the sum alone) and stores the sum back
+    const bool hu = c.grad_rounds > 0;
+    k.tlb.push_back(ceil_ns((hu ? 8 : 12) * p, link_bw));
+    k.tmv.push_back(ceil_ns((hu ? 4 : 8) * p, link_bw));
+    k.ts.push_back(ceil_ns((hu ? 4 : 12) * p, d2h));
   }
   return k;
 }
@@ -469,10 +472,11 @@ static void fill_plan(const Eval& ev, int C, const std::vector<int>& ends, int64
   for (int t = 0; t < S; ++t) P.push_back(Eval::s(ev.pP, t == 0 ? 0 : ends[t - 1] + 1, ends[t]));
   int64_t h2d = 0, d2h = 0;
   if (S >= 2) {
+    const bool hu = ev.c.grad_rounds > 0;
     for (int t = 1; t < S; ++t) h2d += 4 * P[t];
-    for (int t = 1; t < S - 1; ++t) h2d += 12 * P[t];
-    h2d += 8 * P[S - 1];
-    for (int t = 1; t < S; ++t) d2h += 12 * P[t];
+    for (int t = 1; t < S - 1; ++t) h2d += (hu ? 8 : 12) * P[t];
+    h2d += (hu ? 4 : 8) * P[S - 1];
+    for (int t = 1; t < S; ++t) d2h += (hu ? 4 : 12) * P[t];
   }
   p->pred_h2d_B = h2d;
   p->pred_d2h_B = d2h;

@@ -68,3 +68,27 @@ def test_two_peer_sync_equals_mean_of_independent_updates():
     assert np.allclose(prs[0].p, mean, atol=1e-15) and np.allclose(prs[1].p, mean, atol=1e-15)
     assert np.array_equal(prs[0].m, ind[0].m) and np.array_equal(prs[1].v, ind[1].v)   # moments stay local
     assert np.allclose(losses[0][0], gpt.loss_only(cfg, p0, toks[0][0]))
+
+
+def test_gradient_rounds_equal_one_step_on_the_joined_batch():
+    """Host update placement (R37): R = 2 rounds on batches A and B, then AdamW on the mean
+    gradient, equals one plain step on the batch A + B (the loss is a mean over equally many
+    tokens, so its gradient is the mean of the two); R = 1 is the plain step."""
+    cfg = synth.GPTConfig("micro", 1, 16, 2, 8, 32, 2)
+    p0 = synth.init_params(cfg, seed=4, perturb=True, dtype=np.float64)
+    h = adamw.AdamWHyper(lr=1e-2, warmup_steps=0)
+    a, b = synth.tokens(cfg, 2, 11), synth.tokens(cfg, 2, 12)
+    two = peers.Peer(cfg, p0, h, grad_rounds=2)
+    two.step(a)
+    assert np.array_equal(two.p, p0) and two.t == 0          # no update after the first round
+    two.step(b)
+    one = peers.Peer(cfg, p0, h)
+    one.step(np.concatenate([a, b]))
+    assert two.t == 1
+    for x, y in ((two.p, one.p), (two.m, one.m), (two.v, one.v)):
+        assert np.allclose(x, y, rtol=1e-12, atol=1e-15)
+    r1, plain = peers.Peer(cfg, p0, h, grad_rounds=1), peers.Peer(cfg, p0, h)
+    for s in range(2):
+        r1.step(synth.tokens(cfg, 2, 20 + s))
+        plain.step(synth.tokens(cfg, 2, 20 + s))
+    assert np.array_equal(r1.p, plain.p) and np.array_equal(r1.v, plain.v)

@@ -142,6 +142,7 @@ def _rand_plan_cfg(rng):
         c.state_budget = rng.randint(10 ** 4, 10 ** 7)
     c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE, pl.ACT_HYBRID])
     c.n_recompute = rng.randint(0, L)
+    c.grad_rounds = rng.choice([0, 0, 2])
     if rng.random() < 0.7:
         tf = [0] + [rng.randint(1, 400) for _ in range(n - 1)]
         c.cost_table = sum(([t, 2 * t + rng.randint(0, 50)] for t in tf), [])
@@ -153,7 +154,7 @@ def _rand_plan_cfg(rng):
 def test_dp_equals_brute_force():
     rng = random.Random(7)
     found = deep = 0
-    for trial in range(900):
+    for trial in range(1100):
         c = _rand_plan_cfg(rng)
         link = rng.choice([10 ** 9, 10 ** 10, 3 * 10 ** 10])
         ev = pl.Evaluator(c, 0, link)

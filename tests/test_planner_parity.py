@@ -18,7 +18,7 @@ def _both(c: pl.PlanCfg, budget, link):
     ac = atom.make_cfg(g, dtype=c.dtype, C_=c.C, max_C=c.max_C, overlap_check=c.overlap_check,
                        peak_flops=c.peak_flops, d2h_bw=c.d2h_bw, state_budget=c.state_budget,
                        cost_table=c.cost_table, forced_ends=c.forced_ends, act_policy=c.act_policy,
-                       n_recompute=c.n_recompute)
+                       n_recompute=c.n_recompute, grad_rounds=c.grad_rounds)
     want = pl.plan(c, budget, link)
     try:
         got = atom.atom_plan(ac, budget, link)
@@ -57,6 +57,7 @@ def test_random_configs_bit_exact():
             c.C = rng.randint(1, 6)
         c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH, pl.ACT_RECOMPUTE, pl.ACT_HYBRID])
         c.n_recompute = rng.randint(0, L)
+        c.grad_rounds = rng.choice([0, 0, 1, 3])
         link = rng.choice([10 ** 8, 10 ** 9, 10 ** 10])
         hi = pl.Evaluator(c, 10 ** 18, link).device_bytes(1, [L + 1])
         budget = rng.randint(hi // 4, int(hi * 1.5))
