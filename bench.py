@@ -52,9 +52,15 @@ WORKLOADS = {
              "profiled compute rate"),
     "13b": ("13b", 0, "GPT-3 13B (40L, d=5120, 40x128 heads, T=2048, b=4): weights and AdamW state host-resident "
             "(236 GB of device state would be needed), swapped per sub-model through the whole HBM"),
-    "small": ("small", 0, "GPT-3 Small 125M (12L, d=768), per-layer sub-models"),
+    "small": ("small", 0, "GPT-3 Small 125M (12L, d=768, 12x64 heads, T=2048, b=8) swapped one layer per sub-model "
+              "(forced partition, C=8, overlap check off: at 49.7 GB/s no hidden plan exists below the resident "
+              "one -- Small's compute per layer is too short to cover its load, the case P:295 describes)"),
     "tiny": ("tiny", 3 * 10 ** 6, "tiny GPT (4L, d=64, T=32, V=256)"),
 }
+
+
+# workloads with a fixed partition instead of the planner's (cfg overrides)
+FORCED = {"small": {"forced_ends": list(range(14)), "C_": 8, "overlap_check": 0}}
 
 
 def host_mem_available():
@@ -342,11 +348,12 @@ def main():
     hbm_budget = int(free - 6 * 2 ** 30)
     # peer averaging cadence from a global batch of 512 sequences (reading R17)
     plan_tf = args.planner_tflops or pk["bf16_tflops"]
+    forced = FORCED.get(args.config, {})
     cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(plan_tf * 1e12),
-                        state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds)
+                        state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds, **forced)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
     profiled = None
-    if not args.planner_tflops and not args.no_profile:
+    if not args.planner_tflops and not args.no_profile and not forced:
         # measured profile -> plan (R34): run the first plan for a few
         # steps, measure the compute rate it sustains, re-plan with that rate (min over ranks so
         # every peer gets the same plan)
