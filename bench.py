@@ -245,8 +245,8 @@ def run_reference(args, g, wl_desc):
     print(json.dumps(line), flush=True)
 
 
-GEMM_NCU = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01f_gemm_step_ncu.json")
-GEMM_NCU_SHAPES = [("qkv", 16384, 7680, 2560, 0), ("proj", 16384, 2560, 2560, 1), ("fc", 16384, 10240, 2560, 0),
+GEMM_NCU = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01j_gemm_step_ncu.json")
+GEMM_NCU_SHAPES = [("qkv", 16384, 7680, 2560, 0), ("proj", 16384, 2560, 2560, 0), ("fc", 16384, 10240, 2560, 0),
                    ("fc2", 16384, 2560, 10240, 1)]
 
 
