@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libatom.so")
+# ATOM_LIB: an alternative build of the same library (tools/build_variant.py A/B experiments)
+LIB_PATH = os.environ.get("ATOM_LIB") or os.path.join(HERE, "libatom.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libatom.so not built at {LIB_PATH}; run `python -m paper_2403_10504_b200.build`")

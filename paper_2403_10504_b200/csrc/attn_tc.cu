@@ -199,6 +199,18 @@ __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
   return d;
 }
 // exp2_poly on a packed pair (same arithmetic, two lanes per instruction)
+// which exponential pairs (of every 8) go to the FMA-pipe polynomial: K of them, spread evenly.
+// Measured on B200 (tools/gpu_run51-53.sh, B=8 T=2048): the d_h = 80 forward is fastest with 3 of
+// 8 (616 -> 631 TF/s); both backward kernels with none (2.7B 992 -> 915 us, XL 617 -> 589 us):
+// their MUFU pipe is not the limit, the polynomial's extra FMA issue is
+__host__ __device__ constexpr bool poly_pick(int p, int K) { return K > 0 && ((p & 7) * K) % 8 < K; }
+#ifndef ATOM_BWD_POLY_KV
+#define ATOM_BWD_POLY_KV 0
+#endif
+#ifndef ATOM_BWD_POLY_Q
+#define ATOM_BWD_POLY_Q 0
+#endif
+
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   float x0, x1;
   f2unpack(x2, x0, x1);
@@ -481,7 +493,10 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int NS = C::NSLOT;
   // of 8 pairs on the FMA pipe: MUFU.EX2 (16/clk/SM) keeps pace with the MMAs at d_h = 128 but
   // not with the shorter MMAs of d_h = 80 / 64
-  constexpr int POLY = DH >= 128 ? 0 : (DH >= 80 ? 1 : 2);
+#ifndef ATOM_FWD_POLY80
+#define ATOM_FWD_POLY80 3
+#endif
+  constexpr int POLY = DH >= 128 ? 0 : (DH >= 80 ? ATOM_FWD_POLY80 : 2);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sQ = sm;                        // tile t at + t * NP * PANEL
@@ -1213,7 +1228,7 @@ __global__ void __launch_bounds__(384, 1)
                          int T_, int h) {
   using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
-  constexpr int POLY = DH < 128;   // one pair in eight on the FMA pipe when the MMAs are short
+  constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sK = sm;
@@ -1380,7 +1395,7 @@ __global__ void __launch_bounds__(384, 1)
           const uint64_t d2 = h2 ? f2pack(d4.z, d4.w) : f2pack(d4.x, d4.y);
           const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
           uint64_t p2;
-          if (!masked && POLY && (c4 & 3) == 0 && h2 == 0) {
+          if (!masked && POLY && poly_pick(2 * c4 + h2, ATOM_BWD_POLY_KV)) {
             p2 = exp2_poly2(x2);
           } else {
             float x0, x1;
@@ -1595,7 +1610,7 @@ __global__ void __launch_bounds__(384, 1)
         const int c = 2 * c2;
         const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
         uint64_t p2;
-        if (!masked && (c2 & 3) == 0) {
+        if (!masked && poly_pick(c2, ATOM_BWD_POLY_Q)) {
           p2 = exp2_poly2(x2);
         } else {
           float x0, x1;
