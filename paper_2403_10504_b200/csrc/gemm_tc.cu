@@ -731,9 +731,18 @@ static int num_sms() {
 }
 
 // m-blocks per raster group: keep ~40 MB of A row panels (group_m x rows x K bf16) live in L2
-static int group_m_for(int K, int ctas_per_tile) {
+// Data-gradient GEMMs (B MN-major, A K-major) run faster with half the footprint: measured on B200
+// (tools/gpu_run55.sh, interleaved A/B) QKV data gradient +6.8 %, fc +1 %, fc2 +2.7 %; the forward
+// and weight-gradient GEMMs showed no gain
+#ifndef ATOM_GEMM_GROUP_MB
+#define ATOM_GEMM_GROUP_MB 40
+#endif
+#ifndef ATOM_GEMM_GROUP_MB_DGRAD
+#define ATOM_GEMM_GROUP_MB_DGRAD 20
+#endif
+static int group_m_for(int K, int ctas_per_tile, bool dgrad) {
   const long panel = (long)BM * ctas_per_tile * K * 2;
-  long g = (40L << 20) / (panel > 0 ? panel : 1);
+  long g = ((long)(dgrad ? ATOM_GEMM_GROUP_MB_DGRAD : ATOM_GEMM_GROUP_MB) << 20) / (panel > 0 ? panel : 1);
   return (int)(g < 2 ? 2 : g > GROUP_M ? GROUP_M : g);
 }
 
@@ -749,7 +758,7 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 1));
+  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 1, !A_MN && B_MN));
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
@@ -776,7 +785,7 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + Tc2Cfg::BN - 1) / Tc2Cfg::BN);
   const int clusters = std::min(tiles, num_sms() / 2);
-  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2));
+  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2, !A_MN && B_MN));
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
