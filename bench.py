@@ -103,7 +103,7 @@ def bind_to_gpu_numa(local):
     return None
 
 
-def link_probe(local, world, nbytes=1 << 30, reps=3):
+def link_probe(local, world, nbytes=2 << 30, reps=3, rounds=3):
     """Pinned host<->device rate per direction when every rank copies both ways at once (the
     backward phase's traffic): host DRAM, not PCIe, is what several peers share (4 GPUs of one
     socket: ~22 GB/s each way per GPU vs 49.7 alone, tools/host_bw_probe.py). Min over ranks."""
@@ -113,8 +113,8 @@ def link_probe(local, world, nbytes=1 << 30, reps=3):
     d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
     d2 = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    rate = 0.0
-    for _ in range(2):
+    rates = []
+    for _ in range(rounds):
         torch.cuda.synchronize()
         if world > 1:
             import torch.distributed as dist
@@ -128,7 +128,8 @@ def link_probe(local, world, nbytes=1 << 30, reps=3):
             for _ in range(reps):
                 h2.copy_(d2, non_blocking=True)
         torch.cuda.synchronize()
-        rate = reps * nbytes / (time.perf_counter() - t)
+        rates.append(reps * nbytes / (time.perf_counter() - t))
+    rate = statistics.median(rates)   # one slow round (page faults, a neighbour's burst) is not the link
     del h, h2, d, d2
     torch.cuda.empty_cache()
     if world > 1:
@@ -403,6 +404,10 @@ def main():
             dist.barrier()
             torch.cuda.synchronize()
 
+    if world > 1:
+        # the first warm-up step averages too: NCCL sets up its connections on a communicator's
+        # first collective (hundreds of ms), which must not land in a timed step
+        atom.atom_sync([peer], flush=False)
     for i in range(args.warmup):
         peer.step_device(dev_batches[i])
     barrier()
