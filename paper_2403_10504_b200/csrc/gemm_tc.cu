@@ -17,6 +17,7 @@
 //   warp 2      TMEM allocator (2*BN columns)
 //   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused epilogue -> global
 #include <cuda.h>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -438,11 +439,40 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Stream-K tail of the fp32-accumulating (weight-gradient) GEMMs: the last partial wave of tiles
+// (num_tiles % clusters of them) would leave most CTA pairs idle, so each of those tiles is split
+// into P parts along K, one work unit each, run by different pairs. A part writes its fp32 partial
+// tile to a workspace; the last part of a tile to finish (atomic ticket: who, never the order)
+// adds the P partials in part order to the output -- deterministic. No unit ever waits for another.
+struct SplitK {
+  int base = 0;          // tiles processed whole (units 0 .. base-1)
+  int P = 1;             // parts per tail tile (1: no split)
+  float* ws = nullptr;   // [tail * P][2 CTAs][BM][BN] fp32 partials
+  int* ticket = nullptr; // [tail][2], zero between launches
+};
+struct Unit {
+  int tile, kb0, kb1, part, tail;
+};
+__device__ __forceinline__ Unit unit_of(int u, int num_kb, const SplitK& sk) {
+  Unit w;
+  if (sk.P <= 1 || u < sk.base) {
+    w.tile = u; w.kb0 = 0; w.kb1 = num_kb; w.part = -1; w.tail = -1;
+  } else {
+    const int v = u - sk.base;
+    w.tail = v / sk.P;
+    w.part = v % sk.P;
+    w.tile = sk.base + w.tail;
+    w.kb0 = (int)((long)w.part * num_kb / sk.P);
+    w.kb1 = (int)((long)(w.part + 1) * num_kb / sk.P);
+  }
+  return w;
+}
+
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
-                    int K, Epi epi, int group_m) {
+                    int K, Epi epi, int group_m, SplitK sk) {
   using Cfg = Tc2Cfg;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -465,6 +495,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int num_kb = (K + BK - 1) / BK;
   const int cluster_id = blockIdx.x >> 1;
   const int num_clusters = gridDim.x >> 1;
+  const int num_units = sk.P <= 1 ? num_tiles : sk.base + (num_tiles - sk.base) * sk.P;
+  __shared__ int sk_last;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -496,12 +528,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      for (int u = cluster_id; u < num_units; u += num_clusters) {
+        const Unit w = unit_of(u, num_kb, sk);
         int mb, nb;
-        tile_coords(tile, num_m, num_n, &mb, &nb, group_m);
+        tile_coords(w.tile, num_m, num_n, &mb, &nb, group_m);
         const int m0 = mb * 2 * BM + rank * BM;
         const int n0 = nb * BN + rank * Cfg::HB;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
@@ -542,13 +575,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+      for (int u = cluster_id; u < num_units; u += num_clusters, ++it) {
+        const Unit w = unit_of(u, num_kb, sk);
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elected) {
@@ -557,10 +591,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t ad = a_desc0 + sofs + (A_MN ? kk * 128 : kk * 2);
               const uint64_t bd = b_desc0 + sofs + (B_MN ? kk * 128 : kk * 2);
-              tc_mma_pair(tmem_d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+              tc_mma_pair(tmem_d, ad, bd, idesc, (kb != w.kb0 || kk != 0) ? 1u : 0u);
             }
             tc_commit_pair(&empty[stage]);
-            if (kb == num_kb - 1) tc_commit_pair(&tfull[acc]);
+            if (kb == w.kb1 - 1) tc_commit_pair(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == Cfg::STAGES) {
@@ -574,7 +608,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------------------------------------------------------- epilogue (both CTAs)
     const int q = warp & 3;
     int it = 0;
-    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++it) {
+    for (int u = cluster_id; u < num_units; u += num_clusters, ++it) {
+      const Unit w = unit_of(u, num_kb, sk);
+      const int tile = w.tile;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mb, nb;
@@ -585,7 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // fast path: interior tiles of the modes without per-row global operands (the residual /
       // pre-activation prefetch of EPI_BIAS_RES / EPI_DGELU measured slower than the plain loop)
       const bool fast = (epi.mode == EPI_STORE || epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_GELU) &&
-                        m0 + BM <= M && n0 + BN <= N;
+                        m0 + BM <= M && n0 + BN <= N && w.part < 0;
       const bool has_bias = epi.mode == EPI_BIAS || epi.mode == EPI_BIAS_RES || epi.mode == EPI_BIAS_GELU;
       bf16* sb = sbias + q * BN;
       if (fast && has_bias) {   // this tile's bias row into the warp's smem row (before the wait)
@@ -596,7 +632,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
-      if (fast) {
+      if (w.part >= 0) {
+        // stream-K tail unit (fp32 accumulate): this part's partial tile to the workspace; the last
+        // part of this CTA's half-tile to finish adds all parts in part order to the output
+        const int r = 32 * q + lane;
+        float* wsp = sk.ws + ((long)(w.tail * sk.P + w.part) * 2 + rank) * (BM * BN) + (long)r * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(trow + c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            __stcg((float4*)(wsp + c0 + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) sk_last = atomicAdd(&sk.ticket[2 * w.tail + rank], 1) == sk.P - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (sk_last) {
+          __threadfence();
+          const float* w0 = sk.ws + ((long)(w.tail * sk.P) * 2 + rank) * (BM * BN) + (long)r * BN;
+          const long pstride = 2L * BM * BN;
+          float* orow = (float*)epi.out + m * epi.ldo;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 4) {
+            const int n = n0 + c0;
+            if (m >= M || n >= N) continue;
+            float4 t = __ldcg((const float4*)(w0 + c0));
+            for (int p = 1; p < sk.P; ++p) {
+              const float4 x = __ldcg((const float4*)(w0 + p * pstride + c0));
+              t.x += x.x; t.y += x.y; t.z += x.z; t.w += x.w;
+            }
+            const float tv[4] = {t.x, t.y, t.z, t.w};
+            for (int j = 0; j < 4 && n + j < N; ++j) orow[n + j] += tv[j];
+          }
+          if (q == 0 && lane == 0) sk.ticket[2 * w.tail + rank] = 0;
+        }
+      } else if (fast) {
         // interior tile, TMEM chunk c + 1 in flight while chunk c is finished.
         // TMA-store epilogue: each warp packs its 32 rows x 32 columns of a chunk into a 64B-swizzled
         // smem box per output and one lane stores the box (full-line writes instead of 32 scattered
@@ -764,6 +836,44 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
   return true;
 }
 
+// stream-K workspace per stream (a split GEMM only ever overlaps split GEMMs of other streams):
+// room for one partial tile per CTA pair (tail * P <= clusters) and the tickets, zeroed once
+struct SplitWs {
+  float* ws = nullptr;
+  int* ticket = nullptr;
+};
+// Off by default: in the 2.7B step the weight-gradient GEMMs run on a side stream whose tails the
+// main stream's kernels already fill, and the split's workspace traffic and final sums cost more
+// than the idle pairs it recovers (interleaved A/B on B200, tools/gpu_run60.sh: 53.4K tokens/s
+// with the split vs 55.1K without). ATOM_GEMM_SPLITK=1 turns it on (tests cover both).
+static bool splitk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("ATOM_GEMM_SPLITK");
+    on = v && v[0] == '1';
+  }
+  return on == 1;
+}
+static SplitWs* splitk_ws(cudaStream_t st, int clusters) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SplitWs> pool;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  SplitWs& w = pool[{dev, st}];
+  if (!w.ws) {
+    clusters = num_sms() / 2;   // the most any launch uses
+    const size_t nws = (size_t)clusters * 2 * BM * Tc2Cfg::BN;
+    if (cudaMalloc((void**)&w.ws, nws * sizeof(float)) != cudaSuccess ||
+        cudaMalloc((void**)&w.ticket, (size_t)clusters * 2 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(w.ticket, 0, (size_t)clusters * 2 * sizeof(int)) != cudaSuccess) {
+      set_error("gemm_tc: stream-K workspace allocation failed");
+      return nullptr;
+    }
+  }
+  return &w;
+}
+
 template <bool A_MN, bool B_MN>
 static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e,
                        cudaStream_t st) {
@@ -784,8 +894,24 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
     attr_set = true;
   }
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + Tc2Cfg::BN - 1) / Tc2Cfg::BN);
-  const int clusters = std::min(tiles, num_sms() / 2);
-  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2, !A_MN && B_MN));
+  int clusters = std::min(tiles, num_sms() / 2);
+  SplitK sk;
+  if (e.mode == EPI_ACC_F32 && splitk_enabled()) {
+    // stream-K tail: split the last partial wave's tiles along K so that it fills the CTA pairs
+    const int tail = tiles % clusters, num_kb = (K + BK - 1) / BK;
+    if (tiles > clusters && tail > 0) {
+      const int P = std::min(std::min(clusters / tail, 16), num_kb / 4);
+      if (P >= 2) {
+        SplitWs* w = splitk_ws(st, clusters);
+        if (!w) return false;
+        sk.base = tiles - tail;
+        sk.P = P;
+        sk.ws = w->ws;
+        sk.ticket = w->ticket;
+      }
+    }
+  }
+  kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2, !A_MN && B_MN), sk);
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;

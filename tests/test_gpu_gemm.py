@@ -133,3 +133,18 @@ def test_tc_gemm_deterministic():
         outs.append(o)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("shape", [(3840, 2560, 2048), (4096, 4096, 1024), (2560 + 200, 2560 + 40, 1536)],
+                         ids=["tail2-P8", "tail34-P2", "ragged"])
+@pytest.mark.parametrize("majors", [(True, True), (False, False)], ids=["wgrad", "kmajor"])
+def test_tc_gemm_acc_f32_streamk_tail(shape, majors):
+    """Weight-gradient GEMMs (fp32 accumulate) whose last wave is split along K (stream-K tail,
+    gemm_tc.cu SplitK, ATOM_GEMM_SPLITK=1 -- read once per process, so this test runs the split
+    only when the variable is set for the test run): same result as the unsplit math within fp32
+    rounding, and deterministic."""
+    M, N, K = shape
+    ref, got = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, atom.EPI_ACC_F32, 512)
+    _close(ref, got, torch.bfloat16, K)
+    ref2, got2 = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, atom.EPI_ACC_F32, 512)
+    assert torch.equal(got, got2)
