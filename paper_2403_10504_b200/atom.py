@@ -336,3 +336,14 @@ def k_attn_fwd(impl, dtype, qkv, o, lse, B, T, h, dh, stream=0):
 
 def k_attn_bwd(impl, dtype, qkv, o, dout, lse, dsum, dqkv, B, T, h, dh, stream=0):
     return check(lib.atom_k_attn_bwd(impl, dtype, qkv, o, dout, lse, dsum, dqkv, B, T, h, dh, stream or None))
+
+
+DROP_EMBD, DROP_ATTN, DROP_RESID_ATTN, DROP_RESID_MLP = 0, 1, 2, 3
+lib.atom_k_dropout.restype = C.c_int
+lib.atom_k_dropout.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_long, C.c_double, C.c_ulonglong, C.c_int,
+                               C.c_int, C.c_int, C.c_void_p]
+
+
+def k_dropout(dtype, x, y, n, p, seed, site, layer, micro_step, stream=0):
+    """atom_k_dropout on device pointers x, y (x == y allowed): y = x * keep / (1 - p)."""
+    return check(lib.atom_k_dropout(dtype, x, y, n, p, seed, site, layer, micro_step, stream or None))
