@@ -1,8 +1,12 @@
 """Achieved HBM GB/s of atom_k_dropout at the 2.7B site shapes (CUDA events, warm, L2-sized inputs
 exceeded).  Algorithmic bytes: 2 x sizeof(T) per element (read x, write y).  Prints one JSON line."""
 import json
+import os
+import sys
 
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2403_10504_b200 import atom
 
