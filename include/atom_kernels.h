@@ -50,11 +50,11 @@ int atom_k_cpu_adamw(float* p, const float* g, float* m, float* v, long n, float
                      float wd, long t, float gscale, int threads);
 
 /* Dropout site multiplier, in place allowed (x == y): y[i] = x[i] * keep(i) / (1 - p) on n
- * elements of dtype ATOM_FP32 (x, y 16-byte aligned) or ATOM_BF16 (8-byte aligned), fp32 math.
- * keep(i) = (word i % 4 of Philox4x32-10(counter = (i / 4, site, layer, micro_step),
- * key = (seed & 0xffffffff, seed >> 32))) >= floor(p * 2^32).  SURVEY §8 NEXT-4 (minGPT's embd /
+ * elements of dtype ATOM_FP32 or ATOM_BF16 (x, y 16-byte aligned), fp32 math.
+ * keep(i) = (16-bit half i % 2 (0 = low) of word (i / 2) % 4 of Philox4x32-10(counter =
+ * (i / 8, site, layer, micro_step), key = (seed & 0xffffffff, seed >> 32))) >= floor(p * 2^16).  SURVEY §8 NEXT-4 (minGPT's embd /
  * attn / resid dropout, the paper's profiled dropout layer); R38.  The
- * backward of a site is the same call on dy.  Requires 0 <= p < 1, n <= 2^34, else
+ * backward of a site is the same call on dy.  Requires 0 <= p < 1, n <= 2^35, else
  * ATOM_E_INVALID. */
 int atom_k_dropout(int dtype, const void* x, void* y, long n, double p, unsigned long long seed, int site, int layer,
                    int micro_step, void* stream);

@@ -14,9 +14,10 @@ out as its definition:
 Pinned by the published known-answer vectors (tests/test_oracle_dropout.py).
 
 Dropout reading (R38): element i (row-major flat index of the site tensor of one
-micro-batch) takes word i % 4 of philox(counter = (i // 4, site, layer, micro_step),
-key = (seed mod 2^32, seed >> 32)); it is dropped iff that word < floor(p * 2^32), kept ones are
-scaled by 1 / (1 - p) (inverted dropout, minGPT / torch.nn.Dropout).
+micro-batch) takes 16-bit half i % 2 (0 = low) of word (i // 2) % 4 of
+philox(counter = (i // 8, site, layer, micro_step), key = (seed mod 2^32, seed >> 32)); it is
+dropped iff that half < floor(p * 2^16), kept ones are scaled by 1 / (1 - p) (inverted dropout,
+minGPT / torch.nn.Dropout).  One Philox call serves 8 elements (p resolution 2^-16).
 """
 from __future__ import annotations
 
@@ -46,18 +47,19 @@ def philox4x32_10(counter, key):
     return [x.astype(np.uint32) for x in c]
 
 
-def uniform_words(n, site, layer, micro_step, seed):
-    """The n uint32 words of one site tensor (flat index order)."""
-    g = np.arange((n + 3) // 4, dtype=np.uint64)       # counter word 0 = i // 4
+def uniform_halves(n, site, layer, micro_step, seed):
+    """The n uint16 draws of one site tensor (flat index order)."""
+    g = np.arange((n + 7) // 8, dtype=np.uint64)       # counter word 0 = i // 8
     z = np.zeros_like(g)
     words = philox4x32_10((g, z + site, z + layer, z + micro_step), (seed & MASK32, seed >> 32))
-    w = np.stack(words, axis=-1).reshape(-1)          # word j of group g -> flat 4g + j
-    return w[:n]
+    w = np.stack(words, axis=-1).reshape(-1)          # word j of group g -> 4g + j
+    halves = np.stack([w & 0xFFFF, w >> 16], axis=-1).reshape(-1)   # half h of word k -> 2k + h
+    return halves[:n].astype(np.uint16)
 
 
 def keep_scale(shape, p, site, layer, micro_step, seed):
     """fp64 multiplier of the site tensor: 0 where dropped, 1/(1-p) where kept."""
     n = int(np.prod(shape))
-    thr = np.uint32(int(np.floor(p * 2.0 ** 32)))
-    keep = uniform_words(n, site, layer, micro_step, seed)[:n] >= thr
+    thr = np.uint16(int(np.floor(p * 2.0 ** 16)))
+    keep = uniform_halves(n, site, layer, micro_step, seed) >= thr
     return (keep.astype(np.float64) / (1.0 - p)).reshape(shape)

@@ -1,12 +1,14 @@
 // Dropout site multiplier y = x * keep(i) / (1 - p) with an in-kernel Philox4x32-10 stream
 // (minGPT's embd / attn / resid dropout, the paper's profiled dropout layer,
-// PAPER.md P:184).  Reading DESIGN.md R38: element i of one site tensor takes word i % 4 of
-// Philox4x32-10(counter = (i / 4, site, layer, micro_step), key = (seed lo, seed hi)); it is kept
-// iff that word >= thr = floor(p * 2^32) (computed on the host in double).  The same call is the
-// backward (dx = dy * the same multiplier).
+// PAPER.md P:184).  Reading DESIGN.md R38: element i of one site tensor takes 16-bit half i % 2
+// (0 = low) of word (i / 2) % 4 of Philox4x32-10(counter = (i / 8, site, layer, micro_step),
+// key = (seed lo, seed hi)); it is kept iff that half >= thr = floor(p * 2^16) (host double).
+// The same call is the backward (dx = dy * the same multiplier).
 //
-// HBM-bound: one thread per Philox group (4 elements, one 16 B fp32 / 8 B bf16 vector), grid
-// stride over a grid of 16 CTAs x 148 SMs; algorithmic bytes 2 x sizeof(T) per element.
+// HBM-bound: one thread per Philox group (8 elements: two 16 B fp32 vectors / one 16 B bf16
+// vector), grid stride over 16 CTAs x 148 SMs; algorithmic bytes 2 x sizeof(T) per element.  With
+// 32-bit draws (4 elements per Philox call) the bf16 kernel was ALU-bound at 3.3-3.8 TB/s
+// (profiles/r01k_dropout.txt); 16-bit halves halve the Philox work per element.
 #include "../../include/atom_kernels.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -27,29 +29,36 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
-template <typename T> struct Quad;
-template <> struct Quad<float> {
-  static __device__ __forceinline__ void load(const float* p, float v[4]) {
-    const float4 q = *reinterpret_cast<const float4*>(p);
-    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+template <typename T> struct Oct;
+template <> struct Oct<float> {
+  static __device__ __forceinline__ void load(const float* p, float v[8]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
   }
-  static __device__ __forceinline__ void store(float* p, const float v[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  static __device__ __forceinline__ void store(float* p, const float v[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
   }
 };
-template <> struct Quad<bf16> {
-  static __device__ __forceinline__ void load(const bf16* p, float v[4]) {
-    const uint2 q = *reinterpret_cast<const uint2*>(p);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.y));
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+template <> struct Oct<bf16> {
+  static __device__ __forceinline__ void load(const bf16* p, float v[8]) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[j]));
+      v[2 * j] = f.x;
+      v[2 * j + 1] = f.y;
+    }
   }
-  static __device__ __forceinline__ void store(bf16* p, const float v[4]) {
-    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-    uint2 q;
-    q.x = *reinterpret_cast<uint32_t*>(&a);
-    q.y = *reinterpret_cast<uint32_t*>(&b);
-    *reinterpret_cast<uint2*>(p) = q;
+  static __device__ __forceinline__ void store(bf16* p, const float v[8]) {
+    uint32_t u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      u[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(u[0], u[1], u[2], u[3]);
   }
 };
 
@@ -57,21 +66,27 @@ template <typename T>
 __global__ void __launch_bounds__(256) dropout_kernel(const T* x, T* y, long n, uint32_t thr,
                                                       float scale, uint32_t site, uint32_t layer, uint32_t step,
                                                       uint32_t k0, uint32_t k1) {
-  const long groups = (n + 3) >> 2;
+  const long groups = (n + 7) >> 3;
   for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < groups; g += (long)gridDim.x * blockDim.x) {
     const uint4 w = philox4x32_10(make_uint4((uint32_t)g, site, layer, step), k0, k1);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    const long i0 = g << 2;
-    float v[4];
-    if (i0 + 4 <= n) {
-      Quad<T>::load(x + i0, v);
+    uint32_t r[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] = ws[j] >= thr ? v[j] * scale : 0.f;
-      Quad<T>::store(y + i0, v);
+    for (int j = 0; j < 4; ++j) {
+      r[2 * j] = ws[j] & 0xFFFFu;
+      r[2 * j + 1] = ws[j] >> 16;
+    }
+    const long i0 = g << 3;
+    float v[8];
+    if (i0 + 8 <= n) {
+      Oct<T>::load(x + i0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = r[j] >= thr ? v[j] * scale : 0.f;
+      Oct<T>::store(y + i0, v);
     } else {
       for (long i = i0; i < n; ++i) {
         const float xv = to_f(x[i]);
-        y[i] = from_f<T>(ws[i - i0] >= thr ? xv * scale : 0.f);
+        y[i] = from_f<T>(r[i - i0] >= thr ? xv * scale : 0.f);
       }
     }
   }
@@ -81,9 +96,9 @@ template <typename T>
 bool dropout(const T* x, T* y, long n, double p, uint64_t seed, uint32_t site, uint32_t layer, uint32_t step,
              cudaStream_t st) {
   if (n <= 0) return true;
-  const uint32_t thr = (uint32_t)floor(p * 4294967296.0);
+  const uint32_t thr = (uint32_t)floor(p * 65536.0);
   const float scale = (float)(1.0 / (1.0 - p));
-  const long groups = (n + 3) >> 2;
+  const long groups = (n + 7) >> 3;
   long g = (groups + 255) / 256;
   const int grid = (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
   dropout_kernel<T><<<grid, 256, 0, st>>>(x, y, n, thr, scale, site, layer, step, (uint32_t)seed,
@@ -103,11 +118,11 @@ extern "C" int atom_k_dropout(int dtype, const void* x, void* y, long n, double 
     set_error("atom_k_dropout: invalid arguments (need 0 <= p < 1, n >= 0, non-null buffers)");
     return ATOM_E_INVALID;
   }
-  if (n > (4l << 32)) {
-    set_error("atom_k_dropout: n > 2^34 (the Philox group index is one 32-bit counter word)");
+  if (n > (8l << 32)) {
+    set_error("atom_k_dropout: n > 2^35 (the Philox group index is one 32-bit counter word)");
     return ATOM_E_INVALID;
   }
-  const size_t align = dtype == ATOM_FP32 ? 16 : 8;
+  const size_t align = 16;
   if (((uintptr_t)x % align) || ((uintptr_t)y % align)) {
     set_error("atom_k_dropout: x and y must be %zu-byte aligned", align);
     return ATOM_E_INVALID;

@@ -2,7 +2,7 @@
 
 - the generator: Philox4x32-10 known-answer vectors published with the algorithm (Random123
   kat_vectors: counter / key all zero, all ones, and the pi digits);
-- the mask: flat index -> (counter, word) mapping, the keep rate within a binomial bound, the
+- the mask: flat index -> (counter, word, half) mapping, the keep rate within a binomial bound, the
   exact 1/(1-p) scale, independence of sites, layers and micro-steps;
 - the model: p = 0 reduces bit for bit to the dropout-free oracle; finite differences with a
   fixed mask; torch fp64 autograd of an independently written module fed the same masks.
@@ -34,10 +34,10 @@ def test_philox_known_answers(ctr, key, out):
 
 def test_flat_index_mapping():
     seed = (0x1234 << 32) | 0xABCD
-    w = philox.uniform_words(37, philox.SITE_ATTN, 5, 9, seed)
-    for i in (0, 1, 3, 4, 17, 36):
-        ref = philox.philox4x32_10((i // 4, philox.SITE_ATTN, 5, 9), (0xABCD, 0x1234))
-        assert int(w[i]) == int(ref[i % 4])
+    w = philox.uniform_halves(37, philox.SITE_ATTN, 5, 9, seed)
+    for i in (0, 1, 3, 4, 7, 8, 17, 36):
+        ref = int(philox.philox4x32_10((i // 8, philox.SITE_ATTN, 5, 9), (0xABCD, 0x1234))[(i // 2) % 4])
+        assert int(w[i]) == (ref >> 16 if i % 2 else ref & 0xFFFF)
 
 
 @pytest.mark.parametrize("p", [0.1, 0.5])
@@ -46,9 +46,10 @@ def test_keep_rate_and_scale(p):
     m = philox.keep_scale((n,), p, philox.SITE_RESID_MLP, 3, 0, 42)
     kept = m != 0
     assert np.all(m[kept] == 1.0 / (1.0 - p))
-    sd = math.sqrt(n * p * (1 - p))
-    assert abs((~kept).sum() - n * p) <= 6 * sd
-    assert abs(m.mean() - 1.0) <= 6 * sd / n / (1 - p)       # inverted dropout: E[m] = 1
+    p_eff = math.floor(p * 2 ** 16) / 2 ** 16                # drop probability of the 16-bit threshold
+    sd = math.sqrt(n * p_eff * (1 - p_eff))
+    assert abs((~kept).sum() - n * p_eff) <= 6 * sd
+    assert abs(m.mean() - (1 - p_eff) / (1 - p)) <= 6 * sd / n / (1 - p)   # E[m] = 1 + 1e-5 at p = 0.1
 
 
 def test_streams_differ():
