@@ -846,6 +846,13 @@ bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank) {
 bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abort_ops) {
   PEER_OK(peer_stream_sync(p));
   if (!p->comm || n_exclude == 0) return true;
+  if (p->nranks - n_exclude <= 1) {   // sole survivor: nothing left to shrink to, no NCCL call
+    ncclCommAbort(p->comm);
+    p->comm = nullptr;
+    p->nranks = 1;
+    p->rank = 0;
+    return true;
+  }
   ncclComm_t nc = nullptr;
   std::vector<int> ex(exclude, exclude + n_exclude);
   ncclResult_t r = ncclCommShrink(p->comm, ex.data(), n_exclude, &nc, nullptr,

@@ -86,8 +86,12 @@ class Coordinator:
     unique id (atom.atom_nccl_unique_id) -- only the leader calls it."""
 
     def __init__(self, store, pid: int, global_batch: int, ttl: float = 10.0, poll: float = 0.005,
-                 make_id: Optional[Callable[[], bytes]] = None, clock: Callable[[], float] = time.time):
+                 make_id: Optional[Callable[[], bytes]] = None, clock: Callable[[], float] = time.time,
+                 boot_grace: Optional[float] = None):
         self.store, self.pid, self.global_batch = store, pid, global_batch
+        # a member that has never heartbeated (still starting up) is declared dead only after
+        # boot_grace; one whose heartbeat went stale, after ttl
+        self.boot_grace = max(30.0, 4 * ttl) if boot_grace is None else boot_grace
         self.reg = Registry(store, ttl, clock)
         self.poll, self.make_id, self.clock = poll, make_id, clock
         self.members: List[int] = []
@@ -141,7 +145,7 @@ class Coordinator:
             for m, r in recs.items():
                 if r is not None and self.reg.fresh(r) and r["s"] >= s:
                     ready.append(m)
-                elif not ((r is None and now - t0 > self.reg.ttl) or (r is not None and not self.reg.fresh(r))):
+                elif not ((r is None and now - t0 > self.boot_grace) or (r is not None and not self.reg.fresh(r))):
                     waiting = True
             if not waiting and min(ready) == self.pid:
                 self.store.compare_set(key, "", self._decide(s, sorted(ready), recs).to_json())

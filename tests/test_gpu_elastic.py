@@ -14,6 +14,7 @@ import json
 import multiprocessing as mp
 import os
 import socket
+import sys
 import time
 
 import pytest
@@ -65,6 +66,7 @@ def _peer(pid, n0, port, q):
     log = {"pid": pid, "decs": [], "hash": {}, "info": {}}
     if pid == JOINER:
         peer = atom.Peer(cfg, plan, device=gpu, init_params=synth.init_params(g, seed=99), seed=0)
+        print(f"[elastic peer {pid}] registering as joiner", file=sys.stderr, flush=True)
         d = co.join()
         co.apply(d, peer, atom.atom_sync)
         log["decs"].append(d.to_json())
@@ -77,6 +79,12 @@ def _peer(pid, n0, port, q):
         peer = atom.Peer(cfg, plan, device=gpu, init_params=init, seed=0, nccl_id=nid, nranks=n0, rank=pid)
         co.start(list(range(n0)))
     while co.s < STEPS - 1:
+        if pid != JOINER and co.s == STEPS - 4:
+            # the joiner starts a fresh process after dec/{KILL_AT + 2}; on a fast box the members
+            # could finish every step before it registers, so hold until its ticket exists
+            while not store.check(["join/0"]):
+                time.sleep(0.01)
+        print(f"[elastic peer {pid}] s={co.s} members={co.members}", file=sys.stderr, flush=True)
         toks = synth.tokens(g, C * g.micro_batch, synth.step_seed(pid, co.s + 1))
         peer.step(toks)
         torch.cuda.synchronize()
