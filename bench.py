@@ -197,14 +197,16 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(g, seconds_hint=20.0):
-    """Time the fp64 oracle (fwd + hand bwd + AdamW) on one sequence of the workload through a
-    layer-reduced copy of the model (L = 1, same d, h, T, V) and extrapolate to the full depth by
-    algorithmic FLOPs.  Returns (tokens/s, sample description, cores)."""
+def cpu_sample(g, seconds_hint=20.0, max_steps=3):
+    """Time the oracle (fwd + hand bwd + AdamW) in fp32 on one
+    sequence of the workload through a layer-reduced copy of the model (L = 2, same d, h, T, V)
+    and extrapolate to the full depth by algorithmic FLOPs.  Returns (tokens/s at full depth,
+    sample description, cores, wall seconds per timed sample step)."""
     from oracle import adamw as oadamw
     from oracle import gpt as ogpt
-    g1 = synth.GPTConfig(g.name + "-L1", 1, g.d_model, g.n_head, g.seq_len, g.vocab, 1)
-    p = synth.init_params(g1, seed=1, dtype=np.float64)
+    L = min(2, g.n_layer)
+    g1 = synth.GPTConfig(g.name + f"-L{L}", L, g.d_model, g.n_head, g.seq_len, g.vocab, 1)
+    p = synth.init_params(g1, seed=1, dtype=np.float32)
     toks = synth.tokens(g1, 1, 5)
     h = oadamw.AdamWHyper()
     m = np.zeros_like(p)
@@ -212,35 +214,40 @@ def cpu_sample(g, seconds_hint=20.0):
     t0 = time.perf_counter()
     n = 0
     while True:
-        loss, grad = ogpt.loss_and_grad(g1, p, toks)
-        p, m, v = oadamw.adamw_step(h, n + 1, p, grad, m, v)
+        loss, grad = ogpt.loss_and_grad(g1, p, toks, dtype=np.float32)
+        p, m, v = oadamw.adamw_step(h, n + 1, p, grad, m, v, dtype=np.float32)
         n += 1
-        if time.perf_counter() - t0 > seconds_hint or n >= 3:
+        if time.perf_counter() - t0 > seconds_hint or n >= max_steps:
             break
     dt = (time.perf_counter() - t0) / n
     rate_sample = g.seq_len / dt
     rate = rate_sample * f_alg_per_token(g1) / f_alg_per_token(g)
-    desc = (f"oracle fp64 numpy fwd+bwd+AdamW on 1 sequence (T={g.seq_len}) of a 1-block copy of the model "
+    desc = (f"oracle fp32 numpy fwd+bwd+AdamW on 1 sequence (T={g.seq_len}) of a {L}-block copy of the model "
             f"(d={g.d_model}, V={g.vocab}); {n} step(s), {dt:.1f} s each; tokens/s scaled to L={g.n_layer} by "
             f"algorithmic FLOPs per token")
-    return rate, desc, os.cpu_count()
+    return rate, desc, os.cpu_count(), dt
 
 
 def run_reference(args, g, wl_desc):
-    """--impl reference: the oracle timed on this host (rank 0 only)."""
+    """--impl reference: the oracle timed on this host (rank 0 only).  A step = one timed sample
+    (one sequence through the L = 2 copy, fp32); ms_per_step is that sample's wall time, value the
+    full-depth tokens/s it extrapolates to."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rates = []
+    rates, walls = [], []
     for i in range(args.warmup + args.steps):
-        r, desc, cores = cpu_sample(g, seconds_hint=0.0)
+        r, desc, cores, dt = cpu_sample(g, seconds_hint=0.0, max_steps=1)
         if i >= args.warmup:
             rates.append(r)
+            walls.append(dt)
     val = statistics.median(rates)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": g.seq_len / val * 1000.0,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl_desc, "model": g.name, "seq_len": g.seq_len, "sample_tokens_per_step": g.seq_len},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl_desc, "model": g.name, "seq_len": g.seq_len, "sample_tokens_per_step": g.seq_len,
+                       "sample": "each step = one sequence through an L=2 copy of the model (fp32 oracle); "
+                                 "value = the full-depth tokens/s it extrapolates to by algorithmic FLOPs"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -276,27 +283,6 @@ def host_link(trace, plan, probe_gbs):
     return {"h2d_op_GBs": plan.pred_h2d_B / h2d / 1e6 if h2d > 0 else None,
             "d2h_op_GBs": plan.pred_d2h_B / d2h / 1e6 if d2h > 0 else None,
             "probe_bidir_GBs": probe_gbs, "solo_h2d_GBs": H2D_GBS, "solo_d2h_GBs": D2H_GBS}
-
-
-def compute_busy_pct(trace, step_ms):
-    """Share of the compute lane's span in the last step (its first op start -> last op end) in
-    which it runs an op (union of the traced intervals): what is left is the compute stream waiting
-    on swaps. (The step's first prefetch loads start during the previous step, so the whole-trace
-    span is longer than the step.)"""
-    iv = sorted((float(f[5]), float(f[6])) for f in (l.split() for l in trace.splitlines())
-                if len(f) >= 7 and f[0] == "compute")
-    busy, cur_s, cur_e = 0.0, None, None
-    for a, b in iv:
-        if cur_e is None or a > cur_e:
-            if cur_e is not None:
-                busy += cur_e - cur_s
-            cur_s, cur_e = a, b
-        else:
-            cur_e = max(cur_e, b)
-    if cur_e is not None:
-        busy += cur_e - cur_s
-    span = max(b for _, b in iv) - iv[0][0] if iv else 0.0
-    return 100.0 * busy / span if span > 0 else None
 
 
 def main():
@@ -428,6 +414,7 @@ def main():
     with Clocks(local) as clk:
         ms, losses = timed(peer.step_device, dev_batches[args.warmup:args.warmup + args.steps])
     st = peer.stats()
+    klog = peer.kernel_log()
     gemm_shapes = sorted(peer.gemm_log(), key=lambda r: -r["ms"])
     # e2e: host tokens through atom_step (pinned staging + H2D in the step), loss read back
     ms_e2e, _ = timed(peer.step, host_batches[args.warmup + args.steps:])
@@ -440,8 +427,11 @@ def main():
     # the slower of the FLOPs at tensor peak and the plan's swapped bytes over the host link (per
     # direction, the link alone): ~14 N in / 12 N out with the GPU AdamW (less the resident
     # sub-model 1), 12 N / 4 N with host gradient sums (--grad-rounds)
-    t_roof = max(tok_step * f_alg_per_token(g) / (pk["bf16_tflops"] * 1e12),
-                 plan.pred_h2d_B / (H2D_GBS * 1e9), plan.pred_d2h_B / (D2H_GBS * 1e9))
+    def t_roof_at(tflops):   # ms
+        return 1000.0 * max(tok_step * f_alg_per_token(g) / (tflops * 1e12),
+                            plan.pred_h2d_B / (H2D_GBS * 1e9), plan.pred_d2h_B / (D2H_GBS * 1e9))
+
+    t_roof = t_roof_at(pk["bf16_tflops"]) / 1000.0
     trace = peer.trace()
     if rank == 0 and args.trace_out:
         with open(args.trace_out, "w") as f:
@@ -449,7 +439,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            r, desc, cores = cpu_sample(g)
+            r, desc, cores, _ = cpu_sample(g)
             cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -468,6 +458,8 @@ def main():
                        "l2": "inputs larger than L2 (weights/activations stream through HBM every step)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 4 * n_seq * (g.seq_len + 1),
                     "d2h_bytes_per_step": 4},
+            # value is the whole-job aggregate over all peers (the bench contract); per B200 here
+            "value_per_gpu": value / world,
             "gpu_launches": st["kernel_launches"],
             "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05)", "achieved": gemm_tf,
                          "peak": peak_tf, "unit": "TFLOP/s",
@@ -478,13 +470,28 @@ def main():
                                        round(r["ms"], 2), round(r["tflops"], 1)] for r in gemm_shapes],
                          "by_shape_fields": "M N K a_mn b_mn epilogue launches ms TFLOP/s"},
             "step_roofline": {"t_roof_ms": t_roof * 1000.0, "frac": t_roof * 1000.0 / ms_step,
+                              "peak_tflops": pk["bf16_tflops"], "peak": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                              # the same step against the sustained measured peak and the datasheet
+                              "frac_vs_sustained": t_roof_at(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])) / ms_step,
+                              "frac_vs_datasheet_2250": t_roof_at(2250.0) / ms_step,
                               "flops_per_token": f_alg_per_token(g),
                               # the same bound with the host link as all ranks see it at once
                               # (link_probe: host DRAM shared by the peers of one socket)
                               "t_roof_contended_ms": 1000.0 * max(t_roof, plan.pred_d2h_B / (args.link_gbs * 1e9)),
                               "frac_contended": 1000.0 * max(t_roof, plan.pred_d2h_B / (args.link_gbs * 1e9)) / ms_step},
+            # device time per kernel category and step (CUDA events around each launch group on its
+            # stream; the side streams overlap the main one, so the sum exceeds the step)
+            "kernel_ms_per_step": {k: round(v[1] / args.steps, 2) for k, v in klog.items()},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
-            "compute_busy_pct": compute_busy_pct(trace, st["step_ms"]),
+            "swap_hidden": {"h2d_pct": 100.0 * st["h2d_hidden_ms"] / st["h2d_ms"] if st["h2d_ms"] else None,
+                            "d2h_pct": 100.0 * st["d2h_hidden_ms"] / st["d2h_ms"] if st["d2h_ms"] else None,
+                            "combined_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
+                            "h2d_ms": st["h2d_ms"], "d2h_ms": st["d2h_ms"],
+                            "of": "last timed step: copy time overlapping compute-lane FWD/BWD ops (per-op CUDA events)"},
+            "compute_busy_pct": (100.0 * st["compute_busy_ms"] / st["compute_span_ms"]) if st["compute_span_ms"] else None,
+            "hbm_arena": {"total_bytes": plan.device_bytes, "resident_submodel1_bytes": plan.r1_bytes,
+                          "slots_bytes": plan.nslot * plan.slot_bytes, "nslot": plan.nslot,
+                          "stash_bytes": plan.stash_bytes, "work_bytes": plan.work_bytes},
             "h2d_GBs": st["h2d_bytes"] / (ms / 1000.0) / 1e9, "d2h_GBs": st["d2h_bytes"] / (ms / 1000.0) / 1e9,
             # while a copy runs (planned bytes of the last step / busy time of its copy lane) vs the
             # link as every rank sees it at once (link_probe) and alone (profiles/box_probe_r01.json)

@@ -202,12 +202,22 @@ typedef struct {
   double h2d_bytes, d2h_bytes;    /* bytes copied host<->device by the swap engine                     */
   double copy_ms, copy_hidden_ms; /* summed copy time and the part overlapping compute (last step)    */
   double step_ms;                 /* device time of the last step (first op start -> last op end)     */
+  double h2d_ms, h2d_hidden_ms;   /* copy_ms / copy_hidden_ms split by direction: host -> device ...   */
+  double d2h_ms, d2h_hidden_ms;   /* ... and device -> host (last step, both)   */
+  double compute_busy_ms;         /* union of the compute lane's FWD/BWD/ADAM/... op intervals         */
+  double compute_span_ms;         /* compute lane: first op start -> last op end (last step)           */
 } atom_stats_t;
 atom_status atom_get_stats(atom_peer* peer, atom_stats_t* out);
 /* GEMM time per shape since the last reset (timing on): one line per distinct launch shape,
  *   "<M> <N> <K> <a_mn> <b_mn> <epilogue> <launches> <ms> <TFLOP/s>"
  * (ms summed over the launches' CUDA-event durations).  Same buffer rules as atom_plan_schedule. */
 atom_status atom_get_gemm_log(atom_peer* peer, char* buf, int64_t cap, int64_t* len);
+/* Device time per kernel category since the last reset (timing on): one line per category,
+ *   "<category> <launch groups> <ms>"   categories: gemm_fwd gemm_dgrad gemm_wgrad attn_fwd attn_bwd
+ *   layernorm colsum gelu cross_entropy embedding adamw cast
+ * (CUDA events around each launch group on its own stream; with the side streams on, the
+ * categories overlap in time).  Same buffer rules as atom_plan_schedule. */
+atom_status atom_get_kernel_log(atom_peer* peer, char* buf, int64_t cap, int64_t* len);
 /* Reset counters; timing != 0 brackets every GEMM launch with CUDA events (GEMM-time roofline). */
 atom_status atom_reset_stats(atom_peer* peer, int32_t timing);
 

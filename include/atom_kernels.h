@@ -62,6 +62,12 @@ int atom_k_dropout(int dtype, const void* x, void* y, long n, double p, unsigned
 /* Number of kernels libatom launched in this process. */
 unsigned long long atom_k_launch_count(void);
 
+/* Launches per kernel family since the library was loaded, as text: one "<family> <count>" line
+ * per family (e.g. "gemm_tc2<0,1> 12", "attn_fwd2<80> 4"), written NUL-terminated into the
+ * caller-owned buf of cap bytes; *len = text length.  ATOM_E_INVALID if cap <= *len (nothing
+ * written; call again with a larger buffer).  Tests use it to prove which kernels a step ran. */
+int atom_k_launch_log(char* buf, int64_t cap, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,12 +36,13 @@ def lr_at(h: AdamWHyper, t: int) -> float:
     return h.lr * min(1.0, t / h.warmup_steps)
 
 
-def adamw_step(h: AdamWHyper, t: int, p, g, m, v):
-    """One AdamW update at step t (1-based).  Returns new (p, m, v) (fp64)."""
-    p = np.asarray(p, dtype=np.float64)
-    g = np.asarray(g, dtype=np.float64)
-    m = np.asarray(m, dtype=np.float64)
-    v = np.asarray(v, dtype=np.float64)
+def adamw_step(h: AdamWHyper, t: int, p, g, m, v, dtype=np.float64):
+    """One AdamW update at step t (1-based).  Returns new (p, m, v) (fp64; dtype=np.float32 only
+    for timing the oracle as the CPU baseline)."""
+    p = np.asarray(p, dtype=dtype)
+    g = np.asarray(g, dtype=dtype)
+    m = np.asarray(m, dtype=dtype)
+    v = np.asarray(v, dtype=dtype)
     lr_t = lr_at(h, t)
     p = p * (1.0 - lr_t * h.weight_decay)
     m = h.beta1 * m + (1.0 - h.beta1) * g

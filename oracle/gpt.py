@@ -62,9 +62,10 @@ def shapes(cfg):
     return out
 
 
-def unflatten(cfg, flat):
-    """flat vector -> {"E": {...}, "B": [{...}], "H": {...}} (views into a fp64 copy)."""
-    flat = np.asarray(flat, dtype=np.float64)
+def unflatten(cfg, flat, dtype=np.float64):
+    """flat vector -> {"E": {...}, "B": [{...}], "H": {...}} (views into a copy of dtype: fp64 for
+    parity; fp32 only for bench.py's cpu_baseline timing)."""
+    flat = np.asarray(flat, dtype=dtype)
     p = {"E": {}, "B": [dict() for _ in range(cfg.n_layer)], "H": {}}
     off = 0
     for node, name, shp in shapes(cfg):
@@ -286,9 +287,10 @@ def backward(cfg, p, cache):
     return {"E": {"wte": dwte, "wpe": dwpe}, "B": gB, "H": gH}
 
 
-def loss_and_grad(cfg, flat_params, tokens, drop=None):
-    """Flat-vector convenience wrapper: (loss, flat_grad) in fp64."""
-    p = unflatten(cfg, flat_params)
+def loss_and_grad(cfg, flat_params, tokens, drop=None, dtype=np.float64):
+    """Flat-vector convenience wrapper: (loss, flat_grad) in fp64 (dtype=np.float32: the same
+    arithmetic in fp32, used only to time the oracle as the CPU baseline)."""
+    p = unflatten(cfg, flat_params, dtype)
     loss, _, cache = forward(cfg, p, np.asarray(tokens), drop=drop)
     g = backward(cfg, p, cache)
     return loss, flatten(cfg, g)

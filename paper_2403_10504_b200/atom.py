@@ -82,6 +82,23 @@ def launch_count():
     return int(lib.atom_k_launch_count())
 
 
+lib.atom_k_launch_log.restype = C.c_int
+lib.atom_k_launch_log.argtypes = [C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+
+
+def launch_log() -> dict:
+    """{kernel family: launches since load} (atom_k_launch_log)."""
+    n = C.c_int64(0)
+    lib.atom_k_launch_log(None, 0, C.byref(n))
+    buf = C.create_string_buffer(int(n.value) + 1)
+    check(lib.atom_k_launch_log(buf, n.value + 1, C.byref(n)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        k, v = line.rsplit(" ", 1)
+        out[k] = int(v)
+    return out
+
+
 # ---------------------------------------------------------------- training ABI
 class ModelCfg(C.Structure):
     _fields_ = [("n_layer", C.c_int32), ("d_model", C.c_int32), ("n_head", C.c_int32), ("seq_len", C.c_int32),
@@ -161,7 +178,9 @@ class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("gemm_launches", C.c_int64),
                 ("gemm_ms", C.c_double), ("gemm_flops", C.c_double), ("h2d_bytes", C.c_double),
                 ("d2h_bytes", C.c_double), ("copy_ms", C.c_double), ("copy_hidden_ms", C.c_double),
-                ("step_ms", C.c_double)]
+                ("step_ms", C.c_double), ("h2d_ms", C.c_double), ("h2d_hidden_ms", C.c_double),
+                ("d2h_ms", C.c_double), ("d2h_hidden_ms", C.c_double), ("compute_busy_ms", C.c_double),
+                ("compute_span_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -185,6 +204,8 @@ lib.atom_get_trace.restype = C.c_int
 lib.atom_get_trace.argtypes = [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
 lib.atom_get_gemm_log.restype = C.c_int
 lib.atom_get_gemm_log.argtypes = [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+lib.atom_get_kernel_log.restype = C.c_int
+lib.atom_get_kernel_log.argtypes = [_P, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
 lib.atom_get_stats.restype = C.c_int
 lib.atom_get_stats.argtypes = [_P, C.POINTER(Stats)]
 lib.atom_reset_stats.restype = C.c_int
@@ -261,6 +282,18 @@ class Peer:
         buf = C.create_string_buffer(n.value + 1)
         check(lib.atom_get_trace(self.h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
+
+    def kernel_log(self) -> dict:
+        """Per kernel category since the last reset_stats(timing=True): {category: (groups, ms)}."""
+        n = C.c_int64(0)
+        lib.atom_get_kernel_log(self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib.atom_get_kernel_log(self.h, buf, n.value + 1, C.byref(n)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            k, cnt, ms = line.split()
+            out[k] = (int(cnt), float(ms))
+        return out
 
     def gemm_log(self) -> list:
         """Per-shape GEMM timing since the last reset_stats(timing=True): dicts with M, N, K,

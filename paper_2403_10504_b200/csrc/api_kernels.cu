@@ -66,6 +66,17 @@ int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const v
 
 unsigned long long atom_k_launch_count(void) { return g_launch_count; }
 
+int atom_k_launch_log(char* buf, int64_t cap, int64_t* len) {
+  const std::string t = launch_log_text();
+  if (len) *len = (int64_t)t.size();
+  if (!buf || cap <= (int64_t)t.size()) {
+    set_error("atom_k_launch_log: buffer of %lld bytes, need %zu", (long long)cap, t.size() + 1);
+    return ATOM_E_INVALID;
+  }
+  memcpy(buf, t.c_str(), t.size() + 1);
+  return ATOM_OK;
+}
+
 int atom_k_cpu_adamw(float* p, const float* g, float* m, float* v, long n, float lr_t, float b1, float b2, float eps,
                      float wd, long t, float gscale, int threads) {
   if (!p || !g || !m || !v || n < 0 || t < 1) {

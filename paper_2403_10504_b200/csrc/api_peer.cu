@@ -8,14 +8,15 @@
 namespace atom {
 bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const void* nccl_id);
 bool peer_step(atom_peer* p, const int32_t* tokens, bool on_device, float* loss);
-bool peer_flush_average(atom_peer* p);
+bool peers_flush_average(atom_peer* const* ps, int n);
 bool peer_broadcast_state(atom_peer* p, int root, bool adopt);
 bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank);
 bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abort_ops);
 bool peer_get_params(atom_peer* p, float* master, float* m, float* v);
-bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms);
+bool peer_trace(atom_peer* p, std::string* out, atom_stats_t* st);
 bool peer_stats(atom_peer* p, atom_stats_t* s);
 bool peer_gemm_log(atom_peer* p, std::string* out);
+bool peer_kernel_log(atom_peer* p, std::string* out);
 void peer_reset_stats(atom_peer* p, int timing);
 void peer_free(atom_peer* p);
 bool peer_stream_sync(atom_peer* p);
@@ -156,13 +157,16 @@ atom_status atom_sync(atom_peer* const* peers, int32_t n_local, int32_t flush) {
     for (int i = 0; i < n_local; ++i) peers[i]->sync_next = true;
     return ATOM_OK;
   }
-  if (n_local > 1) ncclGroupStart();
-  for (int i = 0; i < n_local; ++i)
-    if (!peer_flush_average(peers[i])) {
-      if (n_local > 1) ncclGroupEnd();
-      return fail(peers[i], cuda_or_nccl());
+  for (int i = 1; i < n_local; ++i)
+    if (peers[i]->S != peers[0]->S || peers[i]->seg_P != peers[0]->seg_P || (peers[0]->nranks > 1 && peers[i]->comm == peers[0]->comm)) {
+      set_error("atom_sync: local peers need the same plan and their own communicator ranks");
+      return ATOM_E_INVALID;
     }
-  if (n_local > 1) ncclGroupEnd();
+  if (!peers_flush_average(peers, n_local)) {
+    const atom_status st = cuda_or_nccl();
+    for (int i = 0; i < n_local; ++i) fail(peers[i], st);
+    return st;
+  }
   return ATOM_OK;
 }
 
@@ -219,8 +223,7 @@ atom_status atom_get_params(atom_peer* p, float* master, float* m, float* v) {
 atom_status atom_get_trace(atom_peer* p, char* buf, int64_t cap, int64_t* len) {
   if (!p) { set_error("atom_get_trace: NULL peer"); return ATOM_E_INVALID; }
   std::string s;
-  double a, b, c;
-  if (!peer_trace(p, &s, &a, &b, &c)) return fail(p, ATOM_E_CUDA);
+  if (!peer_trace(p, &s, nullptr)) return fail(p, ATOM_E_CUDA);
   if (len) *len = (int64_t)s.size();
   if (!buf || cap < (int64_t)s.size() + 1) {
     set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);
@@ -235,6 +238,20 @@ atom_status atom_get_gemm_log(atom_peer* p, char* buf, int64_t cap, int64_t* len
   if (!p) { set_error("atom_get_gemm_log: NULL peer"); return ATOM_E_INVALID; }
   std::string s;
   if (!peer_gemm_log(p, &s)) return fail(p, ATOM_E_CUDA);
+  if (len) *len = (int64_t)s.size();
+  if (!buf || cap < (int64_t)s.size() + 1) {
+    set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);
+    return ATOM_E_INVALID;
+  }
+  memcpy(buf, s.data(), s.size());
+  buf[s.size()] = 0;
+  return ATOM_OK;
+}
+
+atom_status atom_get_kernel_log(atom_peer* p, char* buf, int64_t cap, int64_t* len) {
+  if (!p) { set_error("atom_get_kernel_log: NULL peer"); return ATOM_E_INVALID; }
+  std::string s;
+  if (!peer_kernel_log(p, &s)) return fail(p, ATOM_E_CUDA);
   if (len) *len = (int64_t)s.size();
   if (!buf || cap < (int64_t)s.size() + 1) {
     set_error("buffer too small: need %lld bytes", (long long)s.size() + 1);

@@ -12,6 +12,7 @@
 // the MMA as an MN-major B operand (features contiguous), so no transpose is materialised.
 // Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
 #include <cuda.h>
+#include <string>
 #include <stdlib.h>
 #include <type_traits>
 
@@ -1761,7 +1762,8 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
     if (tsa) attn_fwd2_tc_kernel<DH, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
     else attn_fwd2_tc_kernel<DH, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
   }
-  count_launch();
+  static const std::string name = std::string(v1 ? "attn_fwd_v1<" : "attn_fwd2<") + std::to_string(DH) + ">";
+  count_launch(name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }
@@ -1844,7 +1846,8 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     else
       attn_bwd_dkv2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
                                                                          T_, h);
-    count_launch();
+    static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
+    count_launch(nkv.c_str());
     if (tsa_q)
       attn_bwd_dq2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
                                                                        dqkv, T_, h);
@@ -1856,7 +1859,8 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
       ATOM_CUDA_OK(cudaEventRecord(ev_join, st2));
       ATOM_CUDA_OK(cudaStreamWaitEvent(st, ev_join, 0));
     }
-    count_launch();
+    static const std::string nq = "attn_bwd_dq2<" + std::to_string(DH) + ">";
+    count_launch(nq.c_str());
   }
   ATOM_CUDA_OK(cudaGetLastError());
   return true;

@@ -63,7 +63,12 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // kernel-launch accounting (how many of our kernels ran; bench "gpu_launches")
 extern unsigned long long g_launch_count;
-inline void count_launch() { ++g_launch_count; }
+void count_launch_named(const char* name);
+// name: the kernel family (and template width) for the launch log (atom_k_launch_log)
+inline void count_launch(const char* name = "other") {
+  ++g_launch_count;
+  count_launch_named(name);
+}
 
 }  // namespace atom
 

@@ -4,6 +4,8 @@
 //   deterministic backward, GELU re-application, fused AdamW, casts, parameter init, loss sum.
 // Every reduction has a fixed order (no floating-point atomics): swapped and resident runs are
 // bit-identical (north star).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "planner.h"
@@ -375,6 +377,100 @@ __global__ void __launch_bounds__(256) ce_kernel(T* __restrict__ logits, long ld
   }
 }
 
+// bf16 cross-entropy, one HBM read and one write of the logits row: the row (V bf16, padded to
+// 16 bytes) arrives in shared memory by one TMA bulk copy; three passes over shared memory (max,
+// sum of exp, output) with 16-byte vectors; two CTAs per SM, so one CTA's copy overlaps the other's
+// passes.  Same arithmetic as ce_kernel: fixed-order reductions (thread, warp, then warps in order).
+constexpr int CE_THREADS = 256;
+__device__ __forceinline__ float ce_block_reduce(float v, float* sh, bool is_max) {
+  v = is_max ? warp_max(v) : warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = sh[0];
+#pragma unroll
+  for (int i = 1; i < CE_THREADS / 32; ++i) t = is_max ? fmaxf(t, sh[i]) : t + sh[i];
+  return t;
+}
+__global__ void __launch_bounds__(CE_THREADS, 2) ce_bf16_kernel(bf16* __restrict__ logits, long ld, int V,
+                                                                const int32_t* __restrict__ targets, long tstride,
+                                                                int T_, float scale, float* __restrict__ loss) {
+  extern __shared__ __align__(16) uint8_t ce_smem[];
+  __shared__ float sh[CE_THREADS / 32];
+  __shared__ __align__(8) uint64_t bar;
+  const long row = blockIdx.x;
+  bf16* z = logits + row * ld;
+  const int nv = (V + 7) / 8;                       // 16-byte vectors (the last one partly padding)
+  const uint32_t bytes = (uint32_t)nv * 16;
+  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(&bar);
+  const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(ce_smem);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sdst),
+                 "l"(z), "r"(bytes), "r"(sbar)
+                 : "memory");
+  }
+  const long b = row / T_, t = row - b * T_;
+  const int y = targets[b * tstride + t];
+  {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                   : "=r"(done)
+                   : "r"(sbar)
+                   : "memory");
+  }
+  const uint4* sv = (const uint4*)ce_smem;
+  auto vals = [&](int i, float* f) {
+    const uint4 u = sv[i];
+    const bf16* e = (const bf16*)&u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = (8 * i + k < V) ? __bfloat162float(e[k]) : -INFINITY;
+  };
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < nv; i += CE_THREADS) {
+    float f[8];
+    vals(i, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, f[k]);
+  }
+  const float gm = ce_block_reduce(mx, sh, true);
+  float se = 0.f;
+  for (int i = threadIdx.x; i < nv; i += CE_THREADS) {
+    float f[8];
+    vals(i, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) se += __expf(f[k] - gm);
+  }
+  const float tot = ce_block_reduce(se, sh, false);
+  const float zy = __bfloat162float(((const bf16*)ce_smem)[y]);
+  if (threadIdx.x == 0) loss[row] = gm + logf(tot) - zy;
+  const float inv = 1.f / tot;
+  for (int i = threadIdx.x; i < nv; i += CE_THREADS) {
+    float f[8];
+    vals(i, f);
+    uint4 o;
+    bf16* e = (bf16*)&o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float p = __expf(f[k] - gm) * inv;
+      if (8 * i + k == y) p -= 1.f;
+      e[k] = __float2bfloat16_rn(p * scale);
+    }
+    if (8 * i + 8 <= V) {
+      *(uint4*)(z + 8 * i) = o;
+    } else {
+      for (int k = 0; 8 * i + k < V; ++k) z[8 * i + k] = e[k];
+    }
+  }
+}
+
 // h0[row] = wte[x] + wpe[t]   (P:295, P:307 embedding in sub-model 1)
 template <typename T>
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, long tstride, int T_, const T* __restrict__ wte,
@@ -584,7 +680,7 @@ static int cs_ranges(long rows, int col_blocks) {
 
 #define LAUNCH_OK()                      \
   do {                                   \
-    count_launch();                      \
+    count_launch(__func__);              \
     ATOM_CUDA_OK(cudaGetLastError());    \
   } while (0)
 
@@ -673,7 +769,17 @@ bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, i
 template <typename T>
 bool cross_entropy(T* logits, long ld, int V, const int32_t* targets, long tstride, int T_, long rows, float scale,
                    float* loss, cudaStream_t st) {
-  ce_kernel<T><<<rows, 256, 0, st>>>(logits, ld, V, targets, tstride, T_, scale, loss);
+  const size_t row_bytes = (size_t)(V + 7) / 8 * 16;
+  if (std::is_same<T, bf16>::value && ld % 8 == 0 && ((uintptr_t)logits & 15) == 0 && row_bytes <= 112 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      ATOM_CUDA_OK(cudaFuncSetAttribute(ce_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+      attr = true;
+    }
+    ce_bf16_kernel<<<rows, CE_THREADS, row_bytes, st>>>((bf16*)logits, ld, V, targets, tstride, T_, scale, loss);
+  } else {
+    ce_kernel<T><<<rows, 256, 0, st>>>(logits, ld, V, targets, tstride, T_, scale, loss);
+  }
   LAUNCH_OK();
   return true;
 }

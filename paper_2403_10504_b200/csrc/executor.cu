@@ -20,6 +20,7 @@ using namespace atom;
 namespace atom {
 extern unsigned long long g_launch_count;
 bool peer_flush_average(atom_peer* p);
+bool peers_flush_average(atom_peer* const* ps, int n);
 }
 
 #define PEER_CUDA(expr)                                                                                      \
@@ -130,6 +131,38 @@ Scratch scratch_view(const atom_peer* p) {
   return s;
 }
 
+// ------------------------------------------------------------------ per-category kernel timing
+// (timing on: CUDA events around each launch group on its stream; atom_get_kernel_log)
+enum KCat { KC_GEMM_F, KC_GEMM_D, KC_GEMM_W, KC_ATTN_F, KC_ATTN_B, KC_LN, KC_COLSUM, KC_GELU, KC_CE, KC_EMBED,
+            KC_ADAM, KC_CAST, KC_N };
+const char* kcat_name(int c) {
+  static const char* n[KC_N] = {"gemm_fwd", "gemm_dgrad", "gemm_wgrad", "attn_fwd", "attn_bwd", "layernorm",
+                                "colsum", "gelu", "cross_entropy", "embedding", "adamw", "cast"};
+  return c >= 0 && c < KC_N ? n[c] : "?";
+}
+bool kt_mark(atom_peer* p, int cat, cudaStream_t st, bool end) {
+  if (!p->timing) return true;
+  const size_t i = end ? 2 * (p->kt_n - 1) + 1 : 2 * p->kt_n;
+  if (!end) {
+    while (p->kt_ev.size() < 2 * (p->kt_n + 1)) {
+      cudaEvent_t ev;
+      PEER_CUDA(cudaEventCreate(&ev));
+      p->kt_ev.push_back(ev);
+    }
+    if (p->kt_cat.size() < p->kt_n + 1) p->kt_cat.resize(p->kt_n + 1);
+    p->kt_cat[p->kt_n] = cat;
+    p->kt_n++;
+  }
+  PEER_CUDA(cudaEventRecord(p->kt_ev[i], st ? st : p->s_comp));
+  return true;
+}
+#define KT(cat, st, expr)                  \
+  do {                                     \
+    PEER_OK(kt_mark(p, cat, st, false));   \
+    PEER_OK(expr);                         \
+    PEER_OK(kt_mark(p, cat, st, true));    \
+  } while (0)
+
 // ------------------------------------------------------------------ compute dispatch
 template <typename T>
 bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B, long ldb, bool b_mn,
@@ -147,11 +180,14 @@ bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, co
     PEER_CUDA(cudaEventRecord(e0, st));
   }
   bool ok;
+  const int cat = a_mn ? KC_GEMM_W : (b_mn ? KC_GEMM_D : KC_GEMM_F);
+  PEER_OK(kt_mark(p, cat, st, false));
   if constexpr (std::is_same<T, bf16>::value)
     ok = gemm_tc(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, st);
   else
     ok = gemm_simt<T>(M, N, K, A, lda, a_mn, B, ldb, b_mn, e, st);
   if (!ok) return false;
+  PEER_OK(kt_mark(p, cat, st, true));
   p->gemm_launches++;
   if (p->timing) {
     PEER_CUDA(cudaEventRecord(e1, st));
@@ -208,17 +244,17 @@ bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   StashView s = stash_view(p, l, mb);
   Scratch sc = scratch_view(p);
   T* x = (T*)s.x;
-  PEER_OK(ln_fwd<T>(x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
+  KT(KC_LN, p->s_comp, ln_fwd<T>(x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
   Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
   e.bias = w(T_BQKV);
   PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
-  PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
+  KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
   // x2 = x + o W_o^T + b_o: the GEMM stores o W_o^T + b_o (plain epilogue), LN2 adds the residual
   // (a per-row residual read in the GEMM epilogue held this K = d GEMM well below the others)
   e = epi(EPI_BIAS, s.x2, d);
   e.bias = w(T_BO);
   PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-  PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x));
+  KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x));
   e = epi(EPI_BIAS_GELU, s.u, 4 * d);
   e.bias = w(T_BFC);
   e.out2 = sc.G;
@@ -255,31 +291,31 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
     // ACT_RECOMPUTE: re-run the block forward from its input checkpoint into the shared entry
     // (same kernels and inputs as the forward: bit-identical tensors); the MLP projection's
     // output is not needed by the backward and is skipped
-    PEER_OK(ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), ln1, s.st1, M, d, p->s_comp));
+    KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), ln1, s.st1, M, d, p->s_comp));
     Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
     e.bias = w(T_BQKV);
     PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
-    PEER_OK(attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
+    KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
     e = epi(EPI_BIAS, s.x2, d);
     e.bias = w(T_BO);
     PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-    PEER_OK(ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp, (const T*)s.x));
+    KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp, (const T*)s.x));
     e = epi(EPI_BIAS_GELU, s.u, 4 * d);   // u and GELU(u) in one pass, as in the forward
     e.bias = w(T_BFC);
     e.out2 = G;
     e.ldo2 = 4 * d;
     PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)ln2, d, false, w(T_WFC), d, false, e));
   } else {
-    PEER_OK(gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
+    KT(KC_GELU, p->s_comp, gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   }
   // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
   PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
-  PEER_OK(bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
+  KT(KC_COLSUM, p->s_comp, bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
   // fc pre-activation gradient: (dy W_pr) with a plain-store epilogue, then the GELU derivative
   // and the fc bias gradient in one pass over it (the GEMM epilogue reading u per row was the
   // slow part of the fused form)
   PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
-  PEER_OK(dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
+  KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
   // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
   // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
   // LN2 output (A under stash) is rewritten by LN1's re-apply after the attention backward, which
@@ -303,32 +339,32 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   };
   // MLP fc: u = LN2(x2) W_fc^T + b_fc (under recompute LN2's output is DA, rewritten just below:
   // that gradient stays on the main stream)
-  if (!rc) PEER_OK(ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
+  if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
   if (!rc) PEER_OK(fork());
   PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d),
                   rc ? p->s_comp : sd));
   if (!rc) PEER_OK(mark(1));
   PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
-  PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
+  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
                     p->red_ticket, M, d, p->s_comp));
   // attention projection: x2 = x + o W_o^T + b_o
   PEER_OK(fork());
   PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d),
                   sd));
   PEER_OK(mark(2));
-  PEER_OK(bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
+  KT(KC_COLSUM, p->s_comp, bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, d, (const T*)sc.DX2, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
   // attention (writes G, which the fc weight gradient reads)
   if (!rc) PEER_OK(join(1));
-  PEER_OK(attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
+  KT(KC_ATTN_B, p->s_comp, attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
   // QKV: qkv = LN1(x) W_qkv^T + b_qkv
-  if (!rc) PEER_OK(ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, ln1, M, d, p->s_comp));
+  if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, ln1, M, d, p->s_comp));
   PEER_OK(fork());
   PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)ln1, d, true, epi(EPI_ACC_F32, g(T_WQKV), d), sd));
   PEER_OK(mark(3));
-  PEER_OK(bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
+  KT(KC_COLSUM, p->s_comp, bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
-  PEER_OK(ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
+  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
                     p->red, p->red_ticket, M, d, p->s_comp));
   // the side stream is in order: its last mark covers WO and WQKV (and WFC)
   PEER_OK(join(3));
@@ -346,15 +382,15 @@ bool head(atom_peer* p, int mb, const SegView& sv) {
   auto g = [&](int t) { return sv.grad + toff(p, node, t); };
   Scratch sc = scratch_view(p);
   const T* h = (const T*)hfin_ptr(p, mb);
-  PEER_OK(ln_fwd<T>(h, w(T_LNFG), w(T_LNFB), (T*)sc.z, sc.hst, M, d, p->s_comp));
+  KT(KC_LN, p->s_comp, ln_fwd<T>(h, w(T_LNFG), w(T_LNFB), (T*)sc.z, sc.hst, M, d, p->s_comp));
   PEER_OK(gemm<T>(p, M, V, d, (const T*)sc.z, d, false, w(T_WLM), d, false, epi(EPI_STORE, sc.logits, Vp)));
   const int32_t* tgt = p->tokens + (int64_t)mb * dm.b * (dm.T + 1) + 1;
-  PEER_OK(cross_entropy<T>((T*)sc.logits, Vp, V, tgt, dm.T + 1, dm.T, M, 1.f / (float)((double)p->C * M),
+  KT(KC_CE, p->s_comp, cross_entropy<T>((T*)sc.logits, Vp, V, tgt, dm.T + 1, dm.T, M, 1.f / (float)((double)p->C * M),
                            p->losses + (int64_t)mb * M, p->s_comp));
   PEER_OK(gemm<T>(p, M, d, V, (const T*)sc.logits, Vp, false, w(T_WLM), d, true, epi(EPI_STORE, sc.dz, d)));
   PEER_OK(gemm<T>(p, V, d, M, (const T*)sc.logits, Vp, true, (const T*)sc.z, d, true, epi(EPI_ACC_F32, g(T_WLM), d)));
   T* dout = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
-  PEER_OK(ln_bwd<T>((const T*)sc.dz, h, sc.hst, w(T_LNFG), nullptr, dout, g(T_LNFG), g(T_LNFB), p->red,
+  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.dz, h, sc.hst, w(T_LNFG), nullptr, dout, g(T_LNFG), g(T_LNFB), p->red,
                     p->red_ticket, M, d, p->s_comp));
   return true;
 }
@@ -376,15 +412,27 @@ bool embed_backward(atom_peer* p, int mb, const SegView& sv) {
                       sv.grad + toff(p, 0, T_WPE), p->emb, p->s_comp);
 }
 
+// deferred CAST (layer-by-layer loading): wait for node's copy, derive its compute weights
+template <typename T>
+bool cast_node(atom_peer* p, int k, int node, const SegView& sv) {
+  const int64_t off = p->dm.node_off[node] - p->seg_off[k - 1];
+  PEER_CUDA(cudaStreamWaitEvent(p->s_comp, p->node_ev[node], 0));
+  KT(KC_CAST, p->s_comp, cast_params<T>(sv.master + off, (T*)sv.W + off, p->dm.P[node], p->s_comp));
+  return true;
+}
+
 template <typename T>
 bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
   // the gradient buffer starts each step at zero; under gradient rounds (R37) only the first round
   // of an update starts at zero, later rounds continue the running sum (resident sub-model 1: kept
   // on the device; sub-models 2..S: loaded from the host sum with the master)
   if (k == p->S && mb == 0 && p->round == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  const bool cast = p->cast_pending[k - 1];
+  p->cast_pending[k - 1] = 0;
   for (int node = p->seg_lo[k - 1]; node <= p->seg_hi[k - 1]; ++node) {
+    if (cast) PEER_OK(cast_node<T>(p, k, node, sv));
     if (node == 0)
-      PEER_OK(embed_forward<T>(p, mb, sv));
+      KT(KC_EMBED, p->s_comp, embed_forward<T>(p, mb, sv));
     else if (node <= p->dm.L)
       PEER_OK(fwd_block<T>(p, node - 1, mb, sv));
     else
@@ -395,9 +443,12 @@ bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
 template <typename T>
 bool run_bwd(atom_peer* p, int k, int mb, const SegView& sv) {
   if (k < p->S && mb == 0 && p->round == 0) PEER_CUDA(cudaMemsetAsync(sv.grad, 0, 4 * p->seg_P[k - 1], p->s_comp));
+  const bool cast = p->cast_pending[k - 1];
+  p->cast_pending[k - 1] = 0;
   for (int node = p->seg_hi[k - 1]; node >= p->seg_lo[k - 1]; --node) {
+    if (cast) PEER_OK(cast_node<T>(p, k, node, sv));
     if (node == 0)
-      PEER_OK(embed_backward<T>(p, mb, sv));
+      KT(KC_EMBED, p->s_comp, embed_backward<T>(p, mb, sv));
     else if (node <= p->dm.L)
       PEER_OK(bwd_block<T>(p, node - 1, mb, sv));
     // the head's backward ran inside its forward op
@@ -431,6 +482,24 @@ bool copy_seg(atom_peer* p, int k, float* dev, float* host, bool h2d) {
   return true;
 }
 
+// a sub-model's swap-in, layer by layer: every array's node range, then the node's event (forward:
+// nodes in execution order lo..hi; backward: hi..lo, the order the backward consumes them)
+bool load_seg_nodes(atom_peer* p, int k, std::initializer_list<std::pair<float*, const float*>> arrays, bool reverse) {
+  const int lo = p->seg_lo[k - 1], hi = p->seg_hi[k - 1];
+  for (int i = 0; i <= hi - lo; ++i) {
+    const int node = reverse ? hi - i : lo + i;
+    const int64_t off = p->dm.node_off[node] - p->seg_off[k - 1];
+    const size_t bytes = 4 * (size_t)p->dm.P[node];
+    for (auto& a : arrays) {
+      PEER_CUDA(cudaMemcpyAsync(a.first + off, a.second + p->dm.node_off[node], bytes, cudaMemcpyHostToDevice,
+                                p->s_h2d));
+      p->h2d_bytes += bytes;
+    }
+    PEER_CUDA(cudaEventRecord(p->node_ev[node], p->s_h2d));
+  }
+  return true;
+}
+
 // AdamW constants of this step's update: lr warm-up on the update count t; under gradient rounds
 // (R37) the summed gradient of R rounds is scaled to their mean
 AdamConsts step_consts(const atom_peer* p) {
@@ -459,6 +528,8 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
   cudaStream_t st = lane_stream(p, o.lane);
   const bool hu = p->cfg.grad_rounds > 0;
   for (auto& w : o.waits) {
+    // a CAST's load dependency is taken per layer inside the sub-model's first FWD / BWD op
+    if (o.kind == K_CAST && (w.kind == K_LOAD_F || w.kind == K_LOAD_B)) continue;
     if (w.kind == -1) {
       auto it = p->rel_of.find(p->slot_phys[w.seg]);
       if (it != p->rel_of.end() && it->second) PEER_CUDA(cudaStreamWaitEvent(st, it->second, 0));
@@ -478,8 +549,8 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
   SegView sv = base ? seg_view(p, k, base) : SegView{};
   const int64_t P = p->seg_P[k - 1];
   switch (o.kind) {
-    case K_CAST:
-      PEER_OK(cast_params<T>(sv.master, (T*)sv.W, P, st));
+    case K_CAST:   // deferred: layer by layer inside the next FWD / BWD op (cast_node)
+      p->cast_pending[k - 1] = 1;
       break;
     case K_FWD:
       PEER_OK(run_fwd<T>(p, k, o.mb, sv));
@@ -494,7 +565,7 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
       // of an update); the others update on the CPU after their gradient sum is stored
       if (hu && (k != 1 || !p->upd_round)) break;
       T* wout = (k == 1 && !sync) ? (T*)sv.W : nullptr;
-      PEER_OK(adamw<T>(sv.master, sv.grad, sv.m, sv.v, wout, P, step_consts(p), st));
+      KT(KC_ADAM, st, adamw<T>(sv.master, sv.grad, sv.m, sv.v, wout, P, step_consts(p), st));
       break;
     }
     case K_AVG:
@@ -507,25 +578,32 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
       }
       break;
     case K_RECAST:
-      PEER_OK(cast_params<T>(sv.master, (T*)sv.W, P, st));
+      KT(KC_CAST, st, cast_params<T>(sv.master, (T*)sv.W, P, st));
       break;
     case K_LOAD_F:
-      PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
       // the interleaved last sub-model accumulates inside its forward op: its running gradient
       // sum comes with the forward load (R37)
-      if (hu && k == p->S && p->round > 0) PEER_OK(copy_seg(p, k, sv.grad, p->h_gacc, true));
+      if (hu && k == p->S && p->round > 0)
+        PEER_OK(load_seg_nodes(p, k, {{sv.master, p->h_master}, {sv.grad, p->h_gacc}}, false));
+      else
+        PEER_OK(load_seg_nodes(p, k, {{sv.master, p->h_master}}, false));
       break;
     case K_LOAD_B:
       if (hu) {
         if (k < p->S) {
-          PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
-          if (p->round > 0) PEER_OK(copy_seg(p, k, sv.grad, p->h_gacc, true));
+          if (p->round > 0)
+            PEER_OK(load_seg_nodes(p, k, {{sv.master, p->h_master}, {sv.grad, p->h_gacc}}, true));
+          else
+            PEER_OK(load_seg_nodes(p, k, {{sv.master, p->h_master}}, true));
         }
         break;
       }
-      if (!(k == p->S && p->S >= 2)) PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
-      PEER_OK(copy_seg(p, k, sv.m, p->h_m, true));
-      PEER_OK(copy_seg(p, k, sv.v, p->h_v, true));
+      if (k == p->S && p->S >= 2) {   // the last sub-model kept its master: AdamW moments only
+        PEER_OK(copy_seg(p, k, sv.m, p->h_m, true));
+        PEER_OK(copy_seg(p, k, sv.v, p->h_v, true));
+      } else {
+        PEER_OK(load_seg_nodes(p, k, {{sv.master, p->h_master}, {sv.m, p->h_m}, {sv.v, p->h_v}}, true));
+      }
       break;
     case K_STORE:
       if (hu) {
@@ -645,6 +723,9 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
     for (auto& ev : p->cpu_ev) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   for (auto& ev : p->ev_side) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  p->node_ev.assign(dm.n_nodes, nullptr);
+  for (auto& ev : p->node_ev) PEER_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  p->cast_pending.assign(p->S, 0);
   {
     const char* e = getenv("ATOM_SIDE_WGRAD");   // 0: all block-backward kernels on one stream
     p->side_wgrad = !(e && e[0] == '0');
@@ -788,35 +869,64 @@ bool peer_step(atom_peer* p, const int32_t* tokens, bool on_device, float* loss)
   return run_step<float>(p, loss);
 }
 
-// standalone averaging pass (atom_sync flush=1): H2D master -> allreduce -> D2H per segment >= 2,
-// in place for the resident segment 1 (then re-derive its compute weights)
-bool peer_flush_average(atom_peer* p) {
-  PEER_OK(peer_stream_sync(p));
-  if (p->nranks <= 1) return true;
-  uint8_t* slot = p->slot_phys.empty() ? nullptr : p->slot_phys[0];
-  for (int k = 1; k <= p->S; ++k) {
-    SegView sv = seg_view(p, k, k == 1 ? p->r1 : slot);
-    const int64_t P = p->seg_P[k - 1];
-    if (k >= 2) PEER_OK(copy_seg(p, k, sv.master, p->h_master, true));
-    PEER_CUDA(cudaStreamSynchronize(p->s_h2d));
-    ncclResult_t r = ncclAllReduce(sv.master, sv.master, (size_t)P, ncclFloat32, ncclAvg, p->comm, p->s_comm);
-    if (r != ncclSuccess) {
-      set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
-      return false;
+// standalone averaging pass (atom_sync flush=1) over the n local peers of this process (each on its
+// own device, all members of one communicator): per segment, H2D every peer's master (segments >= 2)
+// into its slot 0, ONE NCCL group with every peer's allreduce, then D2H (segments >= 2) or re-derive
+// the compute weights (the resident segment 1, averaged in place).  Segments are the outer loop: a
+// peer's slot 0 is reused by its next segment only after that segment's allreduce has completed.
+bool peers_flush_average(atom_peer* const* ps, int n) {
+  for (int i = 0; i < n; ++i) PEER_OK(peer_stream_sync(ps[i]));
+  if (ps[0]->nranks <= 1) return true;
+  auto view = [](atom_peer* p, int k) {
+    uint8_t* slot = p->slot_phys.empty() ? nullptr : p->slot_phys[0];
+    return seg_view(p, k, k == 1 ? p->r1 : slot);
+  };
+  for (int k = 1; k <= ps[0]->S; ++k) {
+    const int64_t P = ps[0]->seg_P[k - 1];
+    for (int i = 0; i < n; ++i) {
+      atom_peer* p = ps[i];
+      PEER_CUDA(cudaSetDevice(p->device));
+      if (k >= 2) PEER_OK(copy_seg(p, k, view(p, k).master, p->h_master, true));
+      PEER_CUDA(cudaStreamSynchronize(p->s_h2d));
     }
-    PEER_CUDA(cudaStreamSynchronize(p->s_comm));
-    if (k >= 2) {
-      PEER_OK(copy_seg(p, k, sv.master, p->h_master, false));
-      PEER_CUDA(cudaStreamSynchronize(p->s_d2h));
-    } else if (p->dm.dtype == ATOM_BF16) {
-      PEER_OK(cast_params<bf16>(sv.master, (bf16*)sv.W, P, p->s_comp));
-    } else {
-      PEER_OK(cast_params<float>(sv.master, (float*)sv.W, P, p->s_comp));
+    if (n > 1) ncclGroupStart();
+    for (int i = 0; i < n; ++i) {
+      atom_peer* p = ps[i];
+      ncclResult_t r = ncclAllReduce(view(p, k).master, view(p, k).master, (size_t)P, ncclFloat32, ncclAvg, p->comm,
+                                     p->s_comm);
+      if (r != ncclSuccess) {
+        if (n > 1) ncclGroupEnd();
+        set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
+        return false;
+      }
+    }
+    if (n > 1) {
+      ncclResult_t r = ncclGroupEnd();
+      if (r != ncclSuccess) {
+        set_error("ncclGroupEnd failed: %s", ncclGetErrorString(r));
+        return false;
+      }
+    }
+    for (int i = 0; i < n; ++i) {
+      atom_peer* p = ps[i];
+      PEER_CUDA(cudaSetDevice(p->device));
+      PEER_CUDA(cudaStreamSynchronize(p->s_comm));
+      SegView sv = view(p, k);
+      if (k >= 2) {
+        PEER_OK(copy_seg(p, k, sv.master, p->h_master, false));
+        PEER_CUDA(cudaStreamSynchronize(p->s_d2h));
+      } else if (p->dm.dtype == ATOM_BF16) {
+        PEER_OK(cast_params<bf16>(sv.master, (bf16*)sv.W, P, p->s_comp));
+      } else {
+        PEER_OK(cast_params<float>(sv.master, (float*)sv.W, P, p->s_comp));
+      }
     }
   }
-  PEER_OK(peer_stream_sync(p));
+  for (int i = 0; i < n; ++i) PEER_OK(peer_stream_sync(ps[i]));
   return true;
 }
+
+bool peer_flush_average(atom_peer* p) { return peers_flush_average(&p, 1); }
 
 // membership change: abort the old communicator, join a new one (P:410 peers join and leave)
 bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank) {
@@ -946,10 +1056,9 @@ bool peer_get_params(atom_peer* p, float* master, float* m, float* v) {
   return true;
 }
 
-bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms, double* hidden_ms) {
+bool peer_trace(atom_peer* p, std::string* out, atom_stats_t* st) {
   PEER_OK(peer_stream_sync(p));
   out->clear();
-  *step_ms = *copy_ms = *hidden_ms = 0;
   if (!p->have_trace) return true;
   const auto& ops = p->trace_ops;
   std::vector<float> t0(ops.size()), t1(ops.size());
@@ -960,7 +1069,8 @@ bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms
     base = std::min(base, t0[i]);
   }
   float lo = 1e30f, hi = -1e30f;
-  std::vector<std::pair<float, float>> comp, copies;
+  std::vector<std::pair<float, float>> comp, comp_all;
+  std::vector<std::pair<float, float>> copies[2];   // h2d, d2h
   char buf[256];
   for (size_t i = 0; i < ops.size(); ++i) {
     const Op& o = ops[i];
@@ -974,16 +1084,44 @@ bool peer_trace(atom_peer* p, std::string* out, double* step_ms, double* copy_ms
              a * 1000.0, b * 1000.0);
     *out += buf;
     if (o.lane == L_COMPUTE && (o.kind == K_FWD || o.kind == K_BWD)) comp.push_back({a, b});
-    if ((o.lane == L_H2D || o.lane == L_D2H) && b > a) copies.push_back({a, b});
+    if (o.lane == L_COMPUTE && b > a) comp_all.push_back({a, b});
+    if ((o.lane == L_H2D || o.lane == L_D2H) && b > a) copies[o.lane == L_D2H].push_back({a, b});
   }
-  *step_ms = hi - lo;
-  for (auto& c : copies) {
-    *copy_ms += c.second - c.first;
-    for (auto& k : comp) {
-      float x = std::max(c.first, k.first), y = std::min(c.second, k.second);
-      if (y > x) *hidden_ms += y - x;
+  if (!st) return true;
+  st->step_ms = hi - lo;
+  double* tot[2] = {&st->h2d_ms, &st->d2h_ms};
+  double* hid[2] = {&st->h2d_hidden_ms, &st->d2h_hidden_ms};
+  for (int dir = 0; dir < 2; ++dir) {
+    *tot[dir] = *hid[dir] = 0;
+    for (auto& c : copies[dir]) {
+      *tot[dir] += c.second - c.first;
+      for (auto& k : comp) {
+        float x = std::max(c.first, k.first), y = std::min(c.second, k.second);
+        if (y > x) *hid[dir] += y - x;
+      }
     }
   }
+  st->copy_ms = st->h2d_ms + st->d2h_ms;
+  st->copy_hidden_ms = st->h2d_hidden_ms + st->d2h_hidden_ms;
+  // compute lane: union of its op intervals over its span (the rest is the lane waiting on swaps)
+  std::sort(comp_all.begin(), comp_all.end());
+  double busy = 0;
+  float cs = 0, ce = -1e30f, first = 0, last = 0;
+  for (size_t i = 0; i < comp_all.size(); ++i) {
+    const auto& iv = comp_all[i];
+    if (i == 0) first = iv.first;
+    last = std::max(last, iv.second);
+    if (iv.first > ce) {
+      if (i) busy += ce - cs;
+      cs = iv.first;
+      ce = iv.second;
+    } else {
+      ce = std::max(ce, iv.second);
+    }
+  }
+  if (!comp_all.empty()) busy += ce - cs;
+  st->compute_busy_ms = busy;
+  st->compute_span_ms = comp_all.empty() ? 0 : last - first;
   return true;
 }
 
@@ -999,6 +1137,13 @@ bool peer_stats(atom_peer* p, atom_stats_t* s) {
     agg.second += ms;
   }
   p->gemm_n = 0;
+  for (size_t i = 0; i < p->kt_n; ++i) {
+    float ms;
+    PEER_CUDA(cudaEventElapsedTime(&ms, p->kt_ev[2 * i], p->kt_ev[2 * i + 1]));
+    p->kt_ms[p->kt_cat[i]] += ms;
+    p->kt_count[p->kt_cat[i]] += 1;
+  }
+  p->kt_n = 0;
   memset(s, 0, sizeof(*s));
   s->steps = p->steps;
   s->kernel_launches = (int64_t)(g_launch_count - p->launch_base);
@@ -1008,7 +1153,7 @@ bool peer_stats(atom_peer* p, atom_stats_t* s) {
   s->h2d_bytes = p->h2d_bytes;
   s->d2h_bytes = p->d2h_bytes;
   std::string tr;
-  PEER_OK(peer_trace(p, &tr, &s->step_ms, &s->copy_ms, &s->copy_hidden_ms));
+  PEER_OK(peer_trace(p, &tr, s));
   return true;
 }
 
@@ -1028,7 +1173,25 @@ bool peer_gemm_log(atom_peer* p, std::string* out) {
   return true;
 }
 
+// per category since the last reset: "category launch_groups ms" lines
+bool peer_kernel_log(atom_peer* p, std::string* out) {
+  atom_stats_t s;
+  PEER_OK(peer_stats(p, &s));
+  out->clear();
+  char buf[160];
+  for (int c = 0; c < KC_N; ++c) {
+    snprintf(buf, sizeof buf, "%s %lld %.3f\n", kcat_name(c), (long long)p->kt_count[c], p->kt_ms[c]);
+    *out += buf;
+  }
+  return true;
+}
+
 void peer_reset_stats(atom_peer* p, int timing) {
+  p->kt_n = 0;
+  for (int c = 0; c < 16; ++c) {
+    p->kt_ms[c] = 0;
+    p->kt_count[c] = 0;
+  }
   p->steps = 0;
   p->gemm_launches = 0;
   p->gemm_ms_acc = p->gemm_fl_acc = 0;
@@ -1046,11 +1209,14 @@ void peer_free(atom_peer* p) {
   if (p->comm) ncclCommDestroy(p->comm);
   for (auto ev : p->ev_side)
     if (ev) cudaEventDestroy(ev);
+  for (auto ev : p->node_ev)
+    if (ev) cudaEventDestroy(ev);
   for (auto ev : p->cpu_ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& kv : p->op_ev) cudaEventDestroy(kv.second);
   for (auto ev : p->trace_ev) cudaEventDestroy(ev);
   for (auto ev : p->gemm_ev) cudaEventDestroy(ev);
+  for (auto ev : p->kt_ev) cudaEventDestroy(ev);
   if (p->ev_loss) cudaEventDestroy(p->ev_loss);
   if (p->step_start) cudaEventDestroy(p->step_start);
   for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn, p->s_cpu})

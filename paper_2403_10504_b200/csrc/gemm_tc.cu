@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <map>
 #include <mutex>
+#include <string>
 
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -831,7 +832,9 @@ static bool launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, M, N, K, e, group_m_for(K, 1, !A_MN && B_MN));
-  count_launch();
+  static const std::string name = "gemm_tc<" + std::to_string(BN) + "," + std::to_string((int)A_MN) + "," +
+                                  std::to_string((int)B_MN) + ">";
+  count_launch(name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }
@@ -912,7 +915,8 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
     }
   }
   kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2, !A_MN && B_MN), sk);
-  count_launch();
+  static const std::string name = "gemm_tc2<" + std::to_string((int)A_MN) + "," + std::to_string((int)B_MN) + ">";
+  count_launch(name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }

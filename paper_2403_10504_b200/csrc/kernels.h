@@ -1,6 +1,7 @@
 // Internal (C++) declarations of libatom's kernel launchers.  The C-ABI lives in
 // include/atom.h (training step) and include/atom_kernels.h (per-kernel test entry points).
 #pragma once
+#include <string>
 #include "adam.h"
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -8,6 +9,7 @@
 namespace atom {
 
 const char* last_error();
+std::string launch_log_text();
 
 // GEMM: D[m,n] = sum_k A[m,k] B[n,k] + epilogue.  *_mn = operand stored MN-major ([K][ld]).
 bool gemm_tc(int M, int N, int K, const bf16* A, long lda, bool a_mn, const bf16* B, long ldb, bool b_mn,

@@ -72,6 +72,11 @@ struct atom_peer {
   cudaEvent_t ev_side[4] = {nullptr, nullptr, nullptr, nullptr};
   bool side_wgrad = true;
   std::map<std::pair<int, int>, cudaEvent_t> op_ev;  // (kind, seg) -> completion event
+  // layer-by-layer loading: every LOAD_F / LOAD_B records one event per node (layer) on the
+  // h2d stream; a sub-model's CAST is deferred into its first FWD / BWD op, which waits for each
+  // layer's event and casts that layer right before computing it
+  std::vector<cudaEvent_t> node_ev;
+  std::vector<char> cast_pending;       // per segment (index k - 1)
   cudaEvent_t ev_loss = nullptr;
 
   // ---- NCCL ----
@@ -96,6 +101,12 @@ struct atom_peer {
   std::vector<std::string> gemm_key;    // "M N K a_mn b_mn epilogue" of each timed launch
   std::map<std::string, std::pair<int64_t, double>> gemm_by_shape;   // launches, ms (since reset)
   size_t gemm_n = 0;
+  // per kernel category (timing on): CUDA events around every launch group of the compute lane
+  std::vector<cudaEvent_t> kt_ev;       // pairs
+  std::vector<int> kt_cat;
+  size_t kt_n = 0;
+  double kt_ms[16] = {0};
+  int64_t kt_count[16] = {0};
   int64_t steps = 0, gemm_launches = 0;
   unsigned long long launch_base = 0;
   double h2d_bytes = 0, d2h_bytes = 0;

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import dataclasses
 import json
+import threading
 import time
 from typing import Callable, List, Optional
 
@@ -57,6 +58,21 @@ class Decision:
         d = json.loads(s)
         d["counts"] = {int(k): v for k, v in d["counts"].items()}
         return Decision(**d)
+
+
+class _LockedStore:
+    """The store shared by the protocol thread and the heartbeat thread: one call at a time."""
+
+    def __init__(self, store):
+        self._s, self.lock = store, threading.RLock()
+
+    def __getattr__(self, name):
+        fn = getattr(self._s, name)
+
+        def call(*a, **k):
+            with self.lock:
+                return fn(*a, **k)
+        return call
 
 
 class Registry:
@@ -88,11 +104,11 @@ class Coordinator:
     def __init__(self, store, pid: int, global_batch: int, ttl: float = 10.0, poll: float = 0.005,
                  make_id: Optional[Callable[[], bytes]] = None, clock: Callable[[], float] = time.time,
                  boot_grace: Optional[float] = None):
-        self.store, self.pid, self.global_batch = store, pid, global_batch
+        self.store, self.pid, self.global_batch = _LockedStore(store), pid, global_batch
         # a member that has never heartbeated (still starting up) is declared dead only after
         # boot_grace; one whose heartbeat went stale, after ttl
         self.boot_grace = max(30.0, 4 * ttl) if boot_grace is None else boot_grace
-        self.reg = Registry(store, ttl, clock)
+        self.reg = Registry(self.store, ttl, clock)
         self.poll, self.make_id, self.clock = poll, make_id, clock
         self.members: List[int] = []
         self.epoch = 0
@@ -100,15 +116,45 @@ class Coordinator:
         self.join_seen = 0
         self.sync_step = False     # the step being run averages parameters
         self.s = -1                # last completed step
+        # heartbeats run for the peer's whole life on a background thread ("periodically"),
+        # not only between steps: a step longer than the TTL must not make a live member stale
+        self._hb_stop = threading.Event()
+        self._hb_thread: Optional[threading.Thread] = None
+
+    # ---------------------------------------------------------------- heartbeats
+    def _beat(self):
+        # (s, count) read and published under the store lock: a beat never regresses s
+        with self.store.lock:
+            self.reg.beat(self.pid, self.s, self.count)
+
+    def _start_heartbeat(self):
+        if self._hb_thread is not None:
+            return
+        self._beat()
+
+        def run():
+            while not self._hb_stop.wait(self.reg.ttl / 4):
+                self._beat()
+        self._hb_thread = threading.Thread(target=run, name=f"atom-heartbeat-{self.pid}", daemon=True)
+        self._hb_thread.start()
+
+    def stop(self):
+        """Stop heartbeating (graceful leave / shutdown)."""
+        self._hb_stop.set()
+        if self._hb_thread is not None:
+            self._hb_thread.join()
+            self._hb_thread = None
 
     # ---------------------------------------------------------------- membership bootstrap
     def start(self, members: List[int]):
         """Initial members (known to all of them, e.g. the torchrun world)."""
         self.members = sorted(members)
         self.s = -1
+        self._start_heartbeat()
 
     def join(self, timeout: float = 600.0) -> Decision:
         """Register as a joiner and wait to be admitted at some step boundary."""
+        self._start_heartbeat()
         ticket = self.store.add("join_n", 1) - 1
         self.store.set(f"join/{ticket}", str(self.pid))
         t0 = self.clock()
@@ -126,20 +172,23 @@ class Coordinator:
         """Called by every member after each step with the sequences it processed in it.
 
         Waits until every other member has published this step (ready) or gone stale (dead: no
-        heartbeat within ttl; waiting members keep their own heartbeat fresh), then the lowest
-        ready member writes the decision unless one exists already."""
-        self.s += 1
-        s = self.s
-        # a sync step closes the averaging round: its samples are in the averaged parameters
-        self.count = 0 if self.sync_step else self.count + processed
-        self.reg.beat(self.pid, s, self.count)
+        heartbeat within ttl; every live member's heartbeat thread keeps it fresh, also while it
+        is still inside a long step), then the lowest ready member writes the decision unless one
+        exists already.  Joiners are admitted from the STORED decision (read back after the
+        first-writer-wins compare_set, by every member, idempotently): a joiner never sees a
+        decision other than the canonical one, even when the leader dies right after deciding."""
+        with self.store.lock:
+            self.s += 1
+            s = self.s
+            # a sync step closes the averaging round: its samples are in the averaged parameters
+            self.count = 0 if self.sync_step else self.count + processed
+            self.reg.beat(self.pid, s, self.count)
+        if self._hb_thread is None:
+            self._start_heartbeat()
         key = f"dec/{s}"
-        t0 = last = self.clock()
+        t0 = self.clock()
         while not self.store.check([key]):
             now = self.clock()
-            if now - last > self.reg.ttl / 4:
-                self.reg.beat(self.pid, s, self.count)
-                last = now
             recs = {m: self.reg.read(m) for m in self.members if m != self.pid}
             ready, waiting = [self.pid], False
             for m, r in recs.items():
@@ -152,6 +201,8 @@ class Coordinator:
                 break
             time.sleep(self.poll)
         d = Decision.from_json(self.store.get(key).decode())
+        for j in d.joiners:
+            self.store.set(f"admit/{j}", d.to_json())
         self._adopt(d)
         return d
 
@@ -172,8 +223,6 @@ class Coordinator:
         d = Decision(s=s, epoch=self.epoch + (1 if changed else 0), prev=list(self.members), members=members,
                      dead=dead, joiners=joiners, leader=self.pid, sync=total >= self.global_batch, total=total,
                      counts=counts, nccl_id=nid, join_seen=seen)
-        for j in joiners:
-            self.store.set(f"admit/{j}", d.to_json())
         return d
 
     def _adopt(self, d: Decision):
@@ -197,4 +246,5 @@ class Coordinator:
 
     def leave(self):
         """Graceful leave: stop heartbeating; the others drop this peer after one TTL."""
+        self.stop()
         self.store.set(f"hb/{self.pid}", json.dumps({"s": self.s, "count": 0, "t": 0.0}))

@@ -132,3 +132,41 @@ def test_heartbeat_trigger_failure_and_join(VICTIM):
     last = dec[steps[-1]]
     outstanding = 0 if last["sync"] else last["total"]
     assert processed == averaged + sync_steps + lost + outstanding, (processed, averaged, sync_steps, lost, outstanding)
+
+
+def _slow_peer(pid, port, q, ttl, slow):
+    import torch.distributed as dist
+    from paper_2403_10504_b200 import elastic
+    store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=__import__("datetime").timedelta(seconds=60))
+    co = elastic.Coordinator(store, pid, 10 ** 9, ttl=ttl, boot_grace=5.0)
+    co.start([0, 1, 2])
+    decs = []
+    for s in range(3):
+        time.sleep(slow if pid == 2 else 0.01)   # peer 2's steps take 4 TTLs
+        decs.append(co.after_step(1).to_json())
+    co.stop()
+    q.put((pid, decs))
+
+
+def test_step_longer_than_ttl_keeps_the_member_alive():
+    """heartbeats were only written between steps, so a step longer than ~ttl made a
+    live member stale and the group collapsed.  The heartbeat thread keeps it fresh."""
+    import datetime
+
+    import torch.distributed as dist
+    port = _free_port()
+    server = dist.TCPStore("127.0.0.1", port, is_master=True, wait_for_workers=False,
+                           timeout=datetime.timedelta(seconds=60))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ttl = 0.5
+    procs = [ctx.Process(target=_slow_peer, args=(pid, port, q, ttl, 4 * ttl)) for pid in range(3)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=30)
+    del server
+    for pid, decs in out.items():
+        for d in map(json.loads, decs):
+            assert d["dead"] == [] and d["members"] == [0, 1, 2], (pid, d)

@@ -1,0 +1,96 @@
+"""The bench's own kernels inside an oracle-compared training step, at full 2.7B width.
+
+VERDICT r1 "Next round" item 1: every oracle-compared bf16 step used to run at tiny / mini sizes,
+where the GEMM chooser picks the 1-CTA kernel and attention runs at d_h = 16 / 64; the kernels that
+produce the bench number (the 2-CTA `gemm_tc2_kernel` with its TMA-store epilogue and K-adaptive
+raster, the tcgen05 attention at d_h = 80, the lm_head GEMMs and the cross-entropy at V = 50257)
+were compared only with torch fp32 at kernel level.
+
+Here one swapped step of GPT-3 2.7B's width -- d = 2560, 32 heads x 80, T = 2048, V = 50257 --
+with L = 2 blocks, b = 1, C = 2 micro-batches and a forced 3-sub-model partition [E B0 | B1 | H]
+(so the swap engine, the interleaved last sub-model and the C-deep boundary buffer all run) goes
+through atom_step (bf16 path) and is compared element by element with the fp64 oracle
+(oracle/gpt.py, the plain definition of SURVEY §8(c) c.3) on the same seeded tokens and init:
+
+* the loss within 5e-4 relative (the north star allows 2e-2; bf16 logits carry 2^-9 relative
+  rounding, |logit| <~ 0.1 at this init, so the CE error is ~1e-4 absolute on ~10.8);
+* the step-1 gradient g = m / (1 - beta1) of EVERY parameter, per tensor (relative L2 <= 2^-6) and
+  per element (|g - g_ref| <= 2^-2 (|g_ref| + rms of the tensor's non-zero rows)), the bf16 bounds
+  of tests/grad_check.py / DESIGN.md §3;
+* and no less accurate than PyTorch's own bf16 arithmetic on the same step (tests/torch_gpt.py,
+  bf16 on the GPU): per tensor, the CUDA path's relative L2 error <= 1.25 x PyTorch bf16's;
+* the launch log proves the bench's kernels ran: gemm_tc2 in all three operand layouts and the
+  d_h = 80 tcgen05 attention forward and backward.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from grad_check import check_bf16_gradient, gradient_errors
+from oracle import gpt as ogpt
+
+pytestmark = pytest.mark.gpu
+
+atom = pytest.importorskip("paper_2403_10504_b200.atom")
+
+WIDE = synth.GPTConfig("wide-2.7b", n_layer=2, d_model=2560, n_head=32, seq_len=2048, vocab=50257, micro_batch=1)
+C = 2
+ENDS = [1, 2, 3]
+LR, B1 = 1e-3, 0.9
+
+
+@pytest.fixture(scope="module")
+def wide_step():
+    cfg = atom.make_cfg(WIDE, dtype=atom.BF16, C_=C, overlap_check=0, forced_ends=ENDS, lr=LR, beta1=B1,
+                        warmup_steps=0)
+    plan = atom.atom_plan(cfg, 10 ** 12, 10 ** 10)
+    assert plan.ends() == ENDS
+    init = synth.init_params(WIDE, seed=1234, perturb=True)
+    toks = synth.tokens(WIDE, C * WIDE.micro_batch, synth.step_seed(0, 0))
+    peer = atom.Peer(cfg, plan, init_params=init)
+    before = atom.launch_log()
+    loss = peer.step(toks)
+    after = atom.launch_log()
+    got = peer.params()
+    peer.destroy()
+    ran = {k: after.get(k, 0) - before.get(k, 0) for k in after}
+    ref_loss, g_ref = ogpt.loss_and_grad(WIDE, init.astype(np.float64), toks)
+    # PyTorch bf16 of the same step: the yardstick of what bf16 arithmetic does to this gradient
+    import torch
+    from torch_gpt import TorchGPT
+    m = TorchGPT(WIDE, init, dtype=torch.bfloat16, device="cuda")
+    m(torch.tensor(toks, dtype=torch.long, device="cuda")).backward()
+    g_torch = torch.cat([q.grad.reshape(-1).double() for q in m.params]).cpu().numpy()
+    del m
+    torch.cuda.empty_cache()
+    return {"loss": loss, "ref_loss": ref_loss, "g": got["m"] / (1.0 - B1), "g_ref": g_ref, "g_torch": g_torch,
+            "ran": ran}
+
+
+def test_wide_step_ran_the_bench_kernels(wide_step):
+    ran = wide_step["ran"]
+    for k in ("gemm_tc2<0,0>", "gemm_tc2<0,1>", "gemm_tc2<1,1>", "attn_fwd2<80>", "attn_bwd_dkv2<80>",
+              "attn_bwd_dq2<80>"):
+        assert ran.get(k, 0) > 0, (k, ran)
+    assert not any(k.startswith(("gemm_tc<", "gemm_simt", "attn_fwd_v1")) for k, v in ran.items() if v), ran
+
+
+def test_wide_step_loss_matches_oracle(wide_step):
+    loss, ref = wide_step["loss"], wide_step["ref_loss"]
+    assert abs(loss - ref) <= 5e-4 * abs(ref), (loss, ref)
+
+
+def test_wide_step_gradient_elementwise(wide_step):
+    errs = check_bf16_gradient(wide_step["g"], wide_step["g_ref"], WIDE)
+    if os.environ.get("ATOM_PRINT_GRAD_ERRS"):
+        for k, v in sorted(errs.items(), key=lambda kv: -kv[1][0]):
+            print(f"grad err {k}: elem {v[0]:.3e} relL2 {v[1]:.3e}")
+
+
+def test_wide_step_gradient_as_accurate_as_torch_bf16(wide_step):
+    ours = gradient_errors(wide_step["g"], wide_step["g_ref"], WIDE)
+    torch_bf16 = gradient_errors(wide_step["g_torch"], wide_step["g_ref"], WIDE)
+    for k in ours:
+        assert ours[k][1] <= 1.25 * torch_bf16[k][1], (k, ours[k], torch_bf16[k])

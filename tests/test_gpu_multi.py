@@ -89,3 +89,47 @@ def test_two_peer_averaging_matches_oracle(mode):
             assert abs(out[r][1][s] - losses[s][r]) <= 1e-4 * abs(losses[s][r])
     assert np.array_equal(out[0][2]["master"], out[1][2]["master"])     # replicas identical after averaging
     assert not np.array_equal(out[0][2]["m"], out[1][2]["m"])
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+def test_two_local_peers_one_process_flush_matches_oracle():
+    """atom_sync with n_local = 2 (both ranks' peers in one process, one NCCL group per segment):
+    the masters of EVERY sub-model become the oracle's mean (sub-models 2..S used to
+    keep their un-averaged values)."""
+    import threading
+
+    import synth
+    from oracle import adamw, peers
+    from paper_2403_10504_b200 import atom
+    g = synth.CONFIGS["tiny"]
+    C = 2
+    cfg = atom.make_cfg(g, dtype=atom.FP32, C_=C, overlap_check=0, forced_ends=[2, 3, 5], lr=1e-3,
+                        warmup_steps=0, sync_every=0)
+    plan = atom.atom_plan(cfg, 10 ** 11, 10 ** 10)
+    assert plan.n_seg == 3
+    nid = atom.atom_nccl_unique_id()
+    init = synth.init_params(g, seed=1234, perturb=True)
+    out = [None, None]
+
+    def make(r):   # ncclCommInitRank blocks until both ranks joined: one thread per local peer
+        out[r] = atom.Peer(cfg, plan, device=r, init_params=init, nccl_id=nid, nranks=2, rank=r)
+
+    th = [threading.Thread(target=make, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert all(p is not None for p in out)
+    toks = [[synth.tokens(g, C * g.micro_batch, synth.step_seed(r, s)) for r in range(2)] for s in range(2)]
+    for s in range(2):
+        for r in range(2):
+            out[r].step(toks[s][r])
+    atom.atom_sync(out, flush=True)
+    got = [p.params() for p in out]
+    for p in out:
+        p.destroy()
+    ref = peers.train(g, init.astype(np.float64), adamw.AdamWHyper(lr=1e-3, warmup_steps=0), toks,
+                      sync_steps={2})[0]
+    for r in range(2):
+        assert np.linalg.norm(got[r]["master"] - ref[r].p) <= 1e-4 * np.linalg.norm(ref[r].p)
+    assert np.array_equal(got[0]["master"], got[1]["master"])

@@ -12,6 +12,7 @@ from oracle import adamw as oadamw
 from oracle import gpt as ogpt
 from oracle import peers as opeers
 from oracle import schedule as osched
+from grad_check import check_bf16_gradient
 
 pytestmark = pytest.mark.gpu
 
@@ -69,10 +70,13 @@ def test_fp32_step_matches_oracle(g, ends, pol, nrc):
         rl, _ = ref.step(toks[s])
         assert abs(loss - rl) <= 1e-4 * abs(rl), (s, loss, rl)
         got = peer.params()
-        for key, want in (("master", ref.p), ("m", ref.m), ("v", ref.v)):
-            rel = per_tensor_rel(got[key], want, g)
+        # v = (1 - beta2) g^2 doubles the relative error of g: the 1e-4 bar is applied to sqrt(v),
+        # which is linear in |g| like m (R39)
+        for key, gv, want in (("master", got["master"], ref.p), ("m", got["m"], ref.m),
+                              ("sqrt(v)", np.sqrt(got["v"].astype(np.float64)), np.sqrt(ref.v))):
+            rel = per_tensor_rel(gv, want, g)
             worst = max(rel.items(), key=lambda kv: kv[1])
-            assert worst[1] <= (1e-4 if key != "v" else 2e-4), (s, key, worst)
+            assert worst[1] <= 1e-4, (s, key, worst)
     peer.destroy()
 
 
@@ -115,12 +119,13 @@ def test_bf16_step_within_north_star_tolerance(g, ends):
     rl, _ = ref.step(toks[0])
     assert abs(loss - rl) <= 2e-2 * abs(rl), (loss, rl)
     got = peer.params()
-    assert np.abs(got["master"] - ref.p).max() <= 3e-2
-    # stronger: the gradient (m = 0.1 g at step 1) per tensor within bf16 accuracy
-    rel = per_tensor_rel(got["m"], ref.m, g)
-    worst = max(rel.items(), key=lambda kv: kv[1])
-    assert worst[1] <= 0.1, worst
     peer.destroy()
+    # the north star's per-parameter bar (vacuous at step 1: |dp| ~ lr whatever the gradient) ...
+    assert np.abs(got["master"] - ref.p).max() <= 3e-2
+    # ... so the real check: the step-1 gradient g = m / (1 - beta1), element by element and per
+    # tensor, against the oracle's, within the bf16 bounds of DESIGN.md §3 (tests/grad_check.py)
+    _, g_ref = ogpt.loss_and_grad(g, init.astype(np.float64), toks[0])
+    check_bf16_gradient(got["m"] / (1.0 - HYPER.beta1), g_ref, g)
 
 
 def test_trace_follows_planned_schedule():
@@ -134,13 +139,17 @@ def test_trace_follows_planned_schedule():
     assert planned == traced
     oracle = [" ".join(l.split()[:5]) for l in osched.to_text(osched.emit(5, C)).splitlines()]
     assert planned == oracle
-    # every forward of a swapped segment starts after its load completed
+    # layer-by-layer loading: a swapped sub-model's CAST is deferred into its first FWD / BWD op,
+    # which waits for each layer's copy; so that op ends after the sub-model's load has ended
+    # (that no layer is computed before its own copy landed is what the swapped == resident
+    # bit-identity tests check: a stale layer would change the result)
     tr = [l.split() for l in peer.trace().splitlines()]
     end = {(r[1], r[2]): float(r[6]) for r in tr if r[1] in ("LOAD_F", "LOAD_B")}
-    for r in tr:
+    for i, r in enumerate(tr):
         if r[1] == "CAST":
             src = ("LOAD_F", r[2]) if ("LOAD_F", r[2]) in end else ("LOAD_B", r[2])
-            assert float(r[5]) >= end[src] - 1e-3
+            nxt = next(x for x in tr[i + 1:] if x[1] in ("FWD", "BWD") and x[2] == r[2])
+            assert float(nxt[6]) >= end[src] - 1e-3
     peer.destroy()
 
 

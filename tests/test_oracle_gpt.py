@@ -11,6 +11,8 @@ import pytest
 import torch
 import torch.nn.functional as F
 
+from torch_gpt import TorchGPT
+
 import synth
 from oracle import gpt
 
@@ -63,49 +65,6 @@ def test_finite_differences_coordinates():
             an = g[off + idx]
             assert abs(fd - an) <= 1e-6 * abs(an) + 2e-9, (name, idx, fd, an)   # 2e-9 ~ loss*eps/h
         off += n
-
-
-class TorchGPT(torch.nn.Module):
-    """An independently written minGPT-style module (torch.nn.functional ops)."""
-
-    def __init__(self, cfg, flat):
-        super().__init__()
-        self.cfg = cfg
-        t = torch.tensor(flat, dtype=torch.float64)
-        self.params = torch.nn.ParameterList()
-        self.names = []
-        off = 0
-        for node, name, shp, _ in synth.param_layout(cfg):
-            n = int(np.prod(shp))
-            self.params.append(torch.nn.Parameter(t[off:off + n].reshape(shp).clone()))
-            self.names.append((node, name))
-            off += n
-
-    def get(self, node, name):
-        return self.params[self.names.index((node, name))]
-
-    def forward(self, toks):
-        cfg = self.cfg
-        x, y = toks[:, :-1], toks[:, 1:]
-        B, T = x.shape
-        d, h = cfg.d_model, cfg.n_head
-        hcur = F.embedding(x, self.get(0, "wte")) + self.get(0, "wpe")[:T]
-        for l in range(cfg.n_layer):
-            n = l + 1
-            a = F.layer_norm(hcur, (d,), self.get(n, "ln1_g"), self.get(n, "ln1_b"), eps=1e-5)
-            qkv = F.linear(a, self.get(n, "w_qkv"), self.get(n, "b_qkv"))
-            q, k, v = qkv.split(d, dim=-1)
-            q, k, v = (t_.view(B, T, h, d // h).transpose(1, 2) for t_ in (q, k, v))
-            o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-            o = o.transpose(1, 2).reshape(B, T, d)
-            hcur = hcur + F.linear(o, self.get(n, "w_o"), self.get(n, "b_o"))
-            a2 = F.layer_norm(hcur, (d,), self.get(n, "ln2_g"), self.get(n, "ln2_b"), eps=1e-5)
-            u = F.linear(a2, self.get(n, "w_fc"), self.get(n, "b_fc"))
-            hcur = hcur + F.linear(F.gelu(u, approximate="tanh"), self.get(n, "w_pr"), self.get(n, "b_pr"))
-        L1 = cfg.n_layer + 1
-        z = F.layer_norm(hcur, (d,), self.get(L1, "lnf_g"), self.get(L1, "lnf_b"), eps=1e-5)
-        logits = F.linear(z, self.get(L1, "w_lm"))
-        return F.cross_entropy(logits.reshape(-1, cfg.vocab), y.reshape(-1))
 
 
 @pytest.mark.parametrize("cfg", [MICRO, synth.CONFIGS["tiny"]], ids=["micro", "tiny"])
@@ -199,3 +158,26 @@ def test_key_bias_gradient_is_zero():
     for blk in gp["B"]:
         assert np.abs(blk["b_qkv"][d:2 * d]).max() < 1e-14
         assert np.abs(blk["b_qkv"][:d]).max() > 1e-6 and np.abs(blk["b_qkv"][2 * d:]).max() > 1e-6
+
+
+def test_fp32_oracle_is_the_same_arithmetic():
+    """bench.py times the oracle in fp32: it must compute the same loss and
+    gradient as the fp64 parity oracle up to fp32 rounding (and really run in fp32)."""
+    import numpy as np
+
+    import synth
+    from oracle import adamw as oadamw
+    from oracle import gpt as ogpt
+    g = synth.CONFIGS["tiny"]
+    p = synth.init_params(g, seed=3, perturb=True)
+    toks = synth.tokens(g, 2, 1)
+    l64, g64 = ogpt.loss_and_grad(g, p.astype(np.float64), toks)
+    l32, g32 = ogpt.loss_and_grad(g, p, toks, dtype=np.float32)
+    assert g32.dtype == np.float32
+    assert abs(l32 - l64) <= 1e-6 * abs(l64)
+    assert np.linalg.norm(g32 - g64) <= 1e-5 * np.linalg.norm(g64)
+    h = oadamw.AdamWHyper(warmup_steps=0)
+    z = np.zeros_like(p)
+    p32 = oadamw.adamw_step(h, 1, p, g32, z, z, dtype=np.float32)[0]
+    p64 = oadamw.adamw_step(h, 1, p.astype(np.float64), g64, z, z)[0]
+    assert p32.dtype == np.float32 and np.abs(p32 - p64).max() <= 1e-6

@@ -116,3 +116,88 @@ def test_positive_idle_with_one_less_micro_batch():
     q = pl.Evaluator(c, 10 ** 12, link).make_plan(p.C - 1, p.seg_end)
     end = _compute_end(sc.emit(p.n_seg, p.C - 1), ev, q)
     assert end > (p.C - 1) * (sum(ev.k.tf) + sum(ev.k.tb))
+
+
+# ---------------------------------------------------------------------------------------------
+# Hand-computed pins for simulate() (SPEC S:233-234 build_schedule examples, "hand-built
+# 3-segment instance evaluated against an event-by-event trace").  The durations are given per
+# segment directly (no planner cost model involved), so a wrong duration lookup, a dropped wait
+# or a wrong lane in simulate() changes the exact makespan / hidden numbers below.
+class _HandEv:
+    """Segment k is node k (seg_end = [1, 2, ..., S]); s(name, k, k) = the table's value for k."""
+
+    def __init__(self, **tables):
+        self.t = tables
+
+    def segments(self, ends):
+        return [(k, k) for k in ends]
+
+    def s(self, name, i, j):
+        assert i == j
+        return self.t[name].get(i, 0)
+
+    def tbn(self, i, j):
+        return self.t["tbx"].get(i, 0)
+
+
+class _HandPlan:
+    def __init__(self, S):
+        self.seg_end = list(range(1, S + 1))
+
+
+def _busy(ev, S, C):
+    return sum(C * ev.s("tf", k, k) for k in range(1, S + 1)) + C * ev.s("tb", S, S) + \
+        sum(C * ev.tbn(k, k) for k in range(1, S))
+
+
+def test_simulate_two_segments_overlap_with_equality_has_zero_idle():
+    """C t_fwd(seg 1) = t_load(seg 2) -> idle 0, the transfer lane busy during the exec."""
+    ev = _HandEv(tf={1: 10, 2: 5}, tbx={1: 20}, tb={2: 10}, tlf={2: 20}, tmv={2: 8}, ts={2: 12})
+    sim = sc.simulate(sc.emit(2, 2), ev, _HandPlan(2))
+    # trace: FWD1 [0,10] [10,20] | LOAD_F2 [0,20] | CAST2 20 | FWD2 [20,25] | LOAD_B2 (m,v) [20,28]
+    # BWD2 [25,35] | FWD2 [35,40] | BWD2 [40,50] | ADAM2 50 | STORE2 [50,62] | BWD1 [50,70] [70,90]
+    assert sim["makespan"] == 90 == _busy(ev, 2, 2)
+    assert sim["copy_ns"] == 20 + 8 + 12
+    assert sim["hidden_ns"] == 40 and sim["hidden_ppm"] == 1_000_000
+
+
+def test_simulate_one_less_micro_batch_idles_by_the_shortfall():
+    """the same instance with C - 1 = 1: idle = sum of (load - compute) shortfalls = 20 - 10."""
+    ev = _HandEv(tf={1: 10, 2: 5}, tbx={1: 20}, tb={2: 10}, tlf={2: 20}, tmv={2: 8}, ts={2: 12})
+    sim = sc.simulate(sc.emit(2, 1), ev, _HandPlan(2))
+    # FWD1 [0,10] | LOAD_F2 [0,20] | CAST2 waits -> 20 | FWD2 [20,25] | LOAD_B2 [20,28] | BWD2 [25,35]
+    # ADAM2 35 | STORE2 [35,47] | BWD1 [35,55]
+    assert _busy(ev, 2, 1) == 45
+    assert sim["makespan"] == 55 == 45 + (20 - 10)
+    # hidden: LOAD_F2 10 (FWD1), LOAD_B2 5 + 3 (FWD2, BWD2), STORE2 12 (BWD1) of 40 copied
+    assert sim["copy_ns"] == 40 and sim["hidden_ns"] == 30
+    assert sim["hidden_ppm"] == 750_000
+
+
+def test_simulate_three_segment_event_by_event_trace():
+    """hand-built 3-segment instance (C = 2) against the trace written out below."""
+    ev = _HandEv(tf={1: 10, 2: 6, 3: 4}, tbx={1: 20, 2: 12}, tb={3: 8}, tlf={2: 14, 3: 9},
+                 tlb={2: 30}, tmv={3: 5}, ts={2: 16, 3: 11})
+    ops = sc.emit(3, 2)
+    kinds = [(ln, kind, k, mb) for ln, kind, k, mb, _, _ in ops]
+    assert kinds == [
+        ("compute", "FWD", 1, 0), ("h2d", "LOAD_F", 2, None), ("compute", "FWD", 1, 1),
+        ("compute", "CAST", 2, None), ("compute", "FWD", 2, 0), ("h2d", "LOAD_F", 3, None),
+        ("compute", "FWD", 2, 1), ("compute", "FREE", 2, None), ("compute", "CAST", 3, None),
+        ("compute", "FWD", 3, 0), ("h2d", "LOAD_B", 3, None), ("h2d", "LOAD_B", 2, None),
+        ("compute", "BWD", 3, 0), ("compute", "FWD", 3, 1), ("compute", "BWD", 3, 1),
+        ("compute", "ADAM", 3, None), ("d2h", "STORE", 3, None), ("compute", "CAST", 2, None),
+        ("compute", "BWD", 2, 0), ("compute", "BWD", 2, 1), ("compute", "ADAM", 2, None),
+        ("d2h", "STORE", 2, None), ("compute", "BWD", 1, 0), ("compute", "BWD", 1, 1),
+        ("compute", "ADAM", 1, None)]
+    sim = sc.simulate(ops, ev, _HandPlan(3))
+    # compute: FWD1 [0,10] [10,20]; FWD2 [20,26] [26,32]; FWD3 [32,36]; BWD3 [36,44]; FWD3 [44,48];
+    #          BWD3 [48,56]; CAST2 waits LOAD_B2 (58): idle 2; BWD2 [58,70] [70,82]; BWD1 [82,102] [102,122]
+    # h2d:     LOAD_F2 [0,14]; LOAD_F3 [14,23]; LOAD_B3 (m,v) [23,28]; LOAD_B2 [28,58]
+    # d2h:     STORE3 [56,67]; STORE2 [82,98]
+    assert _busy(ev, 3, 2) == 120
+    assert sim["makespan"] == 122
+    assert sim["copy_ns"] == 14 + 9 + 5 + 30 + 11 + 16
+    # hidden: 14 + (6 + 3) + (3 + 2) + (4 + 4 + 8 + 4 + 8) + 9 + 16
+    assert sim["hidden_ns"] == 81
+    assert sim["hidden_ppm"] == 81_000_000 // 85
