@@ -206,6 +206,7 @@ typedef struct {
   double d2h_ms, d2h_hidden_ms;   /* ... and device -> host (last step, both)   */
   double compute_busy_ms;         /* union of the compute lane's FWD/BWD/ADAM/... op intervals         */
   double compute_span_ms;         /* compute lane: first op start -> last op end (last step)           */
+  double host_issue_ms;           /* host wall time atom_step spent issuing the last step's work       */
 } atom_stats_t;
 atom_status atom_get_stats(atom_peer* peer, atom_stats_t* out);
 /* GEMM time per shape since the last reset (timing on): one line per distinct launch shape,
@@ -215,10 +216,30 @@ atom_status atom_get_gemm_log(atom_peer* peer, char* buf, int64_t cap, int64_t* 
 /* Device time per kernel category since the last reset (timing on): one line per category,
  *   "<category> <launch groups> <ms>"   categories: gemm_fwd gemm_dgrad gemm_wgrad attn_fwd attn_bwd
  *   layernorm colsum gelu cross_entropy embedding adamw cast
- * (CUDA events around each launch group on its own stream; with the side streams on, the
- * categories overlap in time).  Same buffer rules as atom_plan_schedule. */
+ * (timing level 2: CUDA events around each launch group on its own stream; with the side streams
+ * on, the categories overlap in time).  Same buffer rules as atom_plan_schedule. */
 atom_status atom_get_kernel_log(atom_peer* peer, char* buf, int64_t cap, int64_t* len);
-/* Reset counters; timing != 0 brackets every GEMM launch with CUDA events (GEMM-time roofline). */
+/* Measured profile ("profiled offline", "determine C offline via profiling"; DESIGN.md
+ * R34): what the planner needs, derived from the per-op trace of the peer's last step.
+ *   flops_per_s      FLOPs the step executes (model + re-forward) / compute-lane busy time
+ *   h2d / d2h        planned bytes per direction / summed op time of that copy lane
+ *   cost_table       per node {t_f_ns, t_b_ns} for one micro-batch, the atom_model_cfg.cost_table
+ *                    layout (nodes E, B_0..B_{L-1}, H): blocks from the blocks-only sub-models,
+ *                    E / H from the rest of the first / last sub-model; have_table = 0 when the plan
+ *                    has no blocks-only sub-model (then only the rates are measured).
+ * cost_table: caller-owned int64 [cap >= 2 (L + 2)] or NULL.  ATOM_E_INVALID on a malformed trace or
+ * a short buffer. */
+typedef struct {
+  double flops_per_s, h2d_bytes_per_s, d2h_bytes_per_s;
+  double compute_busy_ms, executed_flops;
+  int32_t n_nodes, have_table;
+} atom_profile_t;
+atom_status atom_profile(atom_peer* peer, int64_t* cost_table, int64_t cap, atom_profile_t* out);
+/* The same derivation from trace text in atom_get_trace's format and the plan it ran (pure host). */
+atom_status atom_profile_trace(const char* trace, const atom_model_cfg* cfg, const atom_plan_t* plan,
+                               int64_t* cost_table, int64_t cap, atom_profile_t* out);
+/* Reset counters; timing >= 1 brackets every GEMM launch with CUDA events (GEMM-time roofline),
+ * timing >= 2 also every other launch group (atom_get_kernel_log). */
 atom_status atom_reset_stats(atom_peer* peer, int32_t timing);
 
 /* Wait for all outstanding device work of the peer, release everything it owns. */

@@ -166,6 +166,34 @@ def atom_plan(cfg: ModelCfg, hbm_budget: int, link_bw: int) -> Plan:
     return p
 
 
+class Profile(C.Structure):
+    _fields_ = [("flops_per_s", C.c_double), ("h2d_bytes_per_s", C.c_double), ("d2h_bytes_per_s", C.c_double),
+                ("compute_busy_ms", C.c_double), ("executed_flops", C.c_double), ("n_nodes", C.c_int32),
+                ("have_table", C.c_int32)]
+
+
+lib.atom_profile.restype = C.c_int
+lib.atom_profile.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.POINTER(Profile)]
+lib.atom_profile_trace.restype = C.c_int
+lib.atom_profile_trace.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_int64,
+                                   C.POINTER(Profile)]
+
+
+def _profile_dict(pr, table):
+    return {"flops": pr.flops_per_s, "h2d": pr.h2d_bytes_per_s, "d2h": pr.d2h_bytes_per_s,
+            "compute_busy_ms": pr.compute_busy_ms, "executed_flops": pr.executed_flops,
+            "cost_table": [int(x) for x in table] if pr.have_table else []}
+
+
+def atom_profile_trace(trace: str, cfg: ModelCfg, plan: Plan) -> dict:
+    """atom_profile_trace: the measured profile (rates, per-node cost table) of a traced step."""
+    n = 2 * (cfg.n_layer + 2)
+    table = (C.c_int64 * n)()
+    pr = Profile()
+    check(lib.atom_profile_trace(trace.encode(), C.byref(cfg), C.byref(plan), table, n, C.byref(pr)))
+    return _profile_dict(pr, table)
+
+
 def atom_plan_schedule(plan: Plan, sync=False) -> str:
     n = C.c_int64(0)
     lib.atom_plan_schedule(C.byref(plan), int(sync), None, 0, C.byref(n))
@@ -180,7 +208,7 @@ class Stats(C.Structure):
                 ("d2h_bytes", C.c_double), ("copy_ms", C.c_double), ("copy_hidden_ms", C.c_double),
                 ("step_ms", C.c_double), ("h2d_ms", C.c_double), ("h2d_hidden_ms", C.c_double),
                 ("d2h_ms", C.c_double), ("d2h_hidden_ms", C.c_double), ("compute_busy_ms", C.c_double),
-                ("compute_span_ms", C.c_double)]
+                ("compute_span_ms", C.c_double), ("host_issue_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -283,6 +311,14 @@ class Peer:
         check(lib.atom_get_trace(self.h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
 
+    def profile(self) -> dict:
+        """atom_profile: rates and per-node cost table measured from this peer's last step."""
+        n = 2 * (self.cfg.n_layer + 2)
+        table = (C.c_int64 * n)()
+        pr = Profile()
+        check(lib.atom_profile(self.h, table, n, C.byref(pr)))
+        return _profile_dict(pr, table)
+
     def kernel_log(self) -> dict:
         """Per kernel category since the last reset_stats(timing=True): {category: (groups, ms)}."""
         n = C.c_int64(0)
@@ -334,7 +370,8 @@ class Peer:
         check(lib.atom_get_stats(self.h, C.byref(s)))
         return s.as_dict()
 
-    def reset_stats(self, timing=False):
+    def reset_stats(self, timing=0):
+        """timing: 0 off, 1 per-GEMM CUDA events, 2 also per kernel category (kernel_log)."""
         check(lib.atom_reset_stats(self.h, int(timing)))
 
     def destroy(self):

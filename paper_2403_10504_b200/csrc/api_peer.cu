@@ -20,6 +20,8 @@ bool peer_kernel_log(atom_peer* p, std::string* out);
 void peer_reset_stats(atom_peer* p, int timing);
 void peer_free(atom_peer* p);
 bool peer_stream_sync(atom_peer* p);
+bool profile_from_trace(const char* trace, const atom_model_cfg& cfg, const atom_plan_t& plan, atom_profile_t* out,
+                        int64_t* table, int64_t cap);
 }  // namespace atom
 
 using namespace atom;
@@ -260,6 +262,14 @@ atom_status atom_get_kernel_log(atom_peer* p, char* buf, int64_t cap, int64_t* l
   memcpy(buf, s.data(), s.size());
   buf[s.size()] = 0;
   return ATOM_OK;
+}
+
+atom_status atom_profile(atom_peer* p, int64_t* cost_table, int64_t cap, atom_profile_t* out) {
+  if (!p || !out) { set_error("atom_profile: NULL"); return ATOM_E_INVALID; }
+  std::string tr;
+  if (!peer_trace(p, &tr, nullptr)) return fail(p, ATOM_E_CUDA);
+  if (tr.empty()) { set_error("atom_profile: the peer has not run a step"); return ATOM_E_STATE; }
+  return profile_from_trace(tr.c_str(), p->cfg, p->plan, out, cost_table, cap) ? ATOM_OK : ATOM_E_INVALID;
 }
 
 atom_status atom_get_stats(atom_peer* p, atom_stats_t* out) {

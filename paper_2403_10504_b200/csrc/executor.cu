@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <string>
 
@@ -141,7 +142,7 @@ const char* kcat_name(int c) {
   return c >= 0 && c < KC_N ? n[c] : "?";
 }
 bool kt_mark(atom_peer* p, int cat, cudaStream_t st, bool end) {
-  if (!p->timing) return true;
+  if (p->timing < 2) return true;   // per-category events only at timing level 2 (they cost step time)
   const size_t i = end ? 2 * (p->kt_n - 1) + 1 : 2 * p->kt_n;
   if (!end) {
     while (p->kt_ev.size() < 2 * (p->kt_n + 1)) {
@@ -644,6 +645,7 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
 
 template <typename T>
 bool run_step(atom_peer* p, float* loss_out) {
+  const auto h0 = std::chrono::steady_clock::now();
   // gradient rounds (R37): step = round; the optimizer step count t advances on update rounds
   const int R = p->cfg.grad_rounds;
   p->round = R > 0 ? (int)(p->steps % R) : 0;
@@ -665,6 +667,9 @@ bool run_step(atom_peer* p, float* loss_out) {
     }
   }
   for (size_t i = 0; i < ops.size(); ++i) PEER_OK(issue_op<T>(p, ops[i], sync, (int)i));
+  // host time spent issuing the step's work (launches, tensor-map encodes, events): if it reaches
+  // the device time of a step the GPU waits for the host
+  p->host_issue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   p->trace_ops = ops;
   p->have_trace = true;
   // relabel logical slots so that the next step starts from the queue [0 .. nslot-1]
@@ -1146,6 +1151,7 @@ bool peer_stats(atom_peer* p, atom_stats_t* s) {
   p->kt_n = 0;
   memset(s, 0, sizeof(*s));
   s->steps = p->steps;
+  s->host_issue_ms = p->host_issue_ms;
   s->kernel_launches = (int64_t)(g_launch_count - p->launch_base);
   s->gemm_launches = p->gemm_launches;
   s->gemm_ms = p->gemm_ms_acc;

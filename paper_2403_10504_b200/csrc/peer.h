@@ -111,4 +111,5 @@ struct atom_peer {
   unsigned long long launch_base = 0;
   double h2d_bytes = 0, d2h_bytes = 0;
   double gemm_ms_acc = 0, gemm_fl_acc = 0;
+  double host_issue_ms = 0;
 };

@@ -1,74 +1,76 @@
-"""Measured-profile helpers (paper_2403_10504_b200/profile.py): trace interval union and the FLOPs a
-planned step executes, checked against hand counts."""
+"""Measured profile (csrc/profile.cpp through atom_profile_trace, pure host): the compute-lane busy
+union, the executed FLOPs of a plan (with its re-forward) and the per-node cost table, checked
+against hand counts on synthetic traces (P:329 per-layer profiling; R34)."""
 import synth
 from paper_2403_10504_b200 import atom
-from paper_2403_10504_b200 import profile as aprof
 
 
-def test_compute_busy_union_and_span():
+def _plan(ends, C=2, n_recompute=0, h2d=0, d2h=0, flops=0):
+    p = atom.Plan()
+    p.n_seg = len(ends)
+    for i, e in enumerate(ends):
+        p.seg_end[i] = e
+    p.C, p.n_recompute, p.pred_h2d_B, p.pred_d2h_B, p.pred_flops = C, n_recompute, h2d, d2h, flops
+    return p
+
+
+def _cfg(L=4, d=64, T=32, b=2):
+    g = synth.GPTConfig("t", n_layer=L, d_model=d, n_head=4, seq_len=T, vocab=256, micro_batch=b)
+    return atom.make_cfg(g, dtype=atom.BF16)
+
+
+def test_busy_union_copy_rates_and_flops():
     tr = "\n".join([
         "compute FWD 1 0 - 100.0 300.0",
         "compute FWD 1 1 - 250.0 400.0",     # overlaps the first: union 100..400
-        "h2d LOAD_F 2 - 1 0.0 1000.0",       # other lanes are ignored
+        "h2d LOAD_F 2 - 1 0.0 1000.0",       # 1 ms of h2d
+        "d2h STORE 2 - 1 0.0 500.0",         # 0.5 ms of d2h
         "compute BWD 1 0 - 500.0 600.0",
     ])
-    assert abs(aprof.compute_busy_ms(tr) - 0.4) < 1e-12       # (300 + 100) us
-    assert abs(aprof.compute_span_ms(tr) - 0.5) < 1e-12       # 100 .. 600 us
-    assert abs(aprof.lane_ms(tr, "h2d") - 1.0) < 1e-12
+    pr = atom.atom_profile_trace(tr, _cfg(), _plan([1, 5], h2d=10 ** 9, d2h=10 ** 9, flops=4 * 10 ** 12))
+    assert abs(pr["compute_busy_ms"] - 0.4) < 1e-12          # (300 + 100) us
+    assert abs(pr["flops"] - 4e12 / 0.4e-3) <= 1e-6 * 1e16
+    assert abs(pr["h2d"] - 1e12) <= 1e3 and abs(pr["d2h"] - 2e12) <= 1e3
+    assert pr["cost_table"] == []                            # no blocks-only sub-model
 
 
 def test_executed_flops_counts_the_reforward():
-    g = synth.CONFIGS["2.7b"]
-    cfg_r = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(1.6e15), state_budget=20 * 2 ** 30,
-                          act_policy=atom.ACT_RECOMPUTE)
-    plan_r = atom.atom_plan(cfg_r, int(178e9), int(49.7e9))
-    ends = plan_r.ends()
-    nb_last = g.n_layer - ends[-2]
-    tok = plan_r.C * g.micro_batch * g.seq_len
-    d, T = g.d_model, g.seq_len
-    # re-forward of every block outside the last segment: QKV + projection + fc GEMMs, attention fwd
-    want = plan_r.pred_flops + (g.n_layer - nb_last) * tok * (2 * (3 + 1 + 4) * d * d + 2 * d * (T + 1))
-    assert abs(aprof.executed_flops(cfg_r, plan_r) - want) <= 1e-9 * want
-    # without a re-forward the executed FLOPs are the model FLOPs
-    cfg_s = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(1.0e15), state_budget=20 * 2 ** 30,
-                          act_policy=atom.ACT_STASH)
-    plan_s = atom.atom_plan(cfg_s, int(178e9), int(49.7e9))
-    assert aprof.executed_flops(cfg_s, plan_s) == float(plan_s.pred_flops)
+    cfg = _cfg(L=4, d=64, T=32, b=2)
+    C, nrc, base = 3, 2, 10 ** 9
+    pr = atom.atom_profile_trace("compute FWD 1 0 - 0 1000\n", cfg, _plan([1, 5], C=C, n_recompute=nrc, flops=base))
+    tok = C * 2 * 32
+    want = base + nrc * tok * (2 * (3 + 1 + 4) * 64 * 64 + 2 * 64 * 33)   # QKV + proj + fc GEMMs, attention fwd
+    assert abs(pr["executed_flops"] - want) <= 1e-9 * want
 
 
-class _Plan:
-    def __init__(self, ends, policy, n_recompute=0):
-        self._ends, self.act_policy, self.n_recompute = ends, policy, n_recompute
-
-    def ends(self):
-        return self._ends
-
-
-def test_cost_table_from_trace_blocks_embed_head():
+def test_cost_table_blocks_embed_head():
     # L = 4: nodes E, B0..B3, H; segments [E, B0] [B1, B2] [B3, H]; 2 micro-batches each
     tf, tb, emb_f, emb_b, hf, hb = 100.0, 250.0, 7.0, 11.0, 30.0, 60.0
-    lines = []
-    for mb in range(2):
-        lines.append(f"compute FWD 1 {mb} - 0 {emb_f + tf}")
-        lines.append(f"compute BWD 1 {mb} - 0 {emb_b + tb}")
-        lines.append(f"compute FWD 2 {mb} - 0 {2 * tf}")
-        lines.append(f"compute BWD 2 {mb} - 0 {2 * tb}")
-        lines.append(f"compute FWD 3 {mb} - 0 {tf + hf + hb}")   # head fwd + bwd inside FWD(S)
-        lines.append(f"compute BWD 3 {mb} - 0 {tb}")
-    t = aprof.cost_table_from_trace("\n".join(lines), _Plan([1, 3, 5], atom.ACT_STASH), 4)
-    us = [x / 1000.0 for x in t]
+    cfg = _cfg()
+
+    def trace(b2=2 * tb, b1=emb_b + tb):
+        lines = []
+        for mb in range(2):
+            lines += [f"compute FWD 1 {mb} - 0 {emb_f + tf}", f"compute BWD 1 {mb} - 0 {b1}",
+                      f"compute FWD 2 {mb} - 0 {2 * tf}", f"compute BWD 2 {mb} - 0 {b2}",
+                      f"compute FWD 3 {mb} - 0 {tf + hf + hb}",   # head fwd + bwd inside FWD(S)
+                      f"compute BWD 3 {mb} - 0 {tb}"]
+        return "\n".join(lines)
+
+    us = [x / 1000.0 for x in atom.atom_profile_trace(trace(), cfg, _plan([1, 3, 5]))["cost_table"]]
     assert us[2:10] == [tf, tb] * 4
     assert abs(us[0] - emb_f) < 1e-6 and abs(us[1] - emb_b) < 1e-6
     assert abs(us[10] - (hf + hb) / 3) < 1e-3 and abs(us[11] - 2 * (hf + hb) / 3) < 1e-3
-    # under the re-forward policy the traced backward includes one forward per block: removed
-    lines_rc = [l.replace(f"BWD 2 ", "BWD 2 ") for l in lines]
-    lines_rc = [(f"compute BWD 2 {l.split()[3]} - 0 {2 * (tb + tf)}" if l.split()[1:3] == ["BWD", "2"] else l)
-                for l in lines_rc]
-    t_rc = aprof.cost_table_from_trace("\n".join(lines_rc), _Plan([1, 3, 5], atom.ACT_HYBRID, 3), 4)
-    assert abs(t_rc[3] / 1000.0 - tb) < 1e-6
-    # hybrid: only blocks 1..2 re-forwarded -> segment 2 holds one of them (B1), segment 1 one (B0)
-    lines_h = [(f"compute BWD 2 {l.split()[3]} - 0 {2 * tb + tf}" if l.split()[1:3] == ["BWD", "2"] else
-                (f"compute BWD 1 {l.split()[3]} - 0 {emb_b + tb + tf}" if l.split()[1:3] == ["BWD", "1"] else l))
-               for l in lines]
-    t_h = aprof.cost_table_from_trace("\n".join(lines_h), _Plan([1, 3, 5], atom.ACT_HYBRID, 2), 4)
-    assert abs(t_h[3] / 1000.0 - tb) < 1e-6 and abs(t_h[1] / 1000.0 - emb_b) < 1e-6
+    # re-forward of blocks 1..3 (B0 in segment 1, B1 B2 in segment 2): their traced backward holds
+    # one forward per block, removed again
+    t = atom.atom_profile_trace(trace(b2=2 * (tb + tf), b1=emb_b + tb + tf), cfg, _plan([1, 3, 5], n_recompute=3))
+    assert abs(t["cost_table"][3] / 1000.0 - tb) < 1e-6 and abs(t["cost_table"][1] / 1000.0 - emb_b) < 1e-6
+    # hybrid: blocks 1..2 only -> segment 2 holds one of them (B1), segment 1 one (B0)
+    t = atom.atom_profile_trace(trace(b2=2 * tb + tf, b1=emb_b + tb + tf), cfg, _plan([1, 3, 5], n_recompute=2))
+    assert abs(t["cost_table"][3] / 1000.0 - tb) < 1e-6 and abs(t["cost_table"][1] / 1000.0 - emb_b) < 1e-6
+
+
+def test_malformed_trace_is_rejected():
+    import pytest
+    with pytest.raises(atom.AtomError):
+        atom.atom_profile_trace("compute FWD one\n", _cfg(), _plan([1, 5]))
