@@ -90,9 +90,20 @@ typedef struct {
                              m and v with the mean gradient; the resident sub-model 1 accumulates on the
                              device and takes the same update on the GPU                                 */
   int32_t cpu_threads;    /* CPU AdamW threads (0 = all online cores)                                       */
+  float dropout_p;        /* minGPT dropout (embd / attn / resid sites; R38), 0 <= p < 1;
+                             masks from Philox4x32-10 keyed by dropout_seed, counter (i / 8, site, layer,
+                             micro_step), micro_step = (atom_step calls so far) * C + micro-batch            */
+  int32_t op_nodes;       /* 1 = operator-granular graph ("a node ... is a layer or an operator"):
+                             each block is two nodes, its attention half (LN1, QKV, attention, output
+                             projection) and its MLP half (LN2, fc, GELU, fc2); nodes E, A_0, M_0, ...,
+                             A_{L-1}, M_{L-1}, H, so a sub-model may end in the middle of a block.  The
+                             full activation stash only (R40); cost_table then has 2 (2L+2)
+                             entries                                                                     */
+  uint64_t dropout_seed;
 } atom_model_cfg;
 
-/* The plan: plain data, fixed capacity, no pointers.  Produced by atom_plan. */
+/* The plan: plain data, fixed capacity, no pointers.  Produced by atom_plan.  Node indices: 0 = E,
+ * blocks 1..L (op_nodes: 2l+1 = attention half of block l, 2l+2 = its MLP half), last = H. */
 typedef struct {
   int32_t n_seg;                  /* S: number of sub-models                                            */
   int32_t seg_end[ATOM_MAX_SEG];  /* last node index of each sub-model (nodes 0=E, 1..L blocks, L+1=H)  */

@@ -175,29 +175,43 @@ class PlanCfg:
     forced_ends: Optional[List[int]] = None
     n_recompute: int = 0          # ACT_HYBRID: re-forward blocks 1..n_recompute (those before the last segment)
     grad_rounds: int = 0          # > 0: host gradient sums + CPU AdamW (reading R37): bwd loads 8 B, stores 4 B
+    op_nodes: int = 0             # 1: operator-granular graph ("a node ... is a layer or an operator"):
+    #                               every block is two nodes, its attention half A_l (LN1, QKV, attention,
+    #                               output projection) and its MLP half M_l (LN2, fc, GELU, fc2), so a
+    #                               sub-model may end in the middle of a block (reading R40)
 
     @classmethod
     def from_gpt(cls, g, **kw):
         return cls(g.n_layer, g.d_model, g.n_head, g.seq_len, g.vocab, g.micro_batch, **kw)
 
 
+def n_nodes(c: PlanCfg) -> int:
+    """E, the block nodes (L, or 2L operator-granular halves), H."""
+    return (2 if c.op_nodes else 1) * c.n_layer + 2
+
+
 def node_params(c: PlanCfg):
-    """Padded parameter count per node: each tensor starts on a 64-element boundary."""
+    """Padded parameter count per node: each tensor starts on a 64-element boundary.
+    Operator-granular: the attention half holds ln1.g, ln1.b, W_qkv, b_qkv, W_o, b_o, the MLP half
+    ln2.g, ln2.b, W_fc, b_fc, W_pr, b_pr (the canonical block order split in two)."""
     d, V, T, L = c.d_model, c.vocab, c.seq_len, c.n_layer
     pE = al64(V * d) + al64(T * d)
-    pB = (al64(d) * 2 + al64(3 * d * d) + al64(3 * d) + al64(d * d) + al64(d)
-          + al64(d) * 2 + al64(4 * d * d) + al64(4 * d) + al64(4 * d * d) + al64(d))
+    pA = al64(d) * 2 + al64(3 * d * d) + al64(3 * d) + al64(d * d) + al64(d)
+    pM = al64(d) * 2 + al64(4 * d * d) + al64(4 * d) + al64(4 * d * d) + al64(d)
     pH = al64(d) * 2 + al64(V * d)
-    return [pE] + [pB] * L + [pH]
+    return [pE] + ([pA, pM] * L if c.op_nodes else [pA + pM] * L) + [pH]
 
 
 def node_flops_fwd(c: PlanCfg):
-    """F^f per micro-batch: blocks 24 d^2 M + 2 d T (T+1) b (causal half); head 2 d V M."""
+    """F^f per micro-batch: blocks 24 d^2 M + 2 d T (T+1) b (causal half); head 2 d V M.
+    Operator-granular: attention half 8 d^2 M + 2 d T (T+1) b (QKV, attention, projection),
+    MLP half 16 d^2 M (fc, fc2)."""
     d, V, T, b, L = c.d_model, c.vocab, c.seq_len, c.micro_batch, c.n_layer
     M = b * T
-    fB = 24 * d * d * M + 2 * d * T * (T + 1) * b
+    fA = 8 * d * d * M + 2 * d * T * (T + 1) * b
+    fM = 16 * d * d * M
     fH = 2 * d * V * M
-    return [0] + [fB] * L + [fH]
+    return [0] + ([fA, fM] * L if c.op_nodes else [fA + fM] * L) + [fH]
 
 
 def node_flops_recompute(c: PlanCfg):
@@ -206,6 +220,8 @@ def node_flops_recompute(c: PlanCfg):
     not needed by the backward)."""
     d, T, b, L = c.d_model, c.seq_len, c.micro_batch, c.n_layer
     M = b * T
+    if c.op_nodes:   # unused: the operator-granular graph plans with the full stash only (R40)
+        return [0] + [8 * d * d * M + 2 * d * T * (T + 1) * b, 8 * d * d * M] * L + [0]
     return [0] + [16 * d * d * M + 2 * d * T * (T + 1) * b] * L + [0]
 
 
@@ -230,7 +246,7 @@ def node_costs(c: PlanCfg, link_bw: int) -> Costs:
     if c.cost_table is not None:
         tf = [c.cost_table[2 * i] for i in range(n)]
         tb = [c.cost_table[2 * i + 1] for i in range(n)]
-        tbr = [tb[i] + (tf[i] if 1 <= i <= c.n_layer else 0) for i in range(n)]
+        tbr = [tb[i] + (tf[i] if 1 <= i < n - 1 else 0) for i in range(n)]
     else:
         tf = [ceil_div(f * 10 ** 9, c.peak_flops) for f in ff]
         tb = [ceil_div(2 * f * 10 ** 9, c.peak_flops) for f in ff]
@@ -362,7 +378,7 @@ class Evaluator:
         self.k = node_costs(c, link_bw)
         self.pre, self.n = _seg_tables(c, self.k)
         self.L = c.n_layer
-        tbx = [self.k.tbr[v] if 1 <= v <= R else self.k.tb[v] for v in range(self.n)]
+        tbx = [self.k.tbr[v] if 1 <= v <= R and not c.op_nodes else self.k.tb[v] for v in range(self.n)]
         self.pre["tbx"] = _seg_tables(c, dataclasses.replace(self.k, tbr=tbx))[0]["tbr"]
 
     def tbn(self, i, j):
@@ -377,7 +393,10 @@ class Evaluator:
         return seg_need(self.c, self.s("P", i, j))
 
     def nblocks(self, i, j):
-        # blocks are nodes 1..L
+        """Whole blocks inside nodes [i..j] (block nodes 1..L; operator-granular: block l is the node
+        pair 2l+1, 2l+2, counted when both halves are inside)."""
+        if self.c.op_nodes:
+            return sum(1 for l in range(self.L) if i <= 2 * l + 1 and 2 * l + 2 <= j)
         lo, hi = max(i, 1), min(j, self.L)
         return max(0, hi - lo + 1)
 
@@ -473,6 +492,8 @@ def policies(c: PlanCfg):
     re-forwards every block before the last segment, ACT_RECOMPUTE): every re-forwarded block
     costs its forward again, so the fewest that make a plan feasible wins, then the smallest C
     (readings R28, R35)."""
+    if c.op_nodes:   # operator-granular graph: the full stash only (reading R40)
+        return [0] if c.act_policy in (ACT_AUTO, ACT_STASH) else []
     if c.act_policy == ACT_AUTO:
         return list(range(c.n_layer + 1))
     return {ACT_STASH: [0], ACT_RECOMPUTE: [c.n_layer], ACT_HYBRID: [c.n_recompute]}[c.act_policy]

@@ -109,7 +109,8 @@ class ModelCfg(C.Structure):
                 ("n_forced", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("eps", C.c_float), ("weight_decay", C.c_float), ("warmup_steps", C.c_int32),
                 ("sync_every", C.c_int32), ("n_recompute", C.c_int32), ("grad_rounds", C.c_int32),
-                ("cpu_threads", C.c_int32)]
+                ("cpu_threads", C.c_int32), ("dropout_p", C.c_float), ("op_nodes", C.c_int32),
+                ("dropout_seed", C.c_uint64)]
 
 
 class Plan(C.Structure):
@@ -132,7 +133,7 @@ class Plan(C.Structure):
 def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 10 ** 12, d2h_bw=0,
              state_budget=0, cost_table=None, forced_ends=None, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8,
              weight_decay=0.01, warmup_steps=3000, sync_every=0, act_policy=0, n_recompute=0, grad_rounds=0,
-             cpu_threads=0):
+             cpu_threads=0, dropout_p=0.0, dropout_seed=0, op_nodes=0):
     """atom_model_cfg from a synth.GPTConfig-like object (keeps ctypes arrays alive on the struct)."""
     c = ModelCfg()
     c.n_layer, c.d_model, c.n_head, c.seq_len, c.vocab, c.micro_batch = (
@@ -151,6 +152,7 @@ def make_cfg(g, dtype=BF16, C_=0, max_C=64, overlap_check=1, peak_flops=1606 * 1
     c.lr, c.beta1, c.beta2, c.eps, c.weight_decay = lr, beta1, beta2, eps, weight_decay
     c.warmup_steps, c.sync_every, c.n_recompute = warmup_steps, sync_every, n_recompute
     c.grad_rounds, c.cpu_threads = grad_rounds, cpu_threads
+    c.dropout_p, c.dropout_seed, c.op_nodes = dropout_p, dropout_seed, op_nodes
     return c
 
 

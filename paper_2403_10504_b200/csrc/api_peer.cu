@@ -87,6 +87,25 @@ atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan,
     delete p;
     return ATOM_E_INVALID;
   }
+  if (cfg->op_nodes) {
+    set_error("atom_peer_create: operator-granular plans are not executable yet");
+    delete p;
+    return ATOM_E_INVALID;
+  }
+  if (cfg->dropout_p != 0.f) {
+    // DESIGN.md R38: masks are drawn per 8-element Philox group of each site tensor (T % 8 keeps the
+    // attention rows whole groups), the group index is one 32-bit counter word, and the bf16
+    // attention kernels that apply the attention-site mask are the tcgen05 ones (d_h 64/80/128)
+    const int dh = dm.d / dm.h;
+    const double n_attn = (double)dm.b * dm.h * dm.T * dm.T;
+    if (!(cfg->dropout_p > 0.f && cfg->dropout_p < 1.f) || dm.T % 8 || n_attn > 34359738368.0 ||
+        (dm.dtype == ATOM_BF16 && !attn_tc_supported(dh, dm.d))) {
+      set_error("invalid config: dropout needs 0 <= p < 1, T %% 8 == 0, b h T^2 <= 2^35 and (bf16) a tcgen05 "
+                "attention head size (64, 80, 128)");
+      delete p;
+      return ATOM_E_INVALID;
+    }
+  }
   p->device = device;
   p->arena = (uint8_t*)device_arena;
   p->arena_bytes = arena_bytes;

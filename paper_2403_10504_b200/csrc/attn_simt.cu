@@ -5,6 +5,8 @@
 // Backward (exact, deterministic, no atomics):
 //   D_t = do_t . o_t;  P_ts = exp(S_ts - lse_t);  dS_ts = P_ts (do_t . v_s - D_t)
 //   dq_t = sum_{s<=t} dS_ts k_s / sqrt(dh);  dk_s = sum_{t>=s} dS_ts q_t / sqrt(dh);  dv_s = sum_{t>=s} P_ts do_t
+// With attention dropout (multiplier m_ts of element ((b h + head) T + t) T + s, R38):
+//   o_t = sum_s m_ts P_ts v_s / l;  dS_ts = P_ts (m_ts do_t . v_s - D_t);  dv_s = sum_t m_ts P_ts do_t
 #include "common.cuh"
 #include "kernels.h"
 
@@ -30,7 +32,7 @@ __device__ __forceinline__ float dotw(const float* a, const float* b) {
 
 template <typename T>
 __global__ void attn_fwd_simt_kernel(const T* __restrict__ qkv, T* __restrict__ o, float* __restrict__ lse, int B,
-                                     int T_, int h, int dh) {
+                                     int T_, int h, int dh, Drop drop) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   if (gw >= (long)B * h * T_) return;
   const int t = (int)(gw % T_);
@@ -53,8 +55,9 @@ __global__ void attn_fwd_simt_kernel(const T* __restrict__ qkv, T* __restrict__ 
     const float corr = __expf(m - mn);
     const float p = __expf(sco - mn);
     l = l * corr + p;
+    const float pm = p * drop_mult(drop, (((uint64_t)b * h + hh) * T_ + t) * (uint64_t)T_ + s);
 #pragma unroll
-    for (int i = 0; i < AMAX; ++i) acc[i] = fmaf(p, v[i], acc[i] * corr);
+    for (int i = 0; i < AMAX; ++i) acc[i] = fmaf(pm, v[i], acc[i] * corr);
     m = mn;
   }
   const int lane = threadIdx.x & 31;
@@ -86,7 +89,7 @@ __global__ void attn_dsum_kernel(const T* __restrict__ o, const T* __restrict__ 
 template <typename T>
 __global__ void attn_dq_simt_kernel(const T* __restrict__ qkv, const T* __restrict__ dout,
                                     const float* __restrict__ lse, const float* __restrict__ Dsum,
-                                    T* __restrict__ dqkv, int B, int T_, int h, int dh) {
+                                    T* __restrict__ dqkv, int B, int T_, int h, int dh, Drop drop) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   if (gw >= (long)B * h * T_) return;
   const int t = (int)(gw % T_);
@@ -107,7 +110,8 @@ __global__ void attn_dq_simt_kernel(const T* __restrict__ qkv, const T* __restri
     load_row(base + (long)s * ld + d + hh * dh, dh, k);
     load_row(base + (long)s * ld + 2 * d + hh * dh, dh, v);
     const float p = __expf(dotw(q, k) * sc - L);
-    const float ds = p * (dotw(g, v) - Dt);
+    const float m = drop_mult(drop, (((uint64_t)b * h + hh) * T_ + t) * (uint64_t)T_ + s);
+    const float ds = p * (m * dotw(g, v) - Dt);
 #pragma unroll
     for (int i = 0; i < AMAX; ++i) dq[i] = fmaf(ds, k[i], dq[i]);
   }
@@ -123,7 +127,7 @@ __global__ void attn_dq_simt_kernel(const T* __restrict__ qkv, const T* __restri
 template <typename T>
 __global__ void attn_dkv_simt_kernel(const T* __restrict__ qkv, const T* __restrict__ dout,
                                      const float* __restrict__ lse, const float* __restrict__ Dsum,
-                                     T* __restrict__ dqkv, int B, int T_, int h, int dh) {
+                                     T* __restrict__ dqkv, int B, int T_, int h, int dh, Drop drop) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   if (gw >= (long)B * h * T_) return;
   const int s = (int)(gw % T_);
@@ -144,10 +148,11 @@ __global__ void attn_dkv_simt_kernel(const T* __restrict__ qkv, const T* __restr
     const float L = lse[((long)b * h + hh) * T_ + t];
     const float Dt = Dsum[((long)b * h + hh) * T_ + t];
     const float p = __expf(dotw(q, k) * sc - L);
-    const float ds = p * (dotw(g, v) - Dt);
+    const float m = drop_mult(drop, (((uint64_t)b * h + hh) * T_ + t) * (uint64_t)T_ + s);
+    const float ds = p * (m * dotw(g, v) - Dt);
 #pragma unroll
     for (int i = 0; i < AMAX; ++i) {
-      dv[i] = fmaf(p, g[i], dv[i]);
+      dv[i] = fmaf(p * m, g[i], dv[i]);
       dk[i] = fmaf(ds, q[i], dk[i]);
     }
   }
@@ -164,10 +169,10 @@ __global__ void attn_dkv_simt_kernel(const T* __restrict__ qkv, const T* __restr
 }
 
 template <typename T>
-bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st) {
+bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st, Drop drop) {
   if (dh > 32 * AMAX) { set_error("attention: head size %d > %d", dh, 32 * AMAX); return false; }
   const long warps = (long)B * h * T_;
-  attn_fwd_simt_kernel<T><<<(warps + 7) / 8, 256, 0, st>>>(qkv, o, lse, B, T_, h, dh);
+  attn_fwd_simt_kernel<T><<<(warps + 7) / 8, 256, 0, st>>>(qkv, o, lse, B, T_, h, dh, drop);
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
@@ -175,25 +180,25 @@ bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh,
 
 template <typename T>
 bool attn_bwd_simt(const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv, int B, int T_,
-                   int h, int dh, cudaStream_t st) {
+                   int h, int dh, cudaStream_t st, Drop drop) {
   if (dh > 32 * AMAX) { set_error("attention: head size %d > %d", dh, 32 * AMAX); return false; }
   const long warps = (long)B * h * T_;
   const int grid = (int)((warps + 7) / 8);
   attn_dsum_kernel<T><<<grid, 256, 0, st>>>(o, dout, Dsum, B, T_, h, dh);
   count_launch();
-  attn_dq_simt_kernel<T><<<grid, 256, 0, st>>>(qkv, dout, lse, Dsum, dqkv, B, T_, h, dh);
+  attn_dq_simt_kernel<T><<<grid, 256, 0, st>>>(qkv, dout, lse, Dsum, dqkv, B, T_, h, dh, drop);
   count_launch();
-  attn_dkv_simt_kernel<T><<<grid, 256, 0, st>>>(qkv, dout, lse, Dsum, dqkv, B, T_, h, dh);
+  attn_dkv_simt_kernel<T><<<grid, 256, 0, st>>>(qkv, dout, lse, Dsum, dqkv, B, T_, h, dh, drop);
   count_launch();
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }
 
-template bool attn_fwd_simt<float>(const float*, float*, float*, int, int, int, int, cudaStream_t);
-template bool attn_fwd_simt<bf16>(const bf16*, bf16*, float*, int, int, int, int, cudaStream_t);
+template bool attn_fwd_simt<float>(const float*, float*, float*, int, int, int, int, cudaStream_t, Drop);
+template bool attn_fwd_simt<bf16>(const bf16*, bf16*, float*, int, int, int, int, cudaStream_t, Drop);
 template bool attn_bwd_simt<float>(const float*, const float*, const float*, const float*, float*, float*, int, int,
-                                   int, int, cudaStream_t);
+                                   int, int, cudaStream_t, Drop);
 template bool attn_bwd_simt<bf16>(const bf16*, const bf16*, const bf16*, const float*, float*, bf16*, int, int, int,
-                                  int, cudaStream_t);
+                                  int, cudaStream_t, Drop);
 
 }  // namespace atom

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "philox.cuh"
 
 namespace atom {
 namespace atc {
@@ -229,233 +230,6 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
                 __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
 }
 
-template <int DH>
-struct Cfg {
-  static constexpr int NP = (DH + 63) / 64;        // 64-feature panels per row
-  static constexpr int PANEL = 128 * 128;          // bytes: 128 rows x 128 B
-  static constexpr int Q_BYTES = NP * PANEL;
-  static constexpr int KV_BYTES = 2 * NP * PANEL;  // K and V of one stage
-  static constexpr int P_BYTES = 2 * PANEL;        // 128 queries x 128 keys bf16
-  static constexpr int SMEM = Q_BYTES + 2 * KV_BYTES + P_BYTES + 1024 + 256;
-  static constexpr int S_COL0 = 0, O_COL = 256;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(256, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, float* __restrict__ lse, int T_,
-                       int h) {
-  using C = Cfg<DH>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
-  uint8_t* sQ = sm;
-  uint8_t* sKV = sQ + C::Q_BYTES;  // stage s: K at sKV + s*KV_BYTES, V at + NP*PANEL
-  uint8_t* sP = sKV + 2 * C::KV_BYTES;
-  uint64_t* bars = (uint64_t*)(sP + C::P_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 9);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (T_ + BQ - 1) / BQ;
-  const int qb = nqb - 1 - blockIdx.x;     // heavy (late) query blocks first
-  const int bh = blockIdx.y;
-  const int b = bh / h, hh = bh % h;
-  const int d = h * DH;
-  const int q0 = qb * BQ;
-  const int nkb = min(qb + 1, (T_ + BKV - 1) / BKV);
-  const int row0 = b * T_;   // token row of this sequence in qkv
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-    }
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int p = 0; p < C::NP; ++p) tma_load(sQ + p * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + q0);
-      for (int j = 0; j < nkb; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        uint8_t* k = sKV + s * C::KV_BYTES;
-        uint8_t* v = k + C::NP * C::PANEL;
-        mbar_expect_tx(&kv_full[s], C::KV_BYTES);
-        for (int p = 0; p < C::NP; ++p) {
-          tma_load(k + p * C::PANEL, &tm, &kv_full[s], d + hh * DH + 64 * p, row0 + j * BKV);
-          tma_load(v + p * C::PANEL, &tm, &kv_full[s], 2 * d + hh * DH + 64 * p, row0 + j * BKV);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t id_s = idesc_bf16(128, BKV, false, false);  // S = Q K^T   (both K-major)
-    constexpr uint32_t id_o = idesc_bf16(128, DH, false, true);    // O += P V    (V MN-major)
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(&kv_full[s], (j >> 1) & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sQ), k = smem_u32(sKV + s * C::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::PANEL + (kk & 3) * 32;
-          mma(tbase + C::S_COL0 + s * BKV, desc_sw128(q + off, 16, 1024), desc_sw128(k + off, 16, 1024), id_s,
-              kk > 0);
-        }
-        commit(&s_full[s]);
-      }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int j = 0; j < nkb; ++j) {
-      if (j + 1 < nkb) issue_s(j + 1);
-      mbar_wait(p_full, j & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t p = smem_u32(sP), v = smem_u32(sKV + (j & 1) * C::KV_BYTES + C::NP * C::PANEL);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * C::PANEL + (kk & 3) * 32;
-          mma(tbase + C::O_COL, desc_sw128(p + aoff, 16, 1024), desc_sw128(v + kk * 2048, C::PANEL, 1024), id_o,
-              (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        commit(o_done);
-        commit(&kv_empty[j & 1]);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax
-    const int qw = warp & 3;
-    const int r = 32 * qw + lane;  // query row within the block = TMEM lane
-    const int qi = q0 + r;
-    const uint32_t lane_addr = tbase + ((uint32_t)(32 * qw) << 16);
-    const float sc = rsqrtf((float)DH) * LOG2E;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
-      fence_after();
-      uint32_t raw[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV; c += 32) tmem_ld32(lane_addr + C::S_COL0 + s * BKV + c, raw + c);
-      tmem_wait_ld();
-      // masking only on the diagonal block and the ragged last block
-      const bool masked = j == qb || (j + 1) * BKV > T_;
-      float mx = -INFINITY;
-      if (masked) {
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) {
-          const int kj = j * BKV + c;
-          float v = __uint_as_float(raw[c]) * sc;
-          if (kj > qi || kj >= T_) v = -INFINITY;
-          raw[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BKV; ++c) {
-          const float v = __uint_as_float(raw[c]) * sc;
-          raw[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
-      }
-      // lazy rescale: move the reference max only when it grows by more than 2^8
-      const bool need = mx > m_ref + RESCALE_THRESHOLD;
-      const float new_ref = need ? mx : m_ref;
-      const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable and P buffer free
-      if (__any_sync(0xffffffffu, need) && j > 0) {
-        fence_after();
-#pragma unroll
-        for (int c = 0; c < DH; c += 16) {
-          uint32_t ov[16];
-          tmem_ld16(lane_addr + C::O_COL + c, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st16(lane_addr + C::O_COL + c, ov);
-        }
-        tmem_wait_st();
-      }
-      l *= alpha;
-      m_ref = new_ref;
-      // P = exp2(S - m_ref) -> bf16, 128B-swizzled K-major rows (2 panels of 64 keys)
-      float rs = 0.f;
-      uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-      for (int c8 = 0; c8 < BKV / 8; ++c8) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float p0 = fast_exp2(__uint_as_float(raw[c8 * 8 + 2 * i]) - m_ref);
-          const float p1 = fast_exp2(__uint_as_float(raw[c8 * 8 + 2 * i + 1]) - m_ref);
-          rs += p0 + p1;
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-          pk[i] = *(uint32_t*)&v2;
-        }
-        const int panel = c8 >> 3, ch = c8 & 7;
-        *(uint4*)(prow + panel * C::PANEL + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-      }
-      l += rs;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      mbar_arrive(p_full);
-    }
-    // epilogue: O / l -> bf16, LSE (natural log)
-    mbar_wait(o_done, (nkb - 1) & 1);
-    fence_after();
-    const float inv = 1.f / l;
-    bf16* orow = o + ((long)b * T_ + qi) * d + hh * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 16) {
-      uint32_t ov[16];
-      tmem_ld16(lane_addr + C::O_COL + c, ov);
-      tmem_wait_ld();
-      if (qi < T_) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 v2 =
-              __floats2bfloat162_rn(__uint_as_float(ov[2 * i]) * inv, __uint_as_float(ov[2 * i + 1]) * inv);
-          pk[i] = *(uint32_t*)&v2;
-        }
-        *(uint4*)(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *(uint4*)(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-    if (qi < T_) lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
-  }
-}
-
 // ======================================================================================
 // Forward v2: two 128-query tiles per CTA, ping-pong between two softmax warpgroups so the
 // tensor core works on one tile while the other tile's exponentials run.
@@ -486,12 +260,15 @@ struct Cfg2 {
   static_assert(!TSA || Q_COL + 128 + DH / 2 <= 512, "TMEM budget");
 };
 
-template <int DH, bool TSA>
+// DROP: attention-probability dropout (R38): the P stored for P V is D(P) (one Philox call
+// per 8 keys of the thread's query row), the normaliser l and the LSE keep the undropped P
+template <int DH, bool TSA, bool DROP>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, const bf16* __restrict__ qkv, bf16* __restrict__ o,
-                        float* __restrict__ lse, int T_, int h) {
+                        float* __restrict__ lse, int T_, int h, const Drop drop) {
   using C = Cfg2<DH, TSA>;
   constexpr int NS = C::NSLOT;
+  (void)drop;
   // of 8 pairs on the FMA pipe: MUFU.EX2 (16/clk/SM) keeps pace with the MMAs at d_h = 128 but
   // not with the shorter MMAs of d_h = 80 / 64
 #ifndef ATOM_FWD_POLY80
@@ -702,6 +479,13 @@ __global__ void __launch_bounds__(384, 1)
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c16 = 0; c16 < BKV / 32; ++c16) {
+          uint32_t keep = 0xFFFFFFFFu;   // bit c: key j BKV + 32 c16 + c kept
+          if constexpr (DROP) {
+            const uint64_t g0 = ((((uint64_t)bh * T_ + qi) * T_) >> 3) + (uint64_t)(j * BKV + 32 * c16) / 8;
+            keep = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) keep |= drop_keep8(drop, (uint32_t)(g0 + q)) << (8 * q);
+          }
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -718,6 +502,10 @@ __global__ void __launch_bounds__(384, 1)
             rs2[i & 3] = fadd2(rs2[i & 3], p2);
             float p0, p1;
             f2unpack(p2, p0, p1);
+            if constexpr (DROP) {
+              p0 = (keep >> (2 * i)) & 1u ? p0 * drop.scale : 0.f;
+              p1 = (keep >> (2 * i + 1)) & 1u ? p1 * drop.scale : 0.f;
+            }
             __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
             pk[i] = *(uint32_t*)&v2;
           }
@@ -779,415 +567,6 @@ __global__ void __launch_bounds__(384, 1)
 // ======================================================================================
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-template <int DH>
-struct BCfg {
-  static constexpr int NP = (DH + 63) / 64;
-  static constexpr int P128 = 128 * 128;   // panel of 128 rows x 128 B
-  static constexpr int P64 = 64 * 128;     // panel of 64 rows x 128 B
-  // dK/dV kernel
-  static constexpr int KV_BYTES = 2 * NP * P128;          // K and V of the key block
-  static constexpr int QD_BYTES = 2 * NP * P64;           // Q_i and dO_i of one stage
-  static constexpr int PD_BYTES = 2 * 128 * 128;          // P^T and dS^T: 128 rows x 64 queries each
-  // two P^T/dS^T buffers and two S^T/dP^T TMEM buffers: the MMAs of block i+1 overlap the
-  // thread math of block i
-  static constexpr int SMEM_KV = KV_BYTES + 2 * QD_BYTES + 2 * PD_BYTES + 2 * 2 * 64 * 4 + 1024 + 256;
-  // dQ kernel
-  static constexpr int QO_BYTES = 2 * NP * P128;          // Q and dO of the query block
-  static constexpr int KVS_BYTES = 2 * NP * P64;          // K_j and V_j of one stage
-  static constexpr int DS_BYTES = 128 * 128;              // dS: 128 rows x 64 keys bf16 (x2 buffers)
-  static constexpr int SMEM_Q = QO_BYTES + 2 * KVS_BYTES + 2 * DS_BYTES + 1024 + 256;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(256, 1)
-    attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                           const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
-                           const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
-  using C = BCfg<DH>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
-  uint8_t* sK = sm;
-  uint8_t* sV = sK + C::NP * C::P128;
-  uint8_t* sQD = sm + C::KV_BYTES;                 // stage s: Q at + s*QD_BYTES, dO at + NP*P64
-  uint8_t* sPD = sQD + 2 * C::QD_BYTES;            // buffer u: P^T at + u*PD_BYTES, dS^T at + 128*128
-  float* sL = (float*)(sPD + 2 * C::PD_BYTES);     // [2][64]
-  float* sD = sL + 128;                            // [2][64]
-  uint64_t* bars = (uint64_t*)(sD + 128);
-  uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* pd_full = bars + 7;   // [2]
-  uint64_t* pd_empty = bars + 9;  // [2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x;       // key block 0 has the most work: scheduled first
-  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
-  const int d = h * DH;
-  const int k0 = kb * 128;
-  const int nq = (T_ + 63) / 64;
-  const int i0 = k0 / 64;          // first query block that sees these keys
-  const int nblk = nq - i0;
-  const int row0 = b * T_;
-  // TMEM: buffer u holds S^T at 128u and dP^T at 128u + 64; dV, dK accumulators after them
-  constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 256, DK_COL = 256 + ((DH + 15) / 16) * 16;
-
-  if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&qd_full[s], 1);
-      mbar_init(&qd_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&pd_full[s], 128);
-      mbar_init(&pd_empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(kv_full, C::KV_BYTES);
-      for (int p = 0; p < C::NP; ++p) {
-        tma_load(sK + p * C::P128, &tm_kv, kv_full, d + hh * DH + 64 * p, row0 + k0);
-        tma_load(sV + p * C::P128, &tm_kv, kv_full, 2 * d + hh * DH + 64 * p, row0 + k0);
-      }
-      for (int it = 0; it < nblk; ++it) {
-        const int s = it & 1, q0 = (i0 + it) * 64;
-        mbar_wait(&qd_empty[s], ((it >> 1) & 1) ^ 1);
-        uint8_t* q = sQD + s * C::QD_BYTES;
-        uint8_t* g = q + C::NP * C::P64;
-        mbar_expect_tx(&qd_full[s], C::QD_BYTES);
-        for (int p = 0; p < C::NP; ++p) {
-          tma_load(q + p * C::P64, &tm_q, &qd_full[s], hh * DH + 64 * p, row0 + q0);
-          tma_load(g + p * C::P64, &tm_do, &qd_full[s], hh * DH + 64 * p, row0 + q0);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
-    constexpr uint32_t id_g = idesc_bf16(128, DH, false, true);    // dV += P^T dO, dK += dS^T Q
-    mbar_wait(kv_full, 0);
-    // S^T / dP^T of block it into TMEM buffer it&1 (free: its previous user, block it-2, was
-    // consumed by the threads before they arrived on pd_full[it&1], which precedes dV/dK(it-2))
-    auto issue_s = [&](int it) {
-      const int s = it & 1;
-      mbar_wait(&qd_full[s], (it >> 1) & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
-        const uint32_t k = smem_u32(sK), v = smem_u32(sV);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + ST_COL + 128 * s, desc_sw128(k + oa, 16, 1024), desc_sw128(q + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + DPT_COL + 128 * s, desc_sw128(v + oa, 16, 1024), desc_sw128(g + ob, 16, 1024), id_s, kk > 0);
-        }
-        commit(&s_full[s]);
-      }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int it = 0; it < nblk; ++it) {
-      const int s = it & 1;
-      if (it + 1 < nblk) issue_s(it + 1);
-      mbar_wait(&pd_full[s], (it >> 1) & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t q = smem_u32(sQD + s * C::QD_BYTES), g = q + C::NP * C::P64;
-        const uint32_t pt = smem_u32(sPD + s * C::PD_BYTES), dst = pt + 128 * 128;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
-          const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
-          mma(tbase + DV_COL, desc_sw128(pt + kk * 32, 16, 1024), desc_sw128(g + kk * 2048, C::P64, 1024), id_g,
-              acc);
-          mma(tbase + DK_COL, desc_sw128(dst + kk * 32, 16, 1024), desc_sw128(q + kk * 2048, C::P64, 1024), id_g,
-              acc);
-        }
-        commit(&pd_empty[s]);
-        commit(&qd_empty[s]);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    const int qw = warp & 3;
-    const int r = 32 * qw + lane, kj = k0 + r;
-    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
-    const float sc = rsqrtf((float)DH) * LOG2E;
-    const float* lrow = lse + ((long)b * h + hh) * T_;
-    const float* drow = Dsum + ((long)b * h + hh) * T_;
-    const int t = threadIdx.x - 128;
-    for (int it = 0; it < nblk; ++it) {
-      const int s = it & 1, q0 = (i0 + it) * 64;
-      if (t < 64) {
-        const int qi = q0 + t;
-        sL[s * 64 + t] = qi < T_ ? lrow[qi] * LOG2E : INFINITY;
-      } else {
-        const int qi = q0 + t - 64;
-        sD[s * 64 + t - 64] = qi < T_ ? drow[qi] : 0.f;
-      }
-      named_sync(1, 128);
-      mbar_wait(&s_full[s], (it >> 1) & 1);
-      fence_after();
-      uint32_t sv[64], dv[64];
-      tmem_ld32(la + ST_COL + 128 * s, sv);
-      tmem_ld32(la + ST_COL + 128 * s + 32, sv + 32);
-      tmem_ld32(la + DPT_COL + 128 * s, dv);
-      tmem_ld32(la + DPT_COL + 128 * s + 32, dv + 32);
-      tmem_wait_ld();
-      if (it >= 2) mbar_wait(&pd_empty[s], ((it >> 1) & 1) ^ 1);   // dV/dK of block it-2 read this buffer
-      uint8_t* prow = sPD + s * C::PD_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
-      uint8_t* drw = prow + 128 * 128;
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        uint32_t pk[4], dk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float pp[2], dd[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = c8 * 8 + 2 * e + u, qi = q0 + c;
-            float p = fast_exp2(__uint_as_float(sv[c]) * sc - sL[s * 64 + c]);
-            if (qi < kj || kj >= T_) p = 0.f;
-            pp[u] = p;
-            dd[u] = p * (__uint_as_float(dv[c]) - sD[s * 64 + c]);
-          }
-          __nv_bfloat162 a2 = __floats2bfloat162_rn(pp[0], pp[1]), b2 = __floats2bfloat162_rn(dd[0], dd[1]);
-          pk[e] = *(uint32_t*)&a2;
-          dk[e] = *(uint32_t*)&b2;
-        }
-        const int sw = (c8 ^ (r & 7)) << 4;
-        *(uint4*)(prow + sw) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *(uint4*)(drw + sw) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      mbar_arrive(&pd_full[s]);
-    }
-    mbar_wait(&pd_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);   // last dV/dK MMAs (commit tracks all)
-    fence_after();
-    const float isq = rsqrtf((float)DH);
-    bf16* row = dqkv + ((long)row0 + kj) * 3 * d + hh * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 16) {
-      uint32_t gk[16], gv[16];
-      tmem_ld16(la + DK_COL + c, gk);
-      tmem_ld16(la + DV_COL + c, gv);
-      tmem_wait_ld();
-      if (kj < T_) {
-        uint32_t pk[8], pv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 k2 = __floats2bfloat162_rn(__uint_as_float(gk[2 * i]) * isq, __uint_as_float(gk[2 * i + 1]) * isq);
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(gv[2 * i]), __uint_as_float(gv[2 * i + 1]));
-          pk[i] = *(uint32_t*)&k2;
-          pv[i] = *(uint32_t*)&v2;
-        }
-        *(uint4*)(row + d + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *(uint4*)(row + d + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        *(uint4*)(row + 2 * d + c) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
-        *(uint4*)(row + 2 * d + c + 8) = make_uint4(pv[4], pv[5], pv[6], pv[7]);
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
-  }
-}
-
-template <int DH>
-__global__ void __launch_bounds__(256, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_kv, const float* __restrict__ lse,
-                          const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
-  using C = BCfg<DH>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
-  uint8_t* sQ = sm;
-  uint8_t* sO = sQ + C::NP * C::P128;
-  uint8_t* sKV = sm + C::QO_BYTES;    // stage s: K at + s*KVS_BYTES, V at + NP*P64
-  uint8_t* sdS = sKV + 2 * C::KVS_BYTES;   // buffer u at + u*DS_BYTES
-  uint64_t* bars = (uint64_t*)(sdS + 2 * C::DS_BYTES);
-  uint64_t* qo_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* ds_full = bars + 7;   // [2]
-  uint64_t* ds_empty = bars + 9;  // [2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (T_ + 127) / 128;
-  const int qb = nqb - 1 - blockIdx.x;
-  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
-  const int d = h * DH;
-  const int q0 = qb * 128;
-  const int nblk = min((q0 + 127) / 64 + 1, (T_ + 63) / 64);
-  const int row0 = b * T_;
-  // TMEM: buffer u holds S at 128u and dP at 128u + 64; the dQ accumulator at 256
-  constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 256;
-
-  if (threadIdx.x == 0) {
-    mbar_init(qo_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&ds_full[s], 128);
-      mbar_init(&ds_empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tbase = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(qo_full, C::QO_BYTES);
-      for (int p = 0; p < C::NP; ++p) {
-        tma_load(sQ + p * C::P128, &tm_q, qo_full, hh * DH + 64 * p, row0 + q0);
-        tma_load(sO + p * C::P128, &tm_do, qo_full, hh * DH + 64 * p, row0 + q0);
-      }
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        uint8_t* k = sKV + s * C::KVS_BYTES;
-        uint8_t* v = k + C::NP * C::P64;
-        mbar_expect_tx(&kv_full[s], C::KVS_BYTES);
-        for (int p = 0; p < C::NP; ++p) {
-          tma_load(k + p * C::P64, &tm_kv, &kv_full[s], d + hh * DH + 64 * p, row0 + j * 64);
-          tma_load(v + p * C::P64, &tm_kv, &kv_full[s], 2 * d + hh * DH + 64 * p, row0 + j * 64);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S = Q K^T, dP = dO V^T
-    constexpr uint32_t id_q = idesc_bf16(128, DH, false, true);    // dQ += dS K
-    mbar_wait(qo_full, 0);
-    auto issue_s = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(&kv_full[s], (j >> 1) & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES), v = k + C::NP * C::P64;
-        const uint32_t q = smem_u32(sQ), g = smem_u32(sO);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::P128 + (kk & 3) * 32, ob = (kk >> 2) * C::P64 + (kk & 3) * 32;
-          mma(tbase + S_COL + 128 * s, desc_sw128(q + oa, 16, 1024), desc_sw128(k + ob, 16, 1024), id_s, kk > 0);
-          mma(tbase + DP_COL + 128 * s, desc_sw128(g + oa, 16, 1024), desc_sw128(v + ob, 16, 1024), id_s, kk > 0);
-        }
-        commit(&s_full[s]);
-      }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int j = 0; j < nblk; ++j) {
-      const int s = j & 1;
-      if (j + 1 < nblk) issue_s(j + 1);
-      mbar_wait(&ds_full[s], (j >> 1) & 1);
-      fence_after();
-      if (lane == 0) {
-        const uint32_t k = smem_u32(sKV + s * C::KVS_BYTES);
-        const uint32_t ds = smem_u32(sdS + s * C::DS_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma(tbase + DQ_COL, desc_sw128(ds + kk * 32, 16, 1024), desc_sw128(k + kk * 2048, C::P64, 1024), id_q,
-              (j > 0 || kk > 0) ? 1u : 0u);
-        commit(&ds_empty[s]);
-        commit(&kv_empty[s]);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    const int qw = warp & 3;
-    const int r = 32 * qw + lane, qi = q0 + r;
-    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
-    const float sc = rsqrtf((float)DH) * LOG2E;
-    const float L = qi < T_ ? lse[((long)b * h + hh) * T_ + qi] * LOG2E : INFINITY;
-    const float Dr = qi < T_ ? Dsum[((long)b * h + hh) * T_ + qi] : 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
-      fence_after();
-      uint32_t sv[64], dv[64];
-      tmem_ld32(la + S_COL + 128 * s, sv);
-      tmem_ld32(la + S_COL + 128 * s + 32, sv + 32);
-      tmem_ld32(la + DP_COL + 128 * s, dv);
-      tmem_ld32(la + DP_COL + 128 * s + 32, dv + 32);
-      tmem_wait_ld();
-      if (j >= 2) mbar_wait(&ds_empty[s], ((j >> 1) & 1) ^ 1);   // dQ MMA of block j-2 read this buffer
-      uint8_t* drw = sdS + s * C::DS_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        uint32_t dk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float dd[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = c8 * 8 + 2 * e + u, kj = j * 64 + c;
-            float p = fast_exp2(__uint_as_float(sv[c]) * sc - L);
-            if (kj > qi || kj >= T_) p = 0.f;
-            dd[u] = p * (__uint_as_float(dv[c]) - Dr);
-          }
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(dd[0], dd[1]);
-          dk[e] = *(uint32_t*)&b2;
-        }
-        *(uint4*)(drw + ((c8 ^ (r & 7)) << 4)) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      fence_before();
-      mbar_arrive(&ds_full[s]);
-    }
-    mbar_wait(&ds_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
-    fence_after();
-    const float isq = rsqrtf((float)DH);
-    bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 16) {
-      uint32_t gq[16];
-      tmem_ld16(la + DQ_COL + c, gq);
-      tmem_wait_ld();
-      if (qi < T_) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          __nv_bfloat162 q2 = __floats2bfloat162_rn(__uint_as_float(gq[2 * i]) * isq, __uint_as_float(gq[2 * i + 1]) * isq);
-          pk[i] = *(uint32_t*)&q2;
-        }
-        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
-  }
-}
-
 // ======================================================================================
 // Backward v2. Same math and block shapes as above, re-organised for the tensor core:
 //   * P^T / dS^T (dK/dV kernel) and dS (dQ kernel) go back into TMEM over the S / dP columns
@@ -1221,12 +600,40 @@ struct BCfg2 {
   static_assert(!TSA || ACC1 + DH <= 512, "TMEM budget");
 };
 
-template <int DH, bool TSA>
+// keep bits of 32 queries (q0 .. q0 + 31) at this lane's key: the mask's 8-key Philox groups run
+// along keys, but here a thread is a key row.  Lane l8 = lane % 8 of an 8-lane group (8 consecutive
+// keys) draws the groups of queries l8, l8 + 8, l8 + 16, l8 + 24 (byte m of w: query l8 + 8 m, bit =
+// key offset); an 8 x 8 bit-matrix transpose per byte across the group's lanes (three xor shuffles)
+// leaves bit c of the result = query q0 + c at this lane's key
+__device__ __forceinline__ uint32_t drop_keep_keyrow(const Drop& dr, uint64_t rowbase, int q0, int T_, int kj) {
+  const int lane = threadIdx.x & 31, l8 = lane & 7;
+  const uint32_t kg = (uint32_t)(kj >> 3);
+  uint32_t w = 0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const uint64_t q = (uint64_t)(q0 + l8 + 8 * m);
+    const uint32_t g = (uint32_t)(((rowbase + q) * (uint64_t)T_ >> 3) + kg);
+    w |= drop_keep8(dr, g) << (8 * m);
+  }
+  const uint32_t lo[3] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu};
+#pragma unroll
+  for (int st = 0; st < 3; ++st) {
+    const int sft = 1 << st;
+    const uint32_t pv = __shfl_xor_sync(0xffffffffu, w, sft);
+    if ((l8 & sft) == 0) w = (w & lo[st]) | ((pv & lo[st]) << sft);
+    else w = (w & ~lo[st]) | ((pv & ~lo[st]) >> sft);
+  }
+  return w;
+}
+
+// DROP: dV += D(P)^T dO and dS^T = P^T (D(dP^T) - D_q) with the forward's mask regenerated
+// (drop_keep_keyrow: the mask's groups run along keys, this kernel's thread is a key row)
+template <int DH, bool TSA, bool DROP>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ qkv,
                          const float* __restrict__ lse, const float* __restrict__ Dsum, bf16* __restrict__ dqkv,
-                         int T_, int h) {
+                         int T_, int h, const Drop drop) {
   using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
@@ -1385,6 +792,8 @@ __global__ void __launch_bounds__(384, 1)
       const bool masked = q0 < k0 + 128;   // block straddles the diagonal
       uint32_t pk[16], dk[16];
       const uint64_t sc2 = f2pack(sc, sc);
+      uint32_t keep = 0xFFFFFFFFu;   // bit c: query q0 + 32 wg + c kept at this key
+      if constexpr (DROP) keep = drop_keep_keyrow(drop, (uint64_t)bh * T_, q0 + 32 * wg, T_, kj);
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         const float4 l4 = *(const float4*)(L + 4 * c4);   // -L
@@ -1408,10 +817,22 @@ __global__ void __launch_bounds__(384, 1)
             }
             p2 = f2pack(p0, p1);
           }
-          const uint64_t ds2 = fmul2(p2, fsub2(f2pack(__uint_as_float(dv[c]), __uint_as_float(dv[c + 1])), d2));
+          float e0 = __uint_as_float(dv[c]), e1 = __uint_as_float(dv[c + 1]);
+          float m0 = 1.f, m1 = 1.f;
+          if constexpr (DROP) {
+            m0 = (keep >> c) & 1u ? drop.scale : 0.f;
+            m1 = (keep >> (c + 1)) & 1u ? drop.scale : 0.f;
+            e0 *= m0;
+            e1 *= m1;
+          }
+          const uint64_t ds2 = fmul2(p2, fsub2(f2pack(e0, e1), d2));
           float p0, p1, g0, g1;
           f2unpack(p2, p0, p1);
           f2unpack(ds2, g0, g1);
+          if constexpr (DROP) {   // dV takes D(P)^T
+            p0 *= m0;
+            p1 *= m1;
+          }
           __nv_bfloat162 a2 = __floats2bfloat162_rn(p0, p1), b2 = __floats2bfloat162_rn(g0, g1);
           pk[2 * c4 + h2] = *(uint32_t*)&a2;
           dk[2 * c4 + h2] = *(uint32_t*)&b2;
@@ -1457,12 +878,13 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int DH, bool TSA>
+// DROP: dS = P (D(dP) - D_row) with the forward's mask regenerated (thread = query row, natural order)
+template <int DH, bool TSA, bool DROP>
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_kv, const bf16* __restrict__ qkv,
                         const bf16* __restrict__ dout, const float* __restrict__ lse,
-                        const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h) {
+                        const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h, const Drop drop) {
   using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   extern __shared__ uint8_t smem_raw[];
@@ -1606,6 +1028,13 @@ __global__ void __launch_bounds__(384, 1)
       const bool masked = j * 64 + 63 > q0 || (j + 1) * 64 > T_;   // diagonal or ragged keys
       uint32_t dk[16];
       const uint64_t sc2 = f2pack(sc, sc), nl2 = f2pack(-L, -L), d2 = f2pack(Dr, Dr);
+      uint32_t keep = 0xFFFFFFFFu;   // bit c: key kbase + c kept
+      if constexpr (DROP) {
+        const uint64_t g0 = ((((uint64_t)bh * T_ + qi) * T_) >> 3) + (uint64_t)kbase / 8;
+        keep = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) keep |= drop_keep8(drop, (uint32_t)(g0 + q)) << (8 * q);
+      }
 #pragma unroll
       for (int c2 = 0; c2 < 16; ++c2) {
         const int c = 2 * c2;
@@ -1623,7 +1052,12 @@ __global__ void __launch_bounds__(384, 1)
           }
           p2 = f2pack(p0, p1);
         }
-        const uint64_t ds2 = fmul2(p2, fsub2(f2pack(__uint_as_float(dv[c]), __uint_as_float(dv[c + 1])), d2));
+        float e0 = __uint_as_float(dv[c]), e1 = __uint_as_float(dv[c + 1]);
+        if constexpr (DROP) {
+          e0 = (keep >> c) & 1u ? e0 * drop.scale : 0.f;
+          e1 = (keep >> (c + 1)) & 1u ? e1 * drop.scale : 0.f;
+        }
+        const uint64_t ds2 = fmul2(p2, fsub2(f2pack(e0, e1), d2));
         float g0, g1;
         f2unpack(ds2, g0, g1);
         __nv_bfloat162 b2 = __floats2bfloat162_rn(g0, g1);
@@ -1721,8 +1155,7 @@ static PFN_encodeTiled encoder() {
 }
 
 template <int DH>
-bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_t st) {
-  using C = Cfg<DH>;
+bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_t st, const Drop& drop) {
   PFN_encodeTiled enc = encoder();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -1740,29 +1173,28 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
     set_error("attention: tensor map encode failed");
     return false;
   }
+  if (drop.thr && T_ % 8) {
+    set_error("tcgen05 attention dropout needs T %% 8 == 0 (8-key Philox groups), T = %d", T_);
+    return false;
+  }
   static bool once = false;
-  static bool v1 = false;   // ATOM_ATTN_FWD_V1=1: the one-tile kernel (A/B comparisons)
   static bool tsa = false;
   if (!once) {
-    const char* e = getenv("ATOM_ATTN_FWD_V1");
-    v1 = e && e[0] == '1';
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Cfg2<DH>::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Cfg2<DH>::SMEM));
+#define ATOM_FWD_ATTR(TS, DR)                                                                                      \
+  ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, TS, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    Cfg2<DH>::SMEM));
+    ATOM_FWD_ATTR(false, false) ATOM_FWD_ATTR(true, false) ATOM_FWD_ATTR(false, true) ATOM_FWD_ATTR(true, true)
+#undef ATOM_FWD_ATTR
     tsa = tsa_mask(0);
     once = true;
   }
-  if (v1) {
-    dim3 grid((T_ + BQ - 1) / BQ, B * h);
-    attn_fwd_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tm, o, lse, T_, h);
-  } else {
-    dim3 grid((T_ + 2 * BQ - 1) / (2 * BQ), B * h);
-    if (tsa) attn_fwd2_tc_kernel<DH, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
-    else attn_fwd2_tc_kernel<DH, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h);
-  }
-  static const std::string name = std::string(v1 ? "attn_fwd_v1<" : "attn_fwd2<") + std::to_string(DH) + ">";
+  dim3 grid((T_ + 2 * BQ - 1) / (2 * BQ), B * h);
+  const bool dr = drop.thr != 0;
+  if (tsa && dr) attn_fwd2_tc_kernel<DH, true, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
+  else if (tsa) attn_fwd2_tc_kernel<DH, true, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
+  else if (dr) attn_fwd2_tc_kernel<DH, false, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
+  else attn_fwd2_tc_kernel<DH, false, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
+  static const std::string name = std::string("attn_fwd2<") + std::to_string(DH) + ">";
   count_launch(name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
@@ -1791,77 +1223,70 @@ static bool make_map2d(CUtensorMap* m, const bf16* base, long cols, long rows, i
 // each fills the SMs the other's causal tail leaves idle), joined back into st
 template <int DH>
 bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B, int T_,
-         int h, cudaStream_t st, cudaStream_t st2) {
-  using C = BCfg<DH>;
+         int h, cudaStream_t st, cudaStream_t st2, const Drop& drop) {
   const long d = (long)h * DH, rows = (long)B * T_;
   CUtensorMap qkv64, qkv128, do64, do128;
   if (!make_map2d(&qkv64, qkv, 3 * d, rows, 64) || !make_map2d(&qkv128, qkv, 3 * d, rows, 128) ||
       !make_map2d(&do64, dout, d, rows, 64) || !make_map2d(&do128, dout, d, rows, 128))
     return false;
+  if (drop.thr && T_ % 8) {
+    set_error("tcgen05 attention dropout needs T %% 8 == 0 (8-key Philox groups), T = %d", T_);
+    return false;
+  }
   static bool once = false;
-  static bool v1 = false;   // ATOM_ATTN_BWD_V1=1: the first-generation kernels (A/B comparisons)
   static bool tsa_kv = false, tsa_q = false;
   if (!once) {
-    const char* e = getenv("ATOM_ATTN_BWD_V1");
-    v1 = e && e[0] == '1';
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      C::SMEM_KV));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      C::SMEM_Q));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      BCfg2<DH>::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv2_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      BCfg2<DH>::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      BCfg2<DH>::SMEM));
-    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq2_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      BCfg2<DH>::SMEM));
+#define ATOM_BWD_ATTR(K, TS, DR)                                                                                   \
+  ATOM_CUDA_OK(cudaFuncSetAttribute(K<DH, TS, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize, BCfg2<DH>::SMEM));
+    ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, false, false) ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, true, false)
+    ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, false, true) ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, true, true)
+    ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, false) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, false)
+    ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, true) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, true)
+#undef ATOM_BWD_ATTR
     tsa_kv = tsa_mask(1);
     tsa_q = tsa_mask(2);
     once = true;
   }
   const long nthr = rows * h;
   dsum_tc_kernel<DH><<<(nthr + 255) / 256, 256, 0, st>>>(o, dout, Dsum, B, T_, h);
-  count_launch();
+  count_launch("attn_dsum");
   dim3 grid((T_ + 127) / 128, B * h);
-  if (v1) {
-    attn_bwd_dkv_tc_kernel<DH><<<grid, 256, C::SMEM_KV, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h);
-    count_launch();
-    attn_bwd_dq_tc_kernel<DH><<<grid, 256, C::SMEM_Q, st>>>(qkv128, do128, qkv64, lse, Dsum, dqkv, T_, h);
-    count_launch();
-  } else {
-    static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (st2 && !ev_fork) {
-      ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
-    if (st2) {   // dQ's inputs (qkv, dO, LSE, D) are ready once dsum has run on st
-      ATOM_CUDA_OK(cudaEventRecord(ev_fork, st));
-      ATOM_CUDA_OK(cudaStreamWaitEvent(st2, ev_fork, 0));
-    }
-    const cudaStream_t sq = st2 ? st2 : st;
-    if (tsa_kv)
-      attn_bwd_dkv2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
-                                                                        T_, h);
-    else
-      attn_bwd_dkv2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv,
-                                                                         T_, h);
-    static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
-    count_launch(nkv.c_str());
-    if (tsa_q)
-      attn_bwd_dq2_kernel<DH, true><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
-                                                                       dqkv, T_, h);
-    else
-      attn_bwd_dq2_kernel<DH, false><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum,
-                                                                        dqkv, T_, h);
-    if (st2) {
-      ATOM_CUDA_OK(cudaGetLastError());
-      ATOM_CUDA_OK(cudaEventRecord(ev_join, st2));
-      ATOM_CUDA_OK(cudaStreamWaitEvent(st, ev_join, 0));
-    }
-    static const std::string nq = "attn_bwd_dq2<" + std::to_string(DH) + ">";
-    count_launch(nq.c_str());
+  // fork / join events of the dQ stream, one pair per device (peers of one process may sit on
+  // different GPUs)
+  static cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
+  int dev = 0;
+  ATOM_CUDA_OK(cudaGetDevice(&dev));
+  if (st2 && dev < 64 && !ev_fork[dev]) {
+    ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_fork[dev], cudaEventDisableTiming));
+    ATOM_CUDA_OK(cudaEventCreateWithFlags(&ev_join[dev], cudaEventDisableTiming));
   }
+  if (dev >= 64) st2 = nullptr;
+  if (st2) {   // dQ's inputs (qkv, dO, LSE, D) are ready once dsum has run on st
+    ATOM_CUDA_OK(cudaEventRecord(ev_fork[dev], st));
+    ATOM_CUDA_OK(cudaStreamWaitEvent(st2, ev_fork[dev], 0));
+  }
+  const cudaStream_t sq = st2 ? st2 : st;
+  const bool dr = drop.thr != 0;
+#define ATOM_DKV(TS, DR) \
+  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, drop)
+#define ATOM_DQ(TS, DR)                                                                                         \
+  attn_bwd_dq2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum, \
+                                                                       dqkv, T_, h, drop)
+  if (tsa_kv) { if (dr) ATOM_DKV(true, true); else ATOM_DKV(true, false); }
+  else { if (dr) ATOM_DKV(false, true); else ATOM_DKV(false, false); }
+  static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
+  count_launch(nkv.c_str());
+  if (tsa_q) { if (dr) ATOM_DQ(true, true); else ATOM_DQ(true, false); }
+  else { if (dr) ATOM_DQ(false, true); else ATOM_DQ(false, false); }
+#undef ATOM_DKV
+#undef ATOM_DQ
+  if (st2) {
+    ATOM_CUDA_OK(cudaGetLastError());
+    ATOM_CUDA_OK(cudaEventRecord(ev_join[dev], st2));
+    ATOM_CUDA_OK(cudaStreamWaitEvent(st, ev_join[dev], 0));
+  }
+  static const std::string nq = "attn_bwd_dq2<" + std::to_string(DH) + ">";
+  count_launch(nq.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }
@@ -1871,21 +1296,21 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
 bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 80 || dh == 128) && ((3 * d) % 8 == 0); }
 
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2) {
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2, Drop drop) {
   switch (dh) {
-    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
-    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
-    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2);
+    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
+    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
+    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
   }
   set_error("tcgen05 attention: unsupported head size %d", dh);
   return false;
 }
 
-bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st) {
+bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st, Drop drop) {
   switch (dh) {
-    case 64: return atc::fwd<64>(qkv, o, lse, B, T_, h, st);
-    case 80: return atc::fwd<80>(qkv, o, lse, B, T_, h, st);
-    case 128: return atc::fwd<128>(qkv, o, lse, B, T_, h, st);
+    case 64: return atc::fwd<64>(qkv, o, lse, B, T_, h, st, drop);
+    case 80: return atc::fwd<80>(qkv, o, lse, B, T_, h, st, drop);
+    case 128: return atc::fwd<128>(qkv, o, lse, B, T_, h, st, drop);
   }
   set_error("tcgen05 attention: unsupported head size %d", dh);
   return false;

@@ -12,22 +12,9 @@
 #include "../../include/atom_kernels.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "philox.cuh"
 
 namespace atom {
-
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-  }
-  return c;
-}
 
 template <typename T> struct Oct;
 template <> struct Oct<float> {
@@ -107,6 +94,59 @@ bool dropout(const T* x, T* y, long n, double p, uint64_t seed, uint32_t site, u
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }
+
+// y <- T(D(y) + r): a residual branch's dropout and the residual add in one pass (the MLP
+// projection's output when dropout is on: minGPT h = x2 + D(fc2(GELU(u))))
+template <typename T>
+__global__ void __launch_bounds__(256) dropout_add_kernel(T* y, const T* r, long n, Drop d) {
+  const long groups = (n + 7) >> 3;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < groups; g += (long)gridDim.x * blockDim.x) {
+    const uint32_t keep = drop_keep8(d, (uint32_t)g);
+    const long i0 = g << 3;
+    float v[8], a[8];
+    if (i0 + 8 <= n) {
+      Oct<T>::load(y + i0, v);
+      Oct<T>::load(r + i0, a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = round_t<T>(((keep >> j) & 1u ? v[j] * d.scale : 0.f) + a[j]);
+      Oct<T>::store(y + i0, v);
+    } else {
+      for (long i = i0; i < n; ++i)
+        y[i] = from_f<T>(((keep >> (i - i0)) & 1u ? to_f(y[i]) * d.scale : 0.f) + to_f(r[i]));
+    }
+  }
+}
+
+template <typename T>
+bool dropout_add(T* y, const T* r, long n, const Drop& d, cudaStream_t st) {
+  if (n <= 0) return true;
+  const long groups = (n + 7) >> 3;
+  long g = (groups + 255) / 256;
+  const int grid = (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+  dropout_add_kernel<T><<<grid, 256, 0, st>>>(y, r, n, d);
+  count_launch("dropout_add");
+  ATOM_CUDA_OK(cudaGetLastError());
+  return true;
+}
+template bool dropout_add<float>(float*, const float*, long, const Drop&, cudaStream_t);
+template bool dropout_add<bf16>(bf16*, const bf16*, long, const Drop&, cudaStream_t);
+
+template <typename T>
+bool dropout(const T* x, T* y, long n, const Drop& d, cudaStream_t st) {
+  if (n <= 0 || d.thr == 0) {
+    if (x != y && n > 0) ATOM_CUDA_OK(cudaMemcpyAsync(y, x, n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    return true;
+  }
+  const long groups = (n + 7) >> 3;
+  long g = (groups + 255) / 256;
+  const int grid = (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+  dropout_kernel<T><<<grid, 256, 0, st>>>(x, y, n, d.thr, d.scale, d.site, d.layer, d.step, d.k0, d.k1);
+  count_launch("dropout");
+  ATOM_CUDA_OK(cudaGetLastError());
+  return true;
+}
+template bool dropout<float>(const float*, float*, long, const Drop&, cudaStream_t);
+template bool dropout<bf16>(const bf16*, bf16*, long, const Drop&, cudaStream_t);
 
 }  // namespace atom
 

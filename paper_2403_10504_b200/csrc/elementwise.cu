@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "philox.cuh"
 #include "planner.h"
 
 namespace atom {
@@ -53,12 +54,13 @@ __device__ __forceinline__ void store_vec(T* p, const float* f) {
 }
 
 // y = LN(x) * g + b; stats[row] = (mean, rstd)                       (minGPT nn.LayerNorm)
-// With res: x <- T(x + res) first (written back; the residual add of the producing GEMM moved here)
+// With res: x <- T(D(x) + res) first (written back; the residual add of the producing GEMM moved
+// here; D = the residual-dropout mask of x's site, identity when drop.thr == 0)
 template <typename T, int NC>
 __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                             const T* __restrict__ b, T* __restrict__ y,
                                                             float* __restrict__ stats, int d,
-                                                            const T* __restrict__ res) {
+                                                            const T* __restrict__ res, Drop drop) {
   constexpr int VW = Vec<T>::N;
   __shared__ float sh[4];
   const long row = blockIdx.x;
@@ -74,6 +76,12 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
       if (res) {
         float r[VW];
         load_vec<T>(res + row * d + ch * VW, r);
+        if (drop.thr) {   // VW consecutive elements of the site tensor from one Philox group (VW <= 8)
+          const uint64_t i0 = (uint64_t)row * d + (uint64_t)ch * VW;
+          const uint32_t keep = drop_keep8(drop, (uint32_t)(i0 >> 3)) >> (i0 & 7);
+#pragma unroll
+          for (int i = 0; i < VW; ++i) v[c][i] = (keep >> i) & 1u ? v[c][i] * drop.scale : 0.f;
+        }
 #pragma unroll
         for (int i = 0; i < VW; ++i) v[c][i] = round_t<T>(v[c][i] + r[i]);
         store_vec<T>(const_cast<T*>(xr) + ch * VW, v[c]);
@@ -686,14 +694,14 @@ static int cs_ranges(long rows, int col_blocks) {
 
 template <typename T>
 bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st,
-            const T* res) {
+            const T* res, Drop drop) {
   if (d % Vec<T>::N || d > LN_THREADS * LN_MAXC * Vec<T>::N) {
     set_error("LayerNorm: d must be a multiple of %d and <= %d", Vec<T>::N, LN_THREADS * LN_MAXC * Vec<T>::N);
     return false;
   }
   switch ((d / Vec<T>::N + LN_THREADS - 1) / LN_THREADS) {   // chunks per thread (same order for any NC)
 #define LN_FWD_CASE(NC) \
-  case NC: ln_fwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d, res); break;
+  case NC: ln_fwd_kernel<T, NC><<<rows, LN_THREADS, 0, st>>>(x, g, b, y, stats, d, res, drop); break;
     LN_FWD_CASE(1) LN_FWD_CASE(2) LN_FWD_CASE(3) LN_FWD_CASE(4) LN_FWD_CASE(5) LN_FWD_CASE(6)
 #undef LN_FWD_CASE
   }
@@ -848,7 +856,7 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
 }
 
 #define INST(T)                                                                                                 \
-  template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t, const T*);                   \
+  template bool ln_fwd<T>(const T*, const T*, const T*, T*, float*, long, int, cudaStream_t, const T*, Drop);                   \
   template bool ln_apply<T>(const T*, const T*, const T*, const float*, T*, long, int, cudaStream_t);           \
   template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, int*, long, \
                           int, cudaStream_t);                                                                   \

@@ -203,27 +203,45 @@ bool gemm(atom_peer* p, int M, int N, int K, const T* A, long lda, bool a_mn, co
   return true;
 }
 
+// attention-probability dropout (site DS_ATTN) runs inside the tcgen05 and SIMT kernels; the
+// mma.sync kernels (d_h = 16) have none: peer creation rejects that combination
 template <typename T>
-bool attn_fwd(atom_peer* p, const T* qkv, T* o, float* lse) {
+bool attn_fwd(atom_peer* p, const T* qkv, T* o, float* lse, const Drop& dr) {
   const ModelDims& dm = p->dm;
   const int dh = dm.d / dm.h;
   if constexpr (std::is_same<T, bf16>::value) {
-    if (attn_tc_supported(dh, dm.d)) return attn_fwd_tc(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
+    if (attn_tc_supported(dh, dm.d)) return attn_fwd_tc(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp, dr);
     if (attn_fa_supported(dh)) return attn_fwd_fa(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
   }
-  return attn_fwd_simt<T>(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp);
+  return attn_fwd_simt<T>(qkv, o, lse, dm.b, dm.T, dm.h, dh, p->s_comp, dr);
 }
 template <typename T>
-bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv) {
+bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv,
+              const Drop& dr) {
   const ModelDims& dm = p->dm;
   const int dh = dm.d / dm.h;
   if constexpr (std::is_same<T, bf16>::value) {
     if (attn_tc_supported(dh, dm.d))
       return attn_bwd_tc(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp,
-                         p->side_wgrad ? p->s_attn : nullptr);
+                         p->side_wgrad ? p->s_attn : nullptr, dr);
     if (attn_fa_supported(dh)) return attn_bwd_fa(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
   }
-  return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
+  return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp, dr);
+}
+
+// one dropout site of micro-batch mb of this step (R38); thr = 0 when the model has none
+Drop mkdrop(const atom_peer* p, uint32_t site, int layer, int mb) {
+  Drop d;
+  const double pr = p->cfg.dropout_p;
+  if (pr <= 0.0) return d;
+  d.thr = (uint32_t)floor(pr * 65536.0);
+  d.scale = (float)(1.0 / (1.0 - pr));
+  d.site = site;
+  d.layer = (uint32_t)layer;
+  d.step = (uint32_t)(p->rng_step * p->C + mb);
+  d.k0 = (uint32_t)p->cfg.dropout_seed;
+  d.k1 = (uint32_t)(p->cfg.dropout_seed >> 32);
+  return d;
 }
 
 Epi epi(int mode, void* out, long ldo) {
@@ -249,24 +267,29 @@ bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
   e.bias = w(T_BQKV);
   PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
-  KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
-  // x2 = x + o W_o^T + b_o: the GEMM stores o W_o^T + b_o (plain epilogue), LN2 adds the residual
-  // (a per-row residual read in the GEMM epilogue held this K = d GEMM well below the others)
+  KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse, mkdrop(p, DS_ATTN, l, mb)));
+  // x2 = x + D(o W_o^T + b_o): the GEMM stores o W_o^T + b_o (plain epilogue), LN2 applies the
+  // residual dropout and adds the residual (a per-row residual read in the GEMM epilogue held this
+  // K = d GEMM well below the others)
   e = epi(EPI_BIAS, s.x2, d);
   e.bias = w(T_BO);
   PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-  KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x));
+  KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x,
+                                 mkdrop(p, DS_RESID_ATTN, l, mb)));
   e = epi(EPI_BIAS_GELU, s.u, 4 * d);
   e.bias = w(T_BFC);
   e.out2 = sc.G;
   e.ldo2 = 4 * d;
   PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)sc.A, d, false, w(T_WFC), d, false, e));
   void* out = (l + 1 < dm.L) ? (void*)stash_view(p, l + 1, mb).x : (void*)hfin_ptr(p, mb);
-  e = epi(EPI_BIAS_RES, out, d);
+  const Drop d3 = mkdrop(p, DS_RESID_MLP, l, mb);
+  e = epi(d3.thr ? EPI_BIAS : EPI_BIAS_RES, out, d);
   e.bias = w(T_BPR);
   e.res = s.x2;
   e.ldr = d;
   PEER_OK(gemm<T>(p, M, d, 4 * d, (const T*)sc.G, 4 * d, false, w(T_WPR), 4 * d, false, e));
+  // with dropout: h = x2 + D(fc2 output) in one pass over the block output
+  if (d3.thr) KT(KC_COLSUM, p->s_comp, dropout_add<T>((T*)out, (const T*)s.x2, M * d, d3, p->s_comp));
   return true;
 }
 
@@ -296,11 +319,12 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
     Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
     e.bias = w(T_BQKV);
     PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
-    KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse));
+    KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse, mkdrop(p, DS_ATTN, l, mb)));
     e = epi(EPI_BIAS, s.x2, d);
     e.bias = w(T_BO);
     PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
-    KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp, (const T*)s.x));
+    KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), ln2, s.st2, M, d, p->s_comp, (const T*)s.x,
+                                   mkdrop(p, DS_RESID_ATTN, l, mb)));
     e = epi(EPI_BIAS_GELU, s.u, 4 * d);   // u and GELU(u) in one pass, as in the forward
     e.bias = w(T_BFC);
     e.out2 = G;
@@ -309,13 +333,22 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   } else {
     KT(KC_GELU, p->s_comp, gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   }
-  // MLP projection: out = GELU(u) W_pr^T + b_pr + x2
-  PEER_OK(gemm<T>(p, d, 4 * d, M, dy, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
-  KT(KC_COLSUM, p->s_comp, bias_grad<T>(dy, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
+  // residual dropout (R38): the projections' branches see the masked gradients
+  // D3(dy) (MLP, in DX2 until LN2's backward rewrites it) and D2(DX2) (attention, in DA until the
+  // QKV data gradient rewrites it); the residual paths keep the unmasked ones
+  const Drop d3 = mkdrop(p, DS_RESID_MLP, l, mb), d2 = mkdrop(p, DS_RESID_ATTN, l, mb);
+  const T* dym = dy;
+  if (d3.thr) {
+    KT(KC_COLSUM, p->s_comp, dropout<T>(dy, (T*)sc.DX2, M * d, d3, p->s_comp));
+    dym = (const T*)sc.DX2;
+  }
+  // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr)
+  PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
+  KT(KC_COLSUM, p->s_comp, bias_grad<T>(dym, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
   // fc pre-activation gradient: (dy W_pr) with a plain-store epilogue, then the GELU derivative
   // and the fc bias gradient in one pass over it (the GEMM epilogue reading u per row was the
   // slow part of the fused form)
-  PEER_OK(gemm<T>(p, M, 4 * d, d, dy, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
+  PEER_OK(gemm<T>(p, M, 4 * d, d, dym, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
   KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
   // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
   // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
@@ -348,22 +381,28 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
   KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
                     p->red_ticket, M, d, p->s_comp));
-  // attention projection: x2 = x + o W_o^T + b_o
+  // attention projection: x2 = x + D2(o W_o^T + b_o)
+  const T* dx2m = (const T*)sc.DX2;
+  if (d2.thr) {
+    KT(KC_COLSUM, p->s_comp, dropout<T>((const T*)sc.DX2, (T*)sc.DA, M * d, d2, p->s_comp));
+    dx2m = (const T*)sc.DA;
+  }
   PEER_OK(fork());
-  PEER_OK(gemm<T>(p, d, d, M, (const T*)sc.DX2, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d),
-                  sd));
+  PEER_OK(gemm<T>(p, d, d, M, dx2m, d, true, (const T*)s.o, d, true, epi(EPI_ACC_F32, g(T_WO), d), sd));
   PEER_OK(mark(2));
-  KT(KC_COLSUM, p->s_comp, bias_grad<T>((const T*)sc.DX2, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
-  PEER_OK(gemm<T>(p, M, d, d, (const T*)sc.DX2, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
+  KT(KC_COLSUM, p->s_comp, bias_grad<T>(dx2m, d, M, d, g(T_BO), p->red, p->red_ticket, p->s_comp));
+  PEER_OK(gemm<T>(p, M, d, d, dx2m, d, false, w(T_WO), d, true, epi(EPI_STORE, sc.DO, d)));
   // attention (writes G, which the fc weight gradient reads)
   if (!rc) PEER_OK(join(1));
-  KT(KC_ATTN_B, p->s_comp, attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G));
+  KT(KC_ATTN_B, p->s_comp, attn_bwd<T>(p, (const T*)s.qkv, (const T*)s.o, (const T*)sc.DO, s.lse, sc.Dsum, G,
+                                       mkdrop(p, DS_ATTN, l, mb)));
   // QKV: qkv = LN1(x) W_qkv^T + b_qkv
   if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), s.st1, ln1, M, d, p->s_comp));
   PEER_OK(fork());
   PEER_OK(gemm<T>(p, 3 * d, d, M, G, 3 * d, true, (const T*)ln1, d, true, epi(EPI_ACC_F32, g(T_WQKV), d), sd));
   PEER_OK(mark(3));
   KT(KC_COLSUM, p->s_comp, bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
+  if (d2.thr) PEER_OK(join(2));   // the side stream's W_o gradient has read D2(DX2) from DA
   PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
   KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
                     p->red, p->red_ticket, M, d, p->s_comp));
@@ -402,13 +441,18 @@ bool embed_forward(atom_peer* p, int mb, const SegView& sv) {
   const T* W = (const T*)sv.W;
   const int32_t* tok = p->tokens + (int64_t)mb * dm.b * (dm.T + 1);
   T* x0 = (T*)stash_view(p, 0, mb).x;
-  return embed_fwd<T>(tok, dm.T + 1, dm.T, dm.M, W + toff(p, 0, T_WTE), W + toff(p, 0, T_WPE), x0, dm.d, p->s_comp);
+  PEER_OK(embed_fwd<T>(tok, dm.T + 1, dm.T, dm.M, W + toff(p, 0, T_WTE), W + toff(p, 0, T_WPE), x0, dm.d, p->s_comp));
+  const Drop d0 = mkdrop(p, DS_EMBD, 0, mb);   // h0 = D(wte[x] + wpe[t])
+  if (d0.thr) PEER_OK(dropout<T>(x0, x0, dm.M * dm.d, d0, p->s_comp));
+  return true;
 }
 template <typename T>
 bool embed_backward(atom_peer* p, int mb, const SegView& sv) {
   const ModelDims& dm = p->dm;
   const int32_t* tok = p->tokens + (int64_t)mb * dm.b * (dm.T + 1);
   const T* dh = (const T*)(p->dh + (int64_t)mb * dm.M * dm.d * dm.wb);
+  const Drop d0 = mkdrop(p, DS_EMBD, 0, mb);   // the embedding sees D(dh0); dh0 is dead after this
+  if (d0.thr) PEER_OK(dropout<T>(dh, (T*)dh, dm.M * dm.d, d0, p->s_comp));
   return embed_bwd<T>(tok, dm.T + 1, dm.T, dm.b, dh, dm.V, dm.d, sv.grad + toff(p, 0, T_WTE),
                       sv.grad + toff(p, 0, T_WPE), p->emb, p->s_comp);
 }
@@ -677,6 +721,7 @@ bool run_step(atom_peer* p, float* loss_out) {
   for (size_t i = 0; i < endq.size(); ++i) nphys[i] = p->slot_phys[endq[i]];
   p->slot_phys = nphys;
   p->steps++;
+  p->rng_step++;
   PEER_CUDA(cudaEventSynchronize(p->ev_loss));
   *loss_out = *p->h_loss;
   if (flush_after) PEER_OK(peer_flush_average(p));

@@ -5,11 +5,20 @@
 #include "adam.h"
 #include "common.cuh"
 #include "epilogue.cuh"
+#include "philox.cuh"
 
 namespace atom {
 
 const char* last_error();
 std::string launch_log_text();
+
+// dropout site multiplier y = D(x) (in place allowed; dropout.cu; R38)
+template <typename T>
+bool dropout(const T* x, T* y, long n, double p, uint64_t seed, uint32_t site, uint32_t layer, uint32_t step,
+             cudaStream_t st);
+template <typename T> bool dropout(const T* x, T* y, long n, const Drop& d, cudaStream_t st);
+// y <- T(D(y) + r) (a residual branch's dropout fused with the residual add)
+template <typename T> bool dropout_add(T* y, const T* r, long n, const Drop& d, cudaStream_t st);
 
 // GEMM: D[m,n] = sum_k A[m,k] B[n,k] + epilogue.  *_mn = operand stored MN-major ([K][ld]).
 bool gemm_tc(int M, int N, int K, const bf16* A, long lda, bool a_mn, const bf16* B, long ldb, bool b_mn,
@@ -19,9 +28,10 @@ bool gemm_simt(int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
                cudaStream_t st);
 
 // elementwise / reductions (elementwise.cu)
-// res != NULL: x <- T(x + res) in place first (a producing GEMM's residual add, moved here)
+// res != NULL: x <- T(D(x) + res) in place first (a producing GEMM's residual add, moved here; D the
+// residual-dropout mask of x's site, the identity when drop.thr == 0)
 template <typename T> bool ln_fwd(const T* x, const T* g, const T* b, T* y, float* stats, long rows, int d, cudaStream_t st,
-                                  const T* res = nullptr);
+                                  const T* res = nullptr, Drop drop = Drop());
 template <typename T> bool ln_apply(const T* x, const T* g, const T* b, const float* stats, T* y, long rows, int d, cudaStream_t st);
 // part: fp32 range partials (at most 2 x ceil(rows / RED_ROWS) x d for ln_bwd); ticket: CS_TICKETS zeroed
 // ints, one per block of 64 x (16 / sizeof(T)) columns, returned to zero by the kernel
@@ -47,17 +57,21 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st);
 
 // attention (attn_simt.cu: fp32/bf16 CUDA cores; attn_fa.cu: bf16 tensor cores)
 // qkv [B*T, 3d] rows (b,t): [q | k | v], head j at columns j*dh; o [B*T, d]; lse [B, h, T]
-template <typename T> bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
+// drop: attention-probability dropout (site DS_ATTN; element index ((b h + head) T + q) T + k);
+// the softmax normaliser and LSE use the undropped probabilities
+template <typename T> bool attn_fwd_simt(const T* qkv, T* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st,
+                                         Drop drop = Drop());
 template <typename T> bool attn_bwd_simt(const T* qkv, const T* o, const T* dout, const float* lse, float* Dsum, T* dqkv,
-                                         int B, int T_, int h, int dh, cudaStream_t st);
+                                         int B, int T_, int h, int dh, cudaStream_t st, Drop drop = Drop());
 bool attn_fwd_fa(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
 bool attn_bwd_fa(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
                  int T_, int h, int dh, cudaStream_t st);
 bool attn_fa_supported(int dh);
 // tcgen05 / TMEM forward (attn_tc.cu)
 bool attn_tc_supported(int dh, int d);
-bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st);
+bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st,
+                 Drop drop = Drop());
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2 = nullptr);
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2 = nullptr, Drop drop = Drop());
 
 }  // namespace atom

@@ -87,6 +87,7 @@ struct atom_peer {
   std::vector<atom::Op> ops, ops_sync;
   std::vector<int> endq, endq_sync;
   int64_t t = 0;                        // optimizer step count
+  int64_t rng_step = 0;                 // atom_step calls so far (dropout micro_step = rng_step * C + mb)
   bool sync_next = false;
   bool poisoned = false;
 

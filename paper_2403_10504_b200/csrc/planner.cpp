@@ -34,12 +34,17 @@ bool make_dims(const atom_model_cfg& c, ModelDims* o) {
     set_error("invalid config: dtype");
     return false;
   }
+  if (c.op_nodes != 0 && c.op_nodes != 1) {
+    set_error("invalid config: op_nodes must be 0 or 1");
+    return false;
+  }
   ModelDims& m = *o;
   m.L = c.n_layer; m.d = c.d_model; m.h = c.n_head; m.T = c.seq_len; m.V = c.vocab; m.b = c.micro_batch;
+  m.op = c.op_nodes;
   m.M = (int64_t)m.b * m.T;
   m.dtype = c.dtype;
   m.wb = c.dtype == ATOM_FP32 ? 4 : 2;
-  m.n_nodes = m.L + 2;
+  m.n_nodes = (m.op ? 2 : 1) * m.L + 2;
   const int64_t d = m.d, V = m.V, T = m.T;
   auto mk = [](std::initializer_list<int64_t> sizes) {
     std::vector<TensorSlot> v;
@@ -53,8 +58,14 @@ bool make_dims(const atom_model_cfg& c, ModelDims* o) {
   };
   m.tensors.clear();
   m.tensors.push_back(mk({V * d, T * d}));
-  for (int l = 0; l < m.L; ++l)
-    m.tensors.push_back(mk({d, d, 3 * d * d, 3 * d, d * d, d, d, d, 4 * d * d, 4 * d, 4 * d * d, d}));
+  for (int l = 0; l < m.L; ++l) {
+    if (m.op) {   // attention half, MLP half (the canonical block order split in two)
+      m.tensors.push_back(mk({d, d, 3 * d * d, 3 * d, d * d, d}));
+      m.tensors.push_back(mk({d, d, 4 * d * d, 4 * d, 4 * d * d, d}));
+    } else {
+      m.tensors.push_back(mk({d, d, 3 * d * d, 3 * d, d * d, d, d, d, 4 * d * d, 4 * d, 4 * d * d, d}));
+    }
+  }
   m.tensors.push_back(mk({d, d, V * d}));
   m.P.clear(); m.P_canon.clear(); m.node_off.clear(); m.node_canon.clear();
   int64_t off = 0, canon = 0;
@@ -84,18 +95,22 @@ Costs node_costs(const atom_model_cfg& c, const ModelDims& dm, int64_t link_bw) 
   const i128 d = dm.d, V = dm.V, T = dm.T, b = dm.b, M = dm.M;
   const int64_t d2h = c.d2h_bw > 0 ? c.d2h_bw : link_bw;
   for (int i = 0; i < n; ++i) {
+    // forward FLOPs per micro-batch: block 24 d^2 M + attention; operator-granular halves
+    // 8 d^2 M + attention (QKV, attention, projection) and 16 d^2 M (fc, fc2)
+    const bool blk = is_block_node(dm, i);
+    const int half = blk ? node_half(dm, i) : 0;
+    const i128 fattn = 2 * d * T * (T + 1) * b;
     i128 ff = 0;
-    if (i >= 1 && i <= dm.L) ff = 24 * d * d * M + 2 * d * T * (T + 1) * b;
-    if (i == dm.L + 1) ff = 2 * d * V * M;
+    if (blk) ff = half == 0 ? 24 * d * d * M + fattn : (half == 1 ? 8 * d * d * M + fattn : 16 * d * d * M);
+    if (i == n - 1) ff = 2 * d * V * M;
     k.ff.push_back((int64_t)ff);
-    const bool blk = i >= 1 && i <= dm.L;
     if (c.cost_table) {
       k.tf.push_back(c.cost_table[2 * i]);
       k.tb.push_back(c.cost_table[2 * i + 1]);
       k.tbr.push_back(k.tb.back() + (blk ? k.tf.back() : 0));
     } else {
       // re-forward inside the backward: QKV, proj and fc GEMMs + attention (not the MLP projection)
-      const i128 fr = blk ? 16 * d * d * M + 2 * d * T * (T + 1) * b : 0;
+      const i128 fr = !blk ? 0 : (half == 0 ? 16 * d * d * M + fattn : (half == 1 ? 8 * d * d * M + fattn : 8 * d * d * M));
       k.tf.push_back(ceil_ns(ff, c.peak_flops));
       k.tb.push_back(ceil_ns(2 * ff, c.peak_flops));
       k.tbr.push_back(ceil_ns(2 * ff + fr, c.peak_flops));
@@ -164,7 +179,8 @@ struct Eval {
       for (size_t i = 0; i < v.size(); ++i) p[i + 1] = p[i] + v[i];
     };
     std::vector<int64_t> tbx(k.tb);
-    for (int v = 1; v <= std::min(R, dm.L); ++v) tbx[v] = k.tbr[v];
+    if (!dm.op)
+      for (int v = 1; v <= std::min(R, dm.L); ++v) tbx[v] = k.tbr[v];
     pre(k.P, pP); pre(k.tf, ptf); pre(k.tb, ptb); pre(tbx, ptbx); pre(k.tlf, ptlf); pre(k.tlb, ptlb);
     pre(k.tmv, ptmv); pre(k.ts, pts);
   }
@@ -172,7 +188,13 @@ struct Eval {
   // backward time of a segment that is not the last one (its re-forwarded blocks included)
   int64_t tbn(int i, int j) const { return s(ptbx, i, j); }
   int64_t need(int i, int j) const { return seg_need(dm, s(pP, i, j)); }
+  // whole blocks inside nodes [i..j] (operator-granular: both halves inside)
   int nblocks(int i, int j) const {
+    if (dm.op) {
+      int nb = 0;
+      for (int l = 0; l < dm.L; ++l) nb += (i <= 2 * l + 1 && 2 * l + 2 <= j) ? 1 : 0;
+      return nb;
+    }
     int lo = std::max(i, 1), hi = std::min(j, dm.L);
     return std::max(0, hi - lo + 1);
   }
@@ -507,7 +529,11 @@ bool check_plan(const atom_model_cfg& c, const atom_plan_t& p) {
   const int S = p.n_seg;
   const int il = S == 1 ? 0 : ends[S - 2] + 1;
   {
-    const int nb_last = std::max(0, dm.L - std::max(il, 1) + 1);   // blocks of the last segment
+    int nb_last = std::max(0, dm.L - std::max(il, 1) + 1);   // blocks of the last segment
+    if (dm.op) {
+      nb_last = 0;
+      for (int l = 0; l < dm.L; ++l) nb_last += il <= 2 * l + 1 ? 1 : 0;
+    }
     const int nb_pre = dm.L - nb_last;
     const int r = p.n_recompute;
     const int want = r == 0 ? ATOM_ACT_STASH : (r == nb_pre ? ATOM_ACT_RECOMPUTE : ATOM_ACT_HYBRID);
@@ -560,10 +586,17 @@ bool make_plan(const atom_model_cfg& c, int64_t budget, int64_t link, atom_plan_
   // re-forward counts R to try: ACT_AUTO the fewest (0 = full stash, ..., L = every block before
   // the last segment), each over C ascending (R35)
   std::vector<int> pols;
-  if (c.act_policy == ATOM_ACT_AUTO)
+  if (dm.op) {   // operator-granular graph: the full stash only (R40)
+    if (c.act_policy != ATOM_ACT_AUTO && c.act_policy != ATOM_ACT_STASH) {
+      set_error("invalid config: op_nodes plans use the full activation stash (act_policy AUTO or STASH)");
+      return false;
+    }
+    pols = {0};
+  } else if (c.act_policy == ATOM_ACT_AUTO) {
     for (int r = 0; r <= dm.L; ++r) pols.push_back(r);
-  else
+  } else {
     pols = {c.act_policy == ATOM_ACT_STASH ? 0 : (c.act_policy == ATOM_ACT_RECOMPUTE ? dm.L : c.n_recompute)};
+  }
   for (int pol : pols) {
     Eval ev(c, dm, budget, link, pol);
     for (int C = c_lo; C <= c_hi; ++C) {

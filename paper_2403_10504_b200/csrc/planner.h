@@ -29,6 +29,7 @@ enum HTensor { T_LNFG, T_LNFB, T_WLM };
 
 struct ModelDims {
   int L, d, h, T, V, b;
+  int op = 0;  // operator-granular nodes: block l = attention half 2l+1 + MLP half 2l+2 (atom_model_cfg.op_nodes)
   int64_t M;  // b*T
   int dtype;  // ATOM_FP32 / ATOM_BF16
   int wb;     // bytes per compute-dtype element (4 / 2)
@@ -41,6 +42,15 @@ struct ModelDims {
   int64_t N_pad = 0, N_canon = 0;
 };
 bool make_dims(const atom_model_cfg& c, ModelDims* out);
+// node of block l's half (0 = attention: LN1 .. b_o, 1 = MLP: LN2 .. b_pr) and the index of block
+// tensor t (BlockTensor) inside that node
+inline int blk_node(const ModelDims& m, int l, int half) { return m.op ? 1 + 2 * l + half : 1 + l; }
+inline int blk_tensor_node(const ModelDims& m, int l, int t) { return blk_node(m, l, t >= T_LN2G ? 1 : 0); }
+inline int blk_tensor_idx(const ModelDims& m, int t) { return m.op && t >= T_LN2G ? t - T_LN2G : t; }
+inline bool is_block_node(const ModelDims& m, int i) { return i >= 1 && i <= m.n_nodes - 2; }
+inline int node_block(const ModelDims& m, int i) { return m.op ? (i - 1) / 2 : i - 1; }
+// 0 = whole block, 1 = attention half, 2 = MLP half (block nodes only)
+inline int node_half(const ModelDims& m, int i) { return m.op ? 1 + (i - 1) % 2 : 0; }
 
 struct Costs {
   std::vector<int64_t> P, tf, tb, tlf, tlb, tmv, ts;

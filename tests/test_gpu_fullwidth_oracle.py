@@ -89,6 +89,30 @@ def test_wide_step_gradient_elementwise(wide_step):
             print(f"grad err {k}: elem {v[0]:.3e} relL2 {v[1]:.3e}")
 
 
+def test_wide_step_with_dropout_matches_oracle():
+    """The same full-width step with dropout p = 0.1 at every minGPT site (R38): the
+    d_h = 80 tcgen05 forward, dQ and dK/dV kernels regenerate the attention mask; oracle = per
+    micro-batch Philox streams averaged over the micro-batches."""
+    p_drop, seed = 0.1, 99
+    cfg = atom.make_cfg(WIDE, dtype=atom.BF16, C_=C, overlap_check=0, forced_ends=ENDS, lr=LR, beta1=B1,
+                        warmup_steps=0, dropout_p=p_drop, dropout_seed=seed)
+    plan = atom.atom_plan(cfg, 10 ** 12, 10 ** 10)
+    init = synth.init_params(WIDE, seed=1234, perturb=True)
+    toks = synth.tokens(WIDE, C * WIDE.micro_batch, synth.step_seed(0, 0))
+    peer = atom.Peer(cfg, plan, init_params=init)
+    loss = peer.step(toks)
+    g = peer.params()["m"] / (1.0 - B1)
+    peer.destroy()
+    b = WIDE.micro_batch
+    ref_loss, g_ref = 0.0, 0.0
+    for mb in range(C):
+        lo, gr = ogpt.loss_and_grad(WIDE, init.astype(np.float64), toks[mb * b:(mb + 1) * b],
+                                    drop=ogpt.Dropout(p_drop, seed, micro_step=mb))
+        ref_loss, g_ref = ref_loss + lo / C, g_ref + gr / C
+    assert abs(loss - ref_loss) <= 5e-4 * abs(ref_loss), (loss, ref_loss)
+    check_bf16_gradient(g, g_ref, WIDE)
+
+
 def test_wide_step_gradient_as_accurate_as_torch_bf16(wide_step):
     ours = gradient_errors(wide_step["g"], wide_step["g_ref"], WIDE)
     torch_bf16 = gradient_errors(wide_step["g_torch"], wide_step["g_ref"], WIDE)

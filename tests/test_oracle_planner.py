@@ -242,3 +242,80 @@ def test_full_stash_2p7b_needs_more_link_than_pcie():
     assert pl.Evaluator(c, 178 * 10 ** 9, 50 * 10 ** 9, q.n_recompute - 1).violation(q.C, q.seg_end) is not None
     assert pl.dp_plan(dataclasses.replace(c, act_policy=pl.ACT_HYBRID, n_recompute=q.n_recompute - 1),
                       178 * 10 ** 9, 50 * 10 ** 9) is None
+
+
+# ---------------------------------------------------------------------------------------------
+# Operator-granular graph ("a node ... is a layer or an operator"; reading R40): every block
+# is an attention-half node and an MLP-half node, so sub-models may end inside a block.
+def test_operator_granular_dp_equals_brute_force():
+    """The exact DP over half-block nodes equals brute force over all 2^(n-1) partitions x C
+    (n = 2L + 2 <= 16 nodes)."""
+    rng = random.Random(17)
+    found = split = 0
+    for trial in range(220):
+        c = _rand_plan_cfg(rng)
+        c.n_layer = min(c.n_layer, 6)
+        c.op_nodes = 1
+        c.act_policy = rng.choice([pl.ACT_AUTO, pl.ACT_STASH])
+        n = 2 * c.n_layer + 2
+        if c.cost_table is not None:
+            tf = [0] + [rng.randint(1, 400) for _ in range(n - 1)]
+            c.cost_table = sum(([t, 2 * t + rng.randint(0, 50)] for t in tf), [])
+        link = rng.choice([10 ** 9, 10 ** 10, 3 * 10 ** 10])
+        hi = pl.Evaluator(c, 10 ** 18, link).device_bytes(1, [n - 1])
+        budget = rng.randint(pl.work_bytes(c, 1), int(hi * 1.3))
+        a = pl.brute_force_plan(c, budget, link)
+        b = pl.dp_plan(c, budget, link)
+        if a is None:
+            assert b is None, trial
+            continue
+        found += 1
+        assert a == b, (trial, a, b)
+        split += any(e % 2 == 1 and 1 <= e < n - 1 for e in a.seg_end)
+    assert found > 40 and split > 8, (found, split)
+
+
+def test_operator_granular_halves_partition_the_block():
+    """Half nodes split each block's parameters and FLOPs exactly (the canonical tensor order cut
+    after b_o); a plan that cuts only between blocks has the block graph's arena, bytes and FLOPs."""
+    for g in (synth.CONFIGS["tiny"], synth.CONFIGS["2.7b"]):
+        cb = pl.PlanCfg.from_gpt(g)
+        co = pl.PlanCfg.from_gpt(g, op_nodes=1)
+        pb, po = pl.node_params(cb), pl.node_params(co)
+        assert len(po) == 2 * g.n_layer + 2 and pb[0] == po[0] and pb[-1] == po[-1]
+        assert all(pb[1 + l] == po[1 + 2 * l] + po[2 + 2 * l] for l in range(g.n_layer))
+        fb, fo = pl.node_flops_fwd(cb), pl.node_flops_fwd(co)
+        assert all(fb[1 + l] == fo[1 + 2 * l] + fo[2 + 2 * l] for l in range(g.n_layer))
+        d, M = g.d_model, g.micro_batch * g.seq_len
+        assert fo[2] == 16 * d * d * M                              # fc + fc2
+        L = g.n_layer
+        for ends_b in ([L + 1], [0, L + 1], [1, L // 2, L + 1], [L, L + 1]):
+            ends_o = [0 if e == 0 else (2 * e if e <= L else 2 * L + 1) for e in ends_b]
+            ends_o = sorted(set(ends_o))
+            evb, evo = pl.Evaluator(cb, 10 ** 18, 10 ** 10), pl.Evaluator(co, 10 ** 18, 10 ** 10)
+            assert evb.device_bytes(2, ends_b) == evo.device_bytes(2, ends_o), (g.name, ends_b)
+            a, b = evb.make_plan(2, ends_b), evo.make_plan(2, ends_o)
+            for f in ("cut_bytes", "r1_bytes", "slot_bytes", "stash_bytes", "work_bytes", "pred_h2d_B",
+                      "pred_d2h_B", "pred_flops"):
+                assert getattr(a, f) == getattr(b, f), (g.name, ends_b, f)
+
+
+def test_operator_granular_mid_block_cut_can_be_the_optimum():
+    """Under a model-state cap the half-block graph finds plans the block graph cannot: a slot only
+    has to hold the largest swapped sub-model, which a mid-block cut makes smaller (the
+    objective P:399, S:174 then prefers the fewest sub-models)."""
+    g = synth.CONFIGS["tiny"]
+    n = 2 * g.n_layer + 2
+    feasible_only_split = fewer_with_split = 0
+    for k in range(60):
+        cap = 2_000_000 + 50_000 * k
+        po = pl.plan(pl.PlanCfg.from_gpt(g, op_nodes=1, C=1, overlap_check=0, state_budget=cap), 10 ** 12, 10 ** 10)
+        pb = pl.plan(pl.PlanCfg.from_gpt(g, C=1, overlap_check=0, state_budget=cap), 10 ** 12, 10 ** 10)
+        if po is None:
+            assert pb is None, cap            # the half-block graph contains every block-graph plan
+            continue
+        assert pb is None or po.n_seg <= pb.n_seg, cap
+        mid = any(e % 2 == 1 and 1 <= e < n - 1 for e in po.seg_end)
+        feasible_only_split += mid and pb is None
+        fewer_with_split += mid and pb is not None and po.n_seg < pb.n_seg
+    assert feasible_only_split > 0 and fewer_with_split > 0, (feasible_only_split, fewer_with_split)

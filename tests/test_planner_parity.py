@@ -18,7 +18,7 @@ def _both(c: pl.PlanCfg, budget, link):
     ac = atom.make_cfg(g, dtype=c.dtype, C_=c.C, max_C=c.max_C, overlap_check=c.overlap_check,
                        peak_flops=c.peak_flops, d2h_bw=c.d2h_bw, state_budget=c.state_budget,
                        cost_table=c.cost_table, forced_ends=c.forced_ends, act_policy=c.act_policy,
-                       n_recompute=c.n_recompute, grad_rounds=c.grad_rounds)
+                       n_recompute=c.n_recompute, grad_rounds=c.grad_rounds, op_nodes=c.op_nodes)
     want = pl.plan(c, budget, link)
     try:
         got = atom.atom_plan(ac, budget, link)
@@ -66,6 +66,45 @@ def test_random_configs_bit_exact():
             _same(want, got)
             found += 1
     assert found > 150
+
+
+def test_random_configs_operator_granular_bit_exact():
+    """Operator-granular graphs (a node per block half, cuts may fall inside a block; reading R40)."""
+    rng = random.Random(23)
+    found = split = 0
+    for _ in range(300):
+        L = rng.randint(1, 7)
+        c = pl.PlanCfg(n_layer=L, d_model=64 * rng.randint(1, 4), n_head=rng.choice([1, 2, 4]),
+                       seq_len=rng.choice([16, 32, 64]), vocab=rng.choice([64, 300, 1001]),
+                       micro_batch=rng.randint(1, 3), dtype=rng.choice([pl.FP32, pl.BF16]),
+                       max_C=rng.randint(1, 12), overlap_check=rng.choice([0, 1, 1, 1]), op_nodes=1,
+                       act_policy=rng.choice([pl.ACT_AUTO, pl.ACT_STASH]))
+        n = 2 * L + 2
+        if rng.random() < 0.6:
+            tf = [0] + [rng.randint(1, 10 ** 6) for _ in range(n - 1)]
+            c.cost_table = sum(([t, 2 * t + rng.randint(0, 10 ** 5)] for t in tf), [])
+        else:
+            c.peak_flops = rng.choice([10 ** 9, 10 ** 10, 10 ** 12])
+        if rng.random() < 0.4:
+            c.state_budget = rng.randint(10 ** 4, 10 ** 8)
+        c.grad_rounds = rng.choice([0, 0, 1, 3])
+        link = rng.choice([10 ** 8, 10 ** 9, 10 ** 10])
+        hi = pl.Evaluator(c, 10 ** 18, link).device_bytes(1, [n - 1])
+        budget = rng.randint(hi // 4, int(hi * 1.5))
+        want, got = _both(c, budget, link)
+        if want is not None:
+            _same(want, got)
+            found += 1
+            split += any(e % 2 == 1 and 1 <= e < n - 1 for e in want.seg_end)   # ends after an attention half
+    assert found > 100 and split > 10, (found, split)
+
+
+def test_operator_granular_rejects_reforward():
+    g = synth.CONFIGS["tiny"]
+    for pol in (atom.ACT_RECOMPUTE, atom.ACT_HYBRID):
+        with pytest.raises(atom.AtomError) as e:
+            atom.atom_plan(atom.make_cfg(g, op_nodes=1, act_policy=pol, n_recompute=1), 10 ** 10, 10 ** 9)
+        assert e.value.code == atom.ATOM_E_INVALID
 
 
 @pytest.mark.parametrize("name,frac,link", [("xl", 2, 50 * 10 ** 9), ("xl", 3, 60 * 10 ** 9),
