@@ -299,6 +299,10 @@ def main():
                     help="compute rate the planner's cost model assumes (default: measured by a profile run)")
     ap.add_argument("--grad-rounds", type=int, default=0,
                     help="host update placement (P:563 CPU AdamW): gradient rounds per update (0 = GPU AdamW every step)")
+    ap.add_argument("--op-nodes", action="store_true",
+                    help="operator-granular graph: sub-models may end between a block's attention and MLP halves "
+                         "(P:332; DESIGN.md R40)")
+    ap.add_argument("--dropout", type=float, default=0.0, help="minGPT dropout p at every site (DESIGN.md R38)")
     ap.add_argument("--no-profile", action="store_true",
                     help="plan with the measured bf16 peak instead of a profiled compute rate")
     args = ap.parse_args()
@@ -335,8 +339,10 @@ def main():
     # peer averaging cadence from a global batch of 512 sequences (reading R17)
     plan_tf = args.planner_tflops or pk["bf16_tflops"]
     forced = FORCED.get(args.config, {})
+    extra = dict(op_nodes=int(args.op_nodes), dropout_p=args.dropout, dropout_seed=7)
     cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(plan_tf * 1e12),
-                        state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds, **forced)
+                        state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds, **forced,
+                        **extra)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
     profiled = None
     if not args.planner_tflops and not args.no_profile and not forced:
@@ -372,7 +378,7 @@ def main():
         link_bw = int(min(rates[1], args.link_gbs * 1e9))
         cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(rates[0]), state_budget=state_cap,
                             lr=1e-4, warmup_steps=3000, cost_table=table or None,
-                            d2h_bw=int(min(rates[2], args.link_gbs * 1e9)), grad_rounds=args.grad_rounds)
+                            d2h_bw=int(min(rates[2], args.link_gbs * 1e9)), grad_rounds=args.grad_rounds, **extra)
         plan = atom.atom_plan(cfg, hbm_budget, link_bw)
     tok_step = plan.C * g.micro_batch * g.seq_len
     cfg.sync_every = adist.sync_every(world, plan.C, g.micro_batch)     # global batch 512
@@ -450,6 +456,10 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_desc, "model": g.name, "global_batch": world * n_seq, "seq_len": g.seq_len,
                        "micro_batch": g.micro_batch, "C": plan.C, "sub_models": plan.ends(),
+                       "graph": ("operator-granular (node 2l+1 = attention half, 2l+2 = MLP half of block l)"
+                                 if args.op_nodes else "block nodes"),
+                       "mid_block_cuts": ([e for e in plan.ends()[:-1] if e % 2 == 1] if args.op_nodes else []),
+                       "dropout_p": args.dropout,
                        "act_policy": {0: "auto", 1: "stash", 2: "recompute", 3: "hybrid"}.get(plan.act_policy),
                        "n_recompute": plan.n_recompute,
                        "planner_tflops": plan_tf, "profile": profiled,

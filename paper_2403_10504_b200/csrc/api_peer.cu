@@ -87,11 +87,6 @@ atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan,
     delete p;
     return ATOM_E_INVALID;
   }
-  if (cfg->op_nodes) {
-    set_error("atom_peer_create: operator-granular plans are not executable yet");
-    delete p;
-    return ATOM_E_INVALID;
-  }
   if (cfg->dropout_p != 0.f) {
     // DESIGN.md R38: masks are drawn per 8-element Philox group of each site tensor (T % 8 keeps the
     // attention rows whole groups), the group index is one 32-bit counter word, and the bf16
@@ -130,9 +125,11 @@ atom_status atom_peer_create(const atom_model_cfg* cfg, const atom_plan_t* plan,
     p->seg_off.push_back(dm.node_off[lo]);
     lo = hi + 1;
   }
-  for (int i = p->seg_lo[p->S - 1]; i <= p->seg_hi[p->S - 1]; ++i)
-    if (i >= 1 && i <= dm.L) {
-      if (p->l0_last < 0) p->l0_last = i - 1;
+  // whole blocks of the last segment (operator-granular: both halves in it); the first of them
+  // reads its input from the C-deep boundary buffer
+  for (int l = 0; l < dm.L; ++l)
+    if (blk_node(dm, l, 0) >= p->seg_lo[p->S - 1]) {
+      if (p->l0_last < 0) p->l0_last = l;
       p->nb_last++;
     }
   if (!peer_create(p, init_params, seed, nccl_id)) {

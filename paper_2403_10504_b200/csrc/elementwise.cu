@@ -479,6 +479,17 @@ __global__ void __launch_bounds__(CE_THREADS, 2) ce_bf16_kernel(bf16* __restrict
   }
 }
 
+// guarded averaging commit (R36): dst <- src only when the flag reduced over all ranks is 1
+__global__ void commit_if_kernel(float* __restrict__ dst, const float* __restrict__ src, long n,
+                                 const int* __restrict__ flag) {
+  if (*flag != 1) return;
+  const long n4 = n >> 2;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x)
+    reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+  for (long i = (n4 << 2) + blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 // h0[row] = wte[x] + wpe[t]   (P:295, P:307 embedding in sub-model 1)
 template <typename T>
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, long tstride, int T_, const T* __restrict__ wte,
@@ -774,6 +785,16 @@ bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, i
   LAUNCH_OK();
   return true;
 }
+bool commit_if(float* dst, const float* src, long n, const int* flag, cudaStream_t st) {
+  if (((uintptr_t)dst | (uintptr_t)src) & 15) {
+    set_error("commit_if: 16-byte aligned buffers required");
+    return false;
+  }
+  commit_if_kernel<<<grid_for(n / 4 + 1), 256, 0, st>>>(dst, src, n, flag);
+  LAUNCH_OK();
+  return true;
+}
+
 template <typename T>
 bool cross_entropy(T* logits, long ld, int V, const int32_t* targets, long tstride, int T_, long rows, float scale,
                    float* loss, cudaStream_t st) {

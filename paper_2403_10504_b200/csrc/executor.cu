@@ -65,6 +65,11 @@ int64_t toff(const atom_peer* p, int node, int tensor) {
   const int k = p->seg_of_node[node];
   return p->dm.node_off[node] - p->seg_off[k - 1] + p->dm.tensors[node][tensor].off;
 }
+// block l's tensor t (BlockTensor) inside the sub-arrays of the segment holding it: the block's
+// node, or (operator-granular graph, R40) the node of the half it belongs to
+int64_t btoff(const atom_peer* p, int l, int t) {
+  return toff(p, blk_tensor_node(p->dm, l, t), blk_tensor_idx(p->dm, t));
+}
 
 struct StashView {
   uint8_t *x, *qkv, *o, *x2, *u;
@@ -72,7 +77,7 @@ struct StashView {
 };
 StashView stash_view(const atom_peer* p, int l, int mb) {
   const ModelDims& dm = p->dm;
-  const int k = p->seg_of_node[l + 1];
+  const int k = p->seg_of_node[blk_node(dm, l, 0)];   // both halves in the last segment: one entry
   const int64_t ab = dm.wb, M = dm.M, d = dm.d;
   StashView s;
   uint8_t* b;
@@ -252,19 +257,23 @@ Epi epi(int mode, void* out, long ldo) {
   return e;
 }
 
-// forward of block l on micro-batch mb (minGPT Block)
+// forward of block l on micro-batch mb (minGPT Block).  part 0: the whole block; in the
+// operator-granular graph (R40) the attention half (part 1: LN1, QKV, attention, output projection
+// into the stash's x2) and the MLP half (part 2: LN2 with the residual, fc, GELU, fc2) are separate
+// nodes, possibly of different sub-models (the stash entry carries x and x2 between them)
 template <typename T>
-bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
+bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   const ModelDims& dm = p->dm;
-  const int node = l + 1;
   const long M = dm.M, d = dm.d;
   const T* W = (const T*)sv.W;
-  auto w = [&](int t) { return W + toff(p, node, t); };
+  auto w = [&](int t) { return W + btoff(p, l, t); };
   StashView s = stash_view(p, l, mb);
   Scratch sc = scratch_view(p);
   T* x = (T*)s.x;
+  Epi e;
+  if (part != 2) {
   KT(KC_LN, p->s_comp, ln_fwd<T>(x, w(T_LN1G), w(T_LN1B), (T*)sc.A, s.st1, M, d, p->s_comp));
-  Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
+  e = epi(EPI_BIAS, s.qkv, 3 * d);
   e.bias = w(T_BQKV);
   PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
   KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse, mkdrop(p, DS_ATTN, l, mb)));
@@ -274,6 +283,8 @@ bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   e = epi(EPI_BIAS, s.x2, d);
   e.bias = w(T_BO);
   PEER_OK(gemm<T>(p, M, d, d, (const T*)s.o, d, false, w(T_WO), d, false, e));
+  }
+  if (part == 1) return true;
   KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), (T*)sc.A, s.st2, M, d, p->s_comp, x,
                                  mkdrop(p, DS_RESID_ATTN, l, mb)));
   e = epi(EPI_BIAS_GELU, s.u, 4 * d);
@@ -293,24 +304,53 @@ bool fwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   return true;
 }
 
-// backward of block l on micro-batch mb: dh[mb] (grad of the block output) -> dh[mb] (grad of its input)
+// backward of block l on micro-batch mb: dh[mb] (grad of the block output) -> dh[mb] (grad of its input).
+// part 0: the whole block; operator-granular graph (R40): part 2 = the MLP half (up to LN2's
+// backward, which yields DX2 = dL/dx2), then part 1 = the attention half.  When the halves sit in
+// different sub-models (their backward ops run at different times) DX2 travels in dh[mb] (LN2's
+// backward writes it over dy in place, LN1's backward writes dL/dx over it in place) and each half
+// drains the side stream that read its scratch buffers before it returns.
 template <typename T>
-bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
+bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   const ModelDims& dm = p->dm;
-  const int node = l + 1;
   const long M = dm.M, d = dm.d;
   const T* W = (const T*)sv.W;
-  auto w = [&](int t) { return W + toff(p, node, t); };
-  auto g = [&](int t) { return sv.grad + toff(p, node, t); };
+  auto w = [&](int t) { return W + btoff(p, l, t); };
+  auto g = [&](int t) { return sv.grad + btoff(p, l, t); };
   StashView s = stash_view(p, l, mb);
   Scratch sc = scratch_view(p);
   T* dy = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
   T* G = (T*)sc.G;
-  const bool rc = !p->blk_full[l];
+  const bool rc = !p->blk_full[l];   // never in the operator-granular graph (stash only)
+  const bool split = part != 0 && p->seg_of_node[blk_node(dm, l, 0)] != p->seg_of_node[blk_node(dm, l, 1)];
+  T* dx2 = split ? dy : (T*)sc.DX2;   // dL/dx2 from LN2's backward to the attention half
   // LN outputs the weight gradients read: re-applied from the stash, or (recompute) kept from the
   // re-run forward -- LN1(x) in A, LN2(x2) in DA (free until the fc data-gradient GEMM)
   T* ln1 = (T*)sc.A;
   T* ln2 = rc ? (T*)sc.DA : (T*)sc.A;
+  const Drop d3 = mkdrop(p, DS_RESID_MLP, l, mb), d2 = mkdrop(p, DS_RESID_ATTN, l, mb);
+  // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
+  // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
+  // LN2 output (A under stash) is rewritten by LN1's re-apply after the attention backward, which
+  // also rewrites G; WO reads DX2 / o, WQKV reads G / A; the next block rewrites G, A, DX2.
+  const bool side = p->side_wgrad;
+  const cudaStream_t sd = side ? p->s_side : p->s_comp;
+  auto fork = [&]() -> bool {
+    if (side) {
+      PEER_CUDA(cudaEventRecord(p->ev_side[0], p->s_comp));
+      PEER_CUDA(cudaStreamWaitEvent(p->s_side, p->ev_side[0], 0));
+    }
+    return true;
+  };
+  auto mark = [&](int i) -> bool {
+    if (side) PEER_CUDA(cudaEventRecord(p->ev_side[i], p->s_side));
+    return true;
+  };
+  auto join = [&](int i) -> bool {
+    if (side) PEER_CUDA(cudaStreamWaitEvent(p->s_comp, p->ev_side[i], 0));
+    return true;
+  };
+  if (part != 1) {
   if (rc) {
     // ACT_RECOMPUTE: re-run the block forward from its input checkpoint into the shared entry
     // (same kernels and inputs as the forward: bit-identical tensors); the MLP projection's
@@ -336,7 +376,6 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   // residual dropout (R38): the projections' branches see the masked gradients
   // D3(dy) (MLP, in DX2 until LN2's backward rewrites it) and D2(DX2) (attention, in DA until the
   // QKV data gradient rewrites it); the residual paths keep the unmasked ones
-  const Drop d3 = mkdrop(p, DS_RESID_MLP, l, mb), d2 = mkdrop(p, DS_RESID_ATTN, l, mb);
   const T* dym = dy;
   if (d3.thr) {
     KT(KC_COLSUM, p->s_comp, dropout<T>(dy, (T*)sc.DX2, M * d, d3, p->s_comp));
@@ -350,27 +389,6 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   // slow part of the fused form)
   PEER_OK(gemm<T>(p, M, 4 * d, d, dym, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
   KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
-  // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
-  // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
-  // LN2 output (A under stash) is rewritten by LN1's re-apply after the attention backward, which
-  // also rewrites G; WO reads DX2 / o, WQKV reads G / A; the next block rewrites G, A, DX2.
-  const bool side = p->side_wgrad;
-  const cudaStream_t sd = side ? p->s_side : p->s_comp;
-  auto fork = [&]() -> bool {
-    if (side) {
-      PEER_CUDA(cudaEventRecord(p->ev_side[0], p->s_comp));
-      PEER_CUDA(cudaStreamWaitEvent(p->s_side, p->ev_side[0], 0));
-    }
-    return true;
-  };
-  auto mark = [&](int i) -> bool {
-    if (side) PEER_CUDA(cudaEventRecord(p->ev_side[i], p->s_side));
-    return true;
-  };
-  auto join = [&](int i) -> bool {
-    if (side) PEER_CUDA(cudaStreamWaitEvent(p->s_comp, p->ev_side[i], 0));
-    return true;
-  };
   // MLP fc: u = LN2(x2) W_fc^T + b_fc (under recompute LN2's output is DA, rewritten just below:
   // that gradient stays on the main stream)
   if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
@@ -379,12 +397,16 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
                   rc ? p->s_comp : sd));
   if (!rc) PEER_OK(mark(1));
   PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
-  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, (T*)sc.DX2, g(T_LN2G), g(T_LN2B), p->red,
+  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, dx2, g(T_LN2G), g(T_LN2B), p->red,
                     p->red_ticket, M, d, p->s_comp));
+  // the attention half runs in another op: the W_fc gradient has read G / LN2's output by then
+  if (split) PEER_OK(join(1));
+  }
+  if (part == 2) return true;
   // attention projection: x2 = x + D2(o W_o^T + b_o)
-  const T* dx2m = (const T*)sc.DX2;
+  const T* dx2m = dx2;
   if (d2.thr) {
-    KT(KC_COLSUM, p->s_comp, dropout<T>((const T*)sc.DX2, (T*)sc.DA, M * d, d2, p->s_comp));
+    KT(KC_COLSUM, p->s_comp, dropout<T>((const T*)dx2, (T*)sc.DA, M * d, d2, p->s_comp));
     dx2m = (const T*)sc.DA;
   }
   PEER_OK(fork());
@@ -404,7 +426,8 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
   KT(KC_COLSUM, p->s_comp, bias_grad<T>(G, 3 * d, M, 3 * d, g(T_BQKV), p->red, p->red_ticket, p->s_comp));
   if (d2.thr) PEER_OK(join(2));   // the side stream's W_o gradient has read D2(DX2) from DA
   PEER_OK(gemm<T>(p, M, d, 3 * d, G, 3 * d, false, w(T_WQKV), d, true, epi(EPI_STORE, sc.DA, d)));
-  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)sc.DX2, dy, g(T_LN1G), g(T_LN1B),
+  if (split && !d2.thr) PEER_OK(join(2));   // W_o's gradient has read DX2 from dh[mb], rewritten next
+  KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)dx2, dy, g(T_LN1G), g(T_LN1B),
                     p->red, p->red_ticket, M, d, p->s_comp));
   // the side stream is in order: its last mark covers WO and WQKV (and WFC)
   PEER_OK(join(3));
@@ -415,7 +438,7 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv) {
 template <typename T>
 bool head(atom_peer* p, int mb, const SegView& sv) {
   const ModelDims& dm = p->dm;
-  const int node = dm.L + 1;
+  const int node = dm.n_nodes - 1;
   const long M = dm.M, d = dm.d, V = dm.V, Vp = al(dm.V, 8);
   const T* W = (const T*)sv.W;
   auto w = [&](int t) { return W + toff(p, node, t); };
@@ -478,8 +501,8 @@ bool run_fwd(atom_peer* p, int k, int mb, const SegView& sv) {
     if (cast) PEER_OK(cast_node<T>(p, k, node, sv));
     if (node == 0)
       KT(KC_EMBED, p->s_comp, embed_forward<T>(p, mb, sv));
-    else if (node <= p->dm.L)
-      PEER_OK(fwd_block<T>(p, node - 1, mb, sv));
+    else if (is_block_node(p->dm, node))
+      PEER_OK(fwd_block<T>(p, node_block(p->dm, node), mb, sv, node_half(p->dm, node)));
     else
       PEER_OK(head<T>(p, mb, sv));
   }
@@ -494,8 +517,8 @@ bool run_bwd(atom_peer* p, int k, int mb, const SegView& sv) {
     if (cast) PEER_OK(cast_node<T>(p, k, node, sv));
     if (node == 0)
       KT(KC_EMBED, p->s_comp, embed_backward<T>(p, mb, sv));
-    else if (node <= p->dm.L)
-      PEER_OK(bwd_block<T>(p, node - 1, mb, sv));
+    else if (is_block_node(p->dm, node))
+      PEER_OK(bwd_block<T>(p, node_block(p->dm, node), mb, sv, node_half(p->dm, node)));
     // the head's backward ran inside its forward op
   }
   return true;
@@ -614,12 +637,22 @@ bool issue_op(atom_peer* p, const Op& o, bool sync, int idx) {
       break;
     }
     case K_AVG:
+      // guarded averaging (R36): the mean of the masters goes out of place into the segment's fp32
+      // gradient buffer (free after ADAM); a one-int allreduce (min) of every rank's "arrived" flag
+      // follows, and the average replaces the master only if it reads 1.  A peer that dies inside
+      // the round never contributes its flag: when the survivors abort the communicator
+      // (atom_comm_shrink with abort_ops) the flag stays 0 on every survivor and each keeps its own
+      // updated master for that round -- consistent, never a partial reduction.
       if (p->nranks > 1 && !hu) {
-        ncclResult_t r = ncclAllReduce(sv.master, sv.master, (size_t)P, ncclFloat32, ncclAvg, p->comm, st);
+        int* flag = p->avg_flags + k;
+        PEER_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+        ncclResult_t r = ncclAllReduce(sv.master, sv.grad, (size_t)P, ncclFloat32, ncclAvg, p->comm, st);
+        if (r == ncclSuccess) r = ncclAllReduce(p->avg_flags, flag, 1, ncclInt32, ncclMin, p->comm, st);
         if (r != ncclSuccess) {
           set_error("ncclAllReduce failed: %s", ncclGetErrorString(r));
           return false;
         }
+        PEER_OK(commit_if(sv.master, sv.grad, P, flag, st));
       }
       break;
     case K_RECAST:
@@ -744,11 +777,12 @@ static float init_std(const atom_peer* p, int node, int t, float* fill) {
   const ModelDims& dm = p->dm;
   *fill = 0.f;
   if (node == 0) return 0.02f;
-  if (node == dm.L + 1) {
+  if (node == dm.n_nodes - 1) {
     if (t == T_LNFG) { *fill = 1.f; return 0.f; }
     if (t == T_LNFB) return 0.f;
     return 0.02f;
   }
+  if (node_half(dm, node) == 2) t += T_LN2G;   // operator-granular MLP half: tensors from ln2.g on
   switch (t) {
     case T_LN1G: case T_LN2G: *fill = 1.f; return 0.f;
     case T_WQKV: case T_WFC: return 0.02f;
@@ -821,7 +855,7 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   // blocks 1..n_recompute (never the last segment's) are re-forwarded: input checkpoints only
   bool any_rc = false;
   for (int l = 0; l < dm.L; ++l) {
-    const bool last = p->seg_of_node[l + 1] == p->S;
+    const bool last = p->seg_of_node[blk_node(dm, l, 0)] == p->S;   // both halves in the last segment
     const bool rc = !last && l < p->n_recompute;
     any_rc |= rc;
     p->blk_off.push_back(off);
@@ -898,6 +932,11 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
       set_error("ncclCommInitRank failed: %s", ncclGetErrorString(r));
       return false;
     }
+  }
+  {   // guarded-averaging flags: [0] = 1 (this rank's contribution), [k] per segment
+    PEER_CUDA(cudaMalloc((void**)&p->avg_flags, sizeof(int) * (p->S + 1)));
+    std::vector<int> ones(p->S + 1, 1);
+    PEER_CUDA(cudaMemcpy(p->avg_flags, ones.data(), sizeof(int) * (p->S + 1), cudaMemcpyHostToDevice));
   }
   p->ops = emit_schedule(p->S, p->C, false, &p->endq);
   p->ops_sync = emit_schedule(p->S, p->C, true, &p->endq_sync);
@@ -1003,15 +1042,20 @@ bool peer_comm_reset(atom_peer* p, const void* nccl_id, int nranks, int rank) {
 }
 
 // failed / leaving ranks dropped from the communicator without a new bootstrap (ncclCommShrink)
+// abort_ops: a peer may have died inside an averaging round, leaving this peer's averaging stuck
+// on the comm stream (and the copies / compute that wait for it): the outstanding operations are
+// aborted first (NCCL_SHRINK_ABORT, or ncclCommAbort for a sole survivor), which releases the
+// streams; the guarded commit (K_AVG) then keeps the local master for the unfinished round
 bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abort_ops) {
-  PEER_OK(peer_stream_sync(p));
-  if (!p->comm || n_exclude == 0) return true;
+  PEER_CUDA(cudaSetDevice(p->device));
+  if (!abort_ops) PEER_OK(peer_stream_sync(p));
+  if (!p->comm || n_exclude == 0) return peer_stream_sync(p);
   if (p->nranks - n_exclude <= 1) {   // sole survivor: nothing left to shrink to, no NCCL call
     ncclCommAbort(p->comm);
     p->comm = nullptr;
     p->nranks = 1;
     p->rank = 0;
-    return true;
+    return peer_stream_sync(p);
   }
   ncclComm_t nc = nullptr;
   std::vector<int> ex(exclude, exclude + n_exclude);
@@ -1021,6 +1065,7 @@ bool peer_comm_shrink(atom_peer* p, const int* exclude, int n_exclude, bool abor
     set_error("ncclCommShrink failed: %s", ncclGetErrorString(r));
     return false;
   }
+  if (abort_ops) PEER_OK(peer_stream_sync(p));   // the aborted operations have released the streams
   ncclCommAbort(p->comm);   // the parent may still reference dead ranks: abort, not destroy
   p->comm = nc;
   int n = 1, rk = 0;
@@ -1258,6 +1303,7 @@ void peer_free(atom_peer* p) {
   for (cudaStream_t s : {p->s_comp, p->s_h2d, p->s_d2h, p->s_comm, p->s_side, p->s_attn, p->s_cpu})
     if (s) cudaStreamSynchronize(s);
   if (p->comm) ncclCommDestroy(p->comm);
+  if (p->avg_flags) cudaFree(p->avg_flags);
   for (auto ev : p->ev_side)
     if (ev) cudaEventDestroy(ev);
   for (auto ev : p->node_ev)

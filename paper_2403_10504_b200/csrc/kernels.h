@@ -54,6 +54,8 @@ template <typename T> bool adamw(float* p, const float* g, float* m, float* v, T
 template <typename T> bool cast_params(const float* src, T* dst, long n, cudaStream_t st);
 bool init_normal(float* dst, long n, uint64_t seed, uint64_t base, float std, float fill, cudaStream_t st);
 bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st);
+// dst <- src (n fp32) iff *flag == 1 (the guarded averaging commit, R36)
+bool commit_if(float* dst, const float* src, long n, const int* flag, cudaStream_t st);
 
 // attention (attn_simt.cu: fp32/bf16 CUDA cores; attn_fa.cu: bf16 tensor cores)
 // qkv [B*T, 3d] rows (b,t): [q | k | v], head j at columns j*dh; o [B*T, d]; lse [B, h, T]

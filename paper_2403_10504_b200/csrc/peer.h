@@ -80,6 +80,10 @@ struct atom_peer {
   cudaEvent_t ev_loss = nullptr;
 
   // ---- NCCL ----
+  // guarded averaging (R36): per segment an "all arrived" flag (int, min over ranks) reduced after
+  // the master's out-of-place average; the commit copies the average over the master only when
+  // every rank's allreduce of that segment completed
+  int* avg_flags = nullptr;             // device: [0] = 1 (this rank's contribution), [1 + k - 1] per segment
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
 

@@ -94,7 +94,7 @@ bool profile_from_trace(const char* trace, const atom_model_cfg& cfg, const atom
   if (!parse_trace(trace, &ops)) return false;
   memset(out, 0, sizeof(*out));
   const int L = cfg.n_layer, S = plan.n_seg;
-  out->n_nodes = L + 2;
+  out->n_nodes = (cfg.op_nodes ? 2 * L : L) + 2;
   const double busy = compute_busy_us(ops);
   out->compute_busy_ms = busy / 1000.0;
   out->executed_flops = executed_flops(cfg, plan);
@@ -138,7 +138,10 @@ bool profile_from_trace(const char* trace, const atom_model_cfg& cfg, const atom
     nb += nblk[k];
     nr += nrc[k];
   }
-  if (nb == 0) return true;   // no table: the caller keeps the single measured rate
+  // no table: the plan has no blocks-only sub-model, or the graph is operator-granular (R40: its
+  // halves would need per-half op times the per-sub-model trace does not separate); the caller
+  // keeps the measured rates
+  if (nb == 0 || cfg.op_nodes) return true;
   const double tf_b = sf / nb;
   const double tb_b = (sb - tf_b * nr) / nb;
   double f1 = 0, b1 = 0, fS = 0;

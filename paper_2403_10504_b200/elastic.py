@@ -240,7 +240,10 @@ class Coordinator:
             peer.comm_reset(bytes.fromhex(d.nccl_id), len(d.members), d.members.index(self.pid))
             peer.broadcast_state(d.members.index(d.leader), self.pid in d.joiners)
         elif d.dead:
-            peer.comm_shrink([d.prev.index(m) for m in d.dead])
+            # the dead peer may have left this peer's averaging round waiting inside the device
+            # stream: abort the outstanding operations, then shrink (the guarded commit keeps the
+            # local master for a round that did not complete on every rank, R36)
+            peer.comm_shrink([d.prev.index(m) for m in d.dead], abort_ops=True)
         if d.sync and atom_sync is not None and len(d.members) > 1:
             atom_sync([peer], flush=False)
 

@@ -154,3 +154,105 @@ def test_failure_shrink_join_and_averaging():
     # survivors and the joiner finished every step
     for pid in [p for p in pids if p != victim]:
         assert json.loads(logs[pid]["decs"][-1])["s"] == STEPS - 1
+
+
+# ---------------------------------------------------------------------------------------------
+# A peer dies INSIDE an averaging round (PAPER P:563 kills GPUs mid-training):
+# with every step a sync step, peer 1 issues a step and exits while that step's backward -- whose
+# fused per-sub-model averaging waits for it -- is still running.  The survivor's averaging is
+# stuck on its comm stream; the coordinator declares peer 1 dead after its TTL and the survivor
+# shrinks with abort_ops (atom_comm_shrink): the outstanding NCCL operations are aborted, the
+# streams drain, and the guarded commit (R36) leaves each sub-model's master either
+# averaged (its round completed on both ranks before the failure) or the survivor's own update --
+# never a partial reduction.  Checked against the fp64 oracle replaying each of those outcomes.
+A_STEPS, A_KILL, A_TTL = 6, 3, 3.0
+
+
+def _avg_peer(pid, port, q):
+    import torch
+    import torch.distributed as dist
+    store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=datetime.timedelta(seconds=300))
+    torch.cuda.set_device(pid)
+    import synth
+    from paper_2403_10504_b200 import atom, elastic
+    g = synth.CONFIGS["tiny"]
+    C = 2
+    cfg = atom.make_cfg(g, dtype=atom.FP32, C_=C, overlap_check=0, forced_ends=[2, 5], lr=1e-3, warmup_steps=0,
+                        sync_every=1)
+    plan = atom.atom_plan(cfg, 10 ** 11, 10 ** 10)
+    init = synth.init_params(g, seed=1234, perturb=True)
+    if pid == 0:
+        store.set("nccl_avg", atom.atom_nccl_unique_id().hex())
+    nid = bytes.fromhex(store.get("nccl_avg").decode())
+    peer = atom.Peer(cfg, plan, device=pid, init_params=init, seed=0, nccl_id=nid, nranks=2, rank=pid)
+    co = elastic.Coordinator(store, pid, 10 ** 9, ttl=A_TTL, make_id=atom.atom_nccl_unique_id)
+    co.start([0, 1])
+    decs = []
+    for s in range(A_STEPS):
+        peer.step(synth.tokens(g, C * g.micro_batch, synth.step_seed(pid, s)))
+        if pid == 1 and s == A_KILL:
+            os._exit(0)    # the step's backward (with its averaging rounds) is still in flight
+        d = co.after_step(C * g.micro_batch)
+        co.apply(d, peer, atom.atom_sync)
+        decs.append(d.to_json())
+    master = peer.params()["master"]
+    peer.destroy()
+    q.put((pid, decs, master.tobytes()))
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_failure_inside_averaging_round_is_recovered():
+    import itertools
+
+    import numpy as np
+    import torch.distributed as dist
+
+    import synth
+    from oracle import adamw, gpt, peers
+    port = _free_port()
+    server = dist.TCPStore("127.0.0.1", port, is_master=True, wait_for_workers=False,
+                           timeout=datetime.timedelta(seconds=300))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_avg_peer, args=(pid, port, q)) for pid in range(2)]
+    for p in procs:
+        p.start()
+    pid, decs, mbytes = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+    del server
+    assert pid == 0
+    decs = [json.loads(d) for d in decs]
+    assert [d["s"] for d in decs] == list(range(A_STEPS))
+    assert decs[A_KILL]["dead"] == [1] and decs[-1]["members"] == [0]
+    got = np.frombuffer(mbytes, dtype=np.float32)
+    # oracle: both peers average after every update up to step A_KILL - 1; at step A_KILL each of
+    # the two sub-models is either averaged or keeps peer 0's update; then peer 0 trains alone
+    g = synth.CONFIGS["tiny"]
+    C = 2
+    h = adamw.AdamWHyper(lr=1e-3, warmup_steps=0)
+    init = synth.init_params(g, seed=1234, perturb=True).astype(np.float64)
+    prs = [peers.Peer(g, init, h) for _ in range(2)]
+    for s in range(A_KILL + 1):
+        for r in range(2):
+            prs[r].step(synth.tokens(g, C * g.micro_batch, synth.step_seed(r, s)))
+        if s < A_KILL:
+            mean = peers.average([pr.p for pr in prs])
+            for pr in prs:
+                pr.p = mean.copy()
+    nodes = gpt.node_ranges(g)
+    segs = [(nodes[0][0], nodes[2][1]), (nodes[3][0], nodes[5][1])]     # sub-models [E B0 B1 | B2 B3 H]
+    mean = peers.average([pr.p for pr in prs])
+    matched = []
+    for choice in itertools.product([0, 1], repeat=2):   # 1 = that sub-model's round committed
+        pr = peers.Peer(g, prs[0].p, h)
+        pr.p, pr.m, pr.v, pr.t = prs[0].p.copy(), prs[0].m.copy(), prs[0].v.copy(), prs[0].t
+        for (a, b), c in zip(segs, choice):
+            if c:
+                pr.p[a:b] = mean[a:b]
+        for s in range(A_KILL + 1, A_STEPS):
+            pr.step(synth.tokens(g, C * g.micro_batch, synth.step_seed(0, s)))
+        err = np.linalg.norm(got - pr.p) / np.linalg.norm(pr.p)
+        if err <= 1e-5:
+            matched.append(choice)
+    assert len(matched) == 1, matched
