@@ -340,9 +340,12 @@ def main():
     plan_tf = args.planner_tflops or pk["bf16_tflops"]
     forced = FORCED.get(args.config, {})
     extra = dict(op_nodes=int(args.op_nodes), dropout_p=args.dropout, dropout_seed=7)
+    # the profile run always uses the block graph (its plan may need the re-forward, which the
+    # half-block graph does not offer, R40); --op-nodes re-plans the half-block graph afterwards
+    first = dict(extra, op_nodes=0) if not args.planner_tflops and not args.no_profile and not forced else extra
     cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(plan_tf * 1e12),
                         state_budget=state_cap, lr=1e-4, warmup_steps=3000, grad_rounds=args.grad_rounds, **forced,
-                        **extra)
+                        **first)
     plan = atom.atom_plan(cfg, hbm_budget, int(args.link_gbs * 1e9))
     profiled = None
     if not args.planner_tflops and not args.no_profile and not forced:
@@ -376,8 +379,10 @@ def main():
                                       if table else None)}
         plan_tf = rates[0] / 1e12
         link_bw = int(min(rates[1], args.link_gbs * 1e9))
+        # the measured per-block cost table fits the block graph; the half-block graph plans with the
+        # measured rates (R40)
         cfg = atom.make_cfg(g, dtype=atom.BF16, max_C=32, peak_flops=int(rates[0]), state_budget=state_cap,
-                            lr=1e-4, warmup_steps=3000, cost_table=table or None,
+                            lr=1e-4, warmup_steps=3000, cost_table=(table or None) if not args.op_nodes else None,
                             d2h_bw=int(min(rates[2], args.link_gbs * 1e9)), grad_rounds=args.grad_rounds, **extra)
         plan = atom.atom_plan(cfg, hbm_budget, link_bw)
     tok_step = plan.C * g.micro_batch * g.seq_len

@@ -33,11 +33,13 @@ int atom_k_gemm(int impl, int dtype, int M, int N, int K, const void* A, long ld
 
 /* Causal attention (minGPT CausalSelfAttention).  qkv: [B*T, 3*h*dh] rows (b, t) =
  * [q | k | v], head j at columns j*dh; o: [B*T, h*dh]; lse: fp32 [B, h, T] (natural log of the
- * softmax normaliser of scores q.k/sqrt(dh)).  impl: ATOM_ATTN_TC (tcgen05/TMEM forward, dh in
- * {64, 80, 128}; backward = the mma.sync kernels), ATOM_ATTN_MMA (mma.sync flash attention, dh in
+ * softmax normaliser of scores q.k/sqrt(dh)).  impl: ATOM_ATTN_TC (tcgen05/TMEM, dh in {64, 80, 128};
+ * the backward's dQ kernel recomputes S and dP), ATOM_ATTN_TC_DS (backward only: the dK/dV kernel
+ * writes dS^T to a temporary [B h][T][T] bf16 buffer and dQ = dS K runs over it -- the step's
+ * path when T % 64 == 0), ATOM_ATTN_MMA (mma.sync flash attention, dh in
  * {16, 64, 80, 128}), ATOM_ATTN_SIMT (CUDA cores, dh <= 128).  dtype ATOM_FP32 always uses SIMT.
  * Backward: dout [B*T, h*dh] -> dqkv [B*T, 3*h*dh]; dsum fp32 [B, h, T] is scratch (rowsum(dout*o)). */
-enum { ATOM_ATTN_TC = 0, ATOM_ATTN_MMA = 1, ATOM_ATTN_SIMT = 2 };
+enum { ATOM_ATTN_TC = 0, ATOM_ATTN_MMA = 1, ATOM_ATTN_SIMT = 2, ATOM_ATTN_TC_DS = 3 };
 int atom_k_attn_fwd(int impl, int dtype, const void* qkv, void* o, float* lse, int B, int T, int h, int dh,
                     void* stream);
 int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const void* dout, const float* lse,

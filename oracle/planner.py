@@ -313,7 +313,9 @@ RED_ROWS = 128   # rows per partial-sum chunk in the deterministic column reduct
 def work_bytes(c: PlanCfg, C: int) -> int:
     """Working set: token buffer, boundary-gradient buffer (all C micro-batches),
     per-token losses, max(block-backward scratch, head scratch), reduction
-    partials, embedding-backward counting-sort scratch, small scalars."""
+    partials, embedding-backward counting-sort scratch, small scalars.  The block-backward
+    scratch of the bf16 path includes the attention backward's dS^T [b, h, T, T] (written by
+    the dK/dV kernel, read by the dQ kernel)."""
     ab = wbytes(c)
     d, V, T, b, h = c.d_model, c.vocab, c.seq_len, c.micro_batch, c.n_head
     M = b * T
@@ -322,6 +324,8 @@ def work_bytes(c: PlanCfg, C: int) -> int:
     dh = al256(ab * C * M * d)
     losses = al256(4 * C * M)
     bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4 * b * h * T)
+    if c.dtype == BF16:   # the attention backward's dS^T [b, h, T, T] (bf16) between its dK/dV and dQ kernels
+        bwd_s += al256(2 * b * h * T * T)
     head_s = al256(ab * M * Vp) + 2 * al256(ab * M * d) + al256(8 * M)
     scratch = max(bwd_s, head_s)
     red = al256(4 * ceil_div(M, RED_ROWS) * 4 * d)

@@ -393,7 +393,7 @@ def atom_sync(peers, flush=False):
     check(lib.atom_sync(arr, len(peers), int(flush)))
 
 
-ATTN_TC, ATTN_MMA, ATTN_SIMT = 0, 1, 2
+ATTN_TC, ATTN_MMA, ATTN_SIMT, ATTN_TC_DS = 0, 1, 2, 3
 lib.atom_k_attn_fwd.restype = C.c_int
 lib.atom_k_attn_fwd.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.c_void_p]

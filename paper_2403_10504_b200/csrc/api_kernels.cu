@@ -55,6 +55,17 @@ int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const v
                               h, dh, st);
   else if (impl == ATOM_ATTN_TC)
     ok = attn_bwd_tc((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);
+  else if (impl == ATOM_ATTN_TC_DS) {
+    bf16* dsT = nullptr;
+    if (cudaMalloc((void**)&dsT, (size_t)B * h * T * T * sizeof(bf16)) != cudaSuccess) {
+      set_error("CUDA: dS^T buffer allocation failed");
+      return ATOM_E_CUDA;
+    }
+    ok = attn_bwd_tc((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st,
+                     nullptr, Drop(), dsT);
+    cudaStreamSynchronize(st);
+    cudaFree(dsT);
+  }
   else if (impl == ATOM_ATTN_MMA)
     ok = attn_bwd_fa((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);
   else

@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ qkv,
                          const float* __restrict__ lse, const float* __restrict__ Dsum, bf16* __restrict__ dqkv,
-                         int T_, int h, const Drop drop) {
+                         int T_, int h, const Drop drop, bf16* __restrict__ dsT) {
   using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
@@ -837,6 +837,13 @@ __global__ void __launch_bounds__(384, 1)
           pk[2 * c4 + h2] = *(uint32_t*)&a2;
           dk[2 * c4 + h2] = *(uint32_t*)&b2;
         }
+      }
+      if (dsT && kj < T_) {   // dS^T row of this key, 32 queries (64 contiguous bytes) for the dQ kernel
+        uint4* dst = (uint4*)(dsT + ((long)bh * T_ + kj) * T_ + q0 + 32 * wg);
+        dst[0] = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+        dst[1] = make_uint4(dk[4], dk[5], dk[6], dk[7]);
+        dst[2] = make_uint4(dk[8], dk[9], dk[10], dk[11]);
+        dst[3] = make_uint4(dk[12], dk[13], dk[14], dk[15]);
       }
       named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
       tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
@@ -1107,6 +1114,128 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// dQ = dS K from the dS^T the dK/dV kernel wrote (no recomputation of S and dP): one CTA per
+// (b, h, 128-query block), key blocks of 64 up to the diagonal (entries above it are exact zeros:
+// the dK/dV kernel masked P there).  A = dS [M = 128 queries, K = 64 keys] read MN-major from the
+// dS^T rows (queries contiguous), B = K_j [N = d_h, K = 64 keys] MN-major, D in TMEM.
+//   warp 0 TMA (dS^T box pair + K tile per stage), warp 1 MMA, warp 2 TMEM, warps 4-7 epilogue.
+// Two CTAs per SM: the second CTA's stream of tiles covers the first one's prologue / epilogue.
+constexpr int DQ_NST = 3;
+template <int DH>
+struct DqCfg {
+  static constexpr int NP = (DH + 63) / 64;
+  static constexpr int A_BYTES = 2 * 64 * 128;      // 128 queries x 64 keys, two 64-query panels
+  static constexpr int B_BYTES = NP * 64 * 128;     // 64 keys x d_h
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int SMEM = DQ_NST * STAGE + 1024 + 256;
+  static constexpr uint32_t TCOLS = DH <= 64 ? 64 : 128;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(256, 2)
+    attn_bwd_dq_ds_kernel(const __grid_constant__ CUtensorMap tm_ds, const __grid_constant__ CUtensorMap tm_kv,
+                          bf16* __restrict__ dqkv, int T_, int h) {
+  using C = DqCfg<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = (uint64_t*)(sm + DQ_NST * C::STAGE);
+  uint64_t* full = bars;               // [NST]
+  uint64_t* empty = bars + DQ_NST;     // [NST]
+  uint64_t* done = bars + 2 * DQ_NST;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (T_ + 127) / 128;
+  const int qb = nqb - 1 - blockIdx.x;   // heavy (late) query blocks first
+  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int d = h * DH;
+  const int q0 = qb * 128;
+  const int nblk = min((q0 + 127) / 64 + 1, (T_ + 63) / 64);
+  const int row0 = b * T_;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DQ_NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j % DQ_NST;
+        mbar_wait(&empty[s], ((j / DQ_NST) & 1) ^ 1);
+        uint8_t* a = sm + s * C::STAGE;
+        uint8_t* k = a + C::A_BYTES;
+        mbar_expect_tx(&full[s], C::STAGE);
+        // dS^T rows j*64 .. +63 (keys) of this (b, h), queries q0 .. q0 + 127 as two 64-wide boxes
+        tma_load(a, &tm_ds, &full[s], q0, bh * T_ + j * 64);
+        tma_load(a + 64 * 128, &tm_ds, &full[s], q0 + 64, bh * T_ + j * 64);
+        for (int p = 0; p < C::NP; ++p) tma_load(k + p * 64 * 128, &tm_kv, &full[s], d + hh * DH + 64 * p, row0 + j * 64);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_q = idesc_bf16(128, DH, true, true);   // dQ += dS K (A and B MN-major)
+    const bool elected = elect_one();
+    const uint64_t da0 = desc_sw128(smem_u32(sm), 64 * 128, 1024);
+    const uint64_t db0 = desc_sw128(smem_u32(sm) + C::A_BYTES, 64 * 128, 1024);
+    for (int j = 0; j < nblk; ++j) {
+      const int s = j % DQ_NST;
+      mbar_wait(&full[s], (j / DQ_NST) & 1);
+      fence_after();
+      if (elected) {
+        const uint64_t so = (uint64_t)((s * C::STAGE) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)   // 64 keys = 4 x 16
+          mma(tbase, da0 + so + kk * 128, db0 + so + kk * 128, id_q, (j > 0 || kk > 0) ? 1u : 0u);
+        commit(&empty[s]);
+        if (j == nblk - 1) commit(done);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int qi = q0 + 32 * qw + lane;
+    const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    mbar_wait(done, 0);
+    fence_after();
+    uint32_t gq[DH];
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) tmem_ld16(la + c, gq + c);
+    tmem_wait_ld();
+    if (qi < T_) {
+      const float isq = rsqrtf((float)DH);
+      bf16* row = dqkv + ((long)row0 + qi) * 3 * d + hh * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 16) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          __nv_bfloat162 q2 = __floats2bfloat162_rn(__uint_as_float(gq[c + 2 * i]) * isq,
+                                                    __uint_as_float(gq[c + 2 * i + 1]) * isq);
+          pk[i] = *(uint32_t*)&q2;
+        }
+        *(uint4*)(row + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *(uint4*)(row + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::TCOLS));
+  }
+}
+
 // D[b, h, t] = sum_f dO[t, h f] O[t, h f]: one thread per (token, head), 16-byte vectors;
 // consecutive threads take consecutive heads of a token (contiguous bytes)
 template <int DH>
@@ -1223,7 +1352,7 @@ static bool make_map2d(CUtensorMap* m, const bf16* base, long cols, long rows, i
 // each fills the SMs the other's causal tail leaves idle), joined back into st
 template <int DH>
 bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B, int T_,
-         int h, cudaStream_t st, cudaStream_t st2, const Drop& drop) {
+         int h, cudaStream_t st, cudaStream_t st2, const Drop& drop, bf16* dsT) {
   const long d = (long)h * DH, rows = (long)B * T_;
   CUtensorMap qkv64, qkv128, do64, do128;
   if (!make_map2d(&qkv64, qkv, 3 * d, rows, 64) || !make_map2d(&qkv128, qkv, 3 * d, rows, 128) ||
@@ -1243,6 +1372,8 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, false) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, false)
     ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, true) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, true)
 #undef ATOM_BWD_ATTR
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_ds_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      DqCfg<DH>::SMEM));
     tsa_kv = tsa_mask(1);
     tsa_q = tsa_mask(2);
     once = true;
@@ -1251,6 +1382,36 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
   dsum_tc_kernel<DH><<<(nthr + 255) / 256, 256, 0, st>>>(o, dout, Dsum, B, T_, h);
   count_launch("attn_dsum");
   dim3 grid((T_ + 127) / 128, B * h);
+  const bool dr = drop.thr != 0;
+  if (dsT && T_ % 64 == 0) {
+    // dK/dV also writes dS^T; dQ = dS K over it (the dQ kernel no longer recomputes S and dP: five
+    // products issued for the five the math needs instead of seven)
+    CUtensorMap tm_ds;
+    PFN_encodeTiled enc = encoder();
+    cuuint64_t dims[2] = {(cuuint64_t)T_, (cuuint64_t)B * h * T_};
+    cuuint64_t strides[1] = {(cuuint64_t)T_ * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    if (!enc || enc(&tm_ds, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dsT, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("attention: dS tensor map encode failed");
+      return false;
+    }
+#define ATOM_DKV_DS(TS, DR)                                                                                       \
+  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
+                                                                      drop, dsT)
+    if (tsa_kv) { if (dr) ATOM_DKV_DS(true, true); else ATOM_DKV_DS(true, false); }
+    else { if (dr) ATOM_DKV_DS(false, true); else ATOM_DKV_DS(false, false); }
+#undef ATOM_DKV_DS
+    static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
+    count_launch(nkv.c_str());
+    attn_bwd_dq_ds_kernel<DH><<<grid, 256, DqCfg<DH>::SMEM, st>>>(tm_ds, qkv64, dqkv, T_, h);
+    static const std::string nq = "attn_bwd_dq_ds<" + std::to_string(DH) + ">";
+    count_launch(nq.c_str());
+    ATOM_CUDA_OK(cudaGetLastError());
+    return true;
+  }
   // fork / join events of the dQ stream, one pair per device (peers of one process may sit on
   // different GPUs)
   static cudaEvent_t ev_fork[64] = {}, ev_join[64] = {};
@@ -1266,9 +1427,9 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     ATOM_CUDA_OK(cudaStreamWaitEvent(st2, ev_fork[dev], 0));
   }
   const cudaStream_t sq = st2 ? st2 : st;
-  const bool dr = drop.thr != 0;
-#define ATOM_DKV(TS, DR) \
-  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, drop)
+#define ATOM_DKV(TS, DR)                                                                                          \
+  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
+                                                                      drop, nullptr)
 #define ATOM_DQ(TS, DR)                                                                                         \
   attn_bwd_dq2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum, \
                                                                        dqkv, T_, h, drop)
@@ -1296,11 +1457,11 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
 bool attn_tc_supported(int dh, int d) { return (dh == 64 || dh == 80 || dh == 128) && ((3 * d) % 8 == 0); }
 
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2, Drop drop) {
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2, Drop drop, bf16* dsT) {
   switch (dh) {
-    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
-    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
-    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop);
+    case 64: return atc::bwd<64>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop, dsT);
+    case 80: return atc::bwd<80>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop, dsT);
+    case 128: return atc::bwd<128>(qkv, o, dout, lse, Dsum, dqkv, B, T_, h, st, st2, drop, dsT);
   }
   set_error("tcgen05 attention: unsupported head size %d", dh);
   return false;

@@ -116,6 +116,7 @@ uint8_t* hfin_ptr(const atom_peer* p, int mb) {
 struct Scratch {
   uint8_t *G, *A, *DA, *DX2, *DO;
   float* Dsum;
+  uint8_t* dsT;
   uint8_t *logits, *z, *dz;
   float* hst;
 };
@@ -129,6 +130,8 @@ Scratch scratch_view(const atom_peer* p) {
   s.DX2 = b; b += al256(ab * M * d);
   s.DO = b; b += al256(ab * M * d);
   s.Dsum = (float*)b;
+  b += al256(4LL * p->dm.b * p->dm.h * p->dm.T);
+  s.dsT = p->dm.dtype == ATOM_BF16 ? b : nullptr;   // [b h][T keys][T queries] bf16
   b = p->scratch;
   s.logits = b; b += al256(ab * M * al(p->dm.V, 8));
   s.z = b; b += al256(ab * M * d);
@@ -228,7 +231,7 @@ bool attn_bwd(atom_peer* p, const T* qkv, const T* o, const T* dout, const float
   if constexpr (std::is_same<T, bf16>::value) {
     if (attn_tc_supported(dh, dm.d))
       return attn_bwd_tc(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp,
-                         p->side_wgrad ? p->s_attn : nullptr, dr);
+                         p->side_wgrad ? p->s_attn : nullptr, dr, (bf16*)scratch_view(p).dsT);
     if (attn_fa_supported(dh)) return attn_bwd_fa(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp);
   }
   return attn_bwd_simt<T>(qkv, o, dout, lse, Dsum, dqkv, dm.b, dm.T, dm.h, dh, p->s_comp, dr);
@@ -873,10 +876,10 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   p->dh = a; a += al256(ab * p->C * M * d);
   p->losses = (float*)a; a += al256(4LL * p->C * M);
   p->scratch = a;
-  p->scratch_bytes = std::max(al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T),
-                              al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
-  a += std::max(al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T),
-                al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
+  const int64_t bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T) +
+                        (dm.dtype == ATOM_BF16 ? al256(2LL * dm.b * dm.h * dm.T * dm.T) : 0);
+  p->scratch_bytes = std::max(bwd_s, al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
+  a += p->scratch_bytes;
   p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);
   p->emb = (int*)a; a += al256(4LL * (3 * dm.V + 1 + M));
   p->loss_dev = (float*)a;                 // 256-byte slot: the step loss at 0,

@@ -73,7 +73,10 @@ bool attn_fa_supported(int dh);
 bool attn_tc_supported(int dh, int d);
 bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int dh, cudaStream_t st,
                  Drop drop = Drop());
+// dsT != NULL: [B h][T][T] bf16 scratch: the dK/dV kernel also writes dS^T there and dQ = dS K runs
+// as a separate kernel over it (no recomputation of S and dP); NULL: the dQ kernel recomputes them
 bool attn_bwd_tc(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, float* Dsum, bf16* dqkv, int B,
-                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2 = nullptr, Drop drop = Drop());
+                 int T_, int h, int dh, cudaStream_t st, cudaStream_t st2 = nullptr, Drop drop = Drop(),
+                 bf16* dsT = nullptr);
 
 }  // namespace atom
