@@ -588,7 +588,8 @@ struct BCfg2 {
   static constexpr int P128 = 128 * 128, P64 = 64 * 128;
   static constexpr int FIX = 2 * NP * P128;          // K,V (dK/dV kernel) or Q,dO (dQ kernel)
   static constexpr int STG = 2 * NP * P64;           // Q_i,dO_i or K_j,V_j: 64 rows each
-  static constexpr int SMEM = FIX + BW_NST * STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
+  static constexpr int DS_STG = 128 * 128;           // dK/dV kernel: one dS^T tile (128 keys x 64 queries) for its TMA store
+  static constexpr int SMEM = FIX + BW_NST * STG + DS_STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
   // d_h <= 80: the per-CTA fixed operands (K, V or Q, dO) live in TMEM as A operands of S / dP
   // (TS MMAs: no shared-memory A reads, which bound the SS MMAs); d_h = 128 has no TMEM room
   static constexpr bool TSA = TSA_ && DH <= 80;
@@ -633,7 +634,7 @@ __global__ void __launch_bounds__(384, 1)
     attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ qkv,
                          const float* __restrict__ lse, const float* __restrict__ Dsum, bf16* __restrict__ dqkv,
-                         int T_, int h, const Drop drop, bf16* __restrict__ dsT) {
+                         int T_, int h, const Drop drop, const bool store_ds, const __grid_constant__ CUtensorMap tm_dsw) {
   using C = BCfg2<DH, TSA>;
   constexpr int NST = BW_NST;
   constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
@@ -642,7 +643,8 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
   uint8_t* sS = sm + C::FIX;                           // stage s: Q at + s*STG, dO at + NP*P64
-  float* sLD = (float*)(sS + NST * C::STG);            // stage s: L[64] at + 128 s, D[64] at + 128 s + 64
+  uint8_t* sDS = sS + NST * C::STG;                    // dS^T tile staging for its TMA store (1024-aligned)
+  float* sLD = (float*)(sDS + C::DS_STG);              // stage s: L[64] at + 128 s, D[64] at + 128 s + 64
   uint64_t* bars = (uint64_t*)(sLD + NST * 128);
   uint64_t* kv_full = bars;
   uint64_t* st_full = bars + 1;           // [NST]  TMA tx + 32 producer lanes
@@ -838,12 +840,29 @@ __global__ void __launch_bounds__(384, 1)
           dk[2 * c4 + h2] = *(uint32_t*)&b2;
         }
       }
-      if (dsT && kj < T_) {   // dS^T row of this key, 32 queries (64 contiguous bytes) for the dQ kernel
-        uint4* dst = (uint4*)(dsT + ((long)bh * T_ + kj) * T_ + q0 + 32 * wg);
-        dst[0] = make_uint4(dk[0], dk[1], dk[2], dk[3]);
-        dst[1] = make_uint4(dk[4], dk[5], dk[6], dk[7]);
-        dst[2] = make_uint4(dk[8], dk[9], dk[10], dk[11]);
-        dst[3] = make_uint4(dk[12], dk[13], dk[14], dk[15]);
+      if (store_ds) {
+        // dS^T for the dQ kernel: each warp stages its 32 keys x 32 queries (64B-swizzled rows) in
+        // its own 2 KB smem box and lane 0 stores it with TMA (full-line writes, no block-wide
+        // barrier; per-thread 64-byte global stores had doubled this kernel's time).  Lane 0 waits
+        // for its previous box to be read before the warp overwrites it
+        const uint32_t box = smem_u32(sDS) + (uint32_t)(warp - 4) * 2048u;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (uint32_t)lane * 64 + ((((uint32_t)i) ^ swz) << 4)),
+                       "r"(dk[4 * i]), "r"(dk[4 * i + 1]), "r"(dk[4 * i + 2]), "r"(dk[4 * i + 3])
+                       : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tm_dsw)),
+                       "r"(box), "r"(q0 + 32 * wg), "r"(bh * T_ + k0 + 32 * qw)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
       named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
       tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
@@ -852,6 +871,7 @@ __global__ void __launch_bounds__(384, 1)
       fence_before();
       mbar_arrive(&p_full[u]);
     }
+    if (store_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     mbar_wait(done, 0);
     fence_after();
     // warpgroup 0 writes dV, warpgroup 1 writes dK (scaled by 1/sqrt(dh))
@@ -1383,7 +1403,7 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
   count_launch("attn_dsum");
   dim3 grid((T_ + 127) / 128, B * h);
   const bool dr = drop.thr != 0;
-  if (dsT && T_ % 64 == 0) {
+  if (dsT && T_ % 128 == 0) {
     // dK/dV also writes dS^T; dQ = dS K over it (the dQ kernel no longer recomputes S and dP: five
     // products issued for the five the math needs instead of seven)
     CUtensorMap tm_ds;
@@ -1392,15 +1412,20 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     cuuint64_t strides[1] = {(cuuint64_t)T_ * 2};
     cuuint32_t box[2] = {64, 64};
     cuuint32_t es[2] = {1, 1};
+    CUtensorMap tm_dsw;   // the dK/dV kernel's stores: one warp's 32 keys x 32 queries per box
+    cuuint32_t boxw[2] = {32, 32};
     if (!enc || enc(&tm_ds, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dsT, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&tm_dsw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dsT, dims, strides, boxw, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       set_error("attention: dS tensor map encode failed");
       return false;
     }
 #define ATOM_DKV_DS(TS, DR)                                                                                       \
   attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
-                                                                      drop, dsT)
+                                                                      drop, true, tm_dsw)
     if (tsa_kv) { if (dr) ATOM_DKV_DS(true, true); else ATOM_DKV_DS(true, false); }
     else { if (dr) ATOM_DKV_DS(false, true); else ATOM_DKV_DS(false, false); }
 #undef ATOM_DKV_DS
@@ -1429,7 +1454,7 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
   const cudaStream_t sq = st2 ? st2 : st;
 #define ATOM_DKV(TS, DR)                                                                                          \
   attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
-                                                                      drop, nullptr)
+                                                                      drop, false, qkv64)
 #define ATOM_DQ(TS, DR)                                                                                         \
   attn_bwd_dq2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum, \
                                                                        dqkv, T_, h, drop)
