@@ -211,6 +211,15 @@ def cpu_sample(g, seconds_hint=20.0, max_steps=3):
     h = oadamw.AdamWHyper()
     m = np.zeros_like(p)
     v = np.zeros_like(p)
+    # BLAS on every host core (torchrun sets OMP_NUM_THREADS=1 for its ranks): the reported core
+    # count is the thread count the sample really used
+    cores = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        limiter = threadpool_limits(limits=cores)
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        limiter = None
     t0 = time.perf_counter()
     n = 0
     while True:
@@ -220,12 +229,14 @@ def cpu_sample(g, seconds_hint=20.0, max_steps=3):
         if time.perf_counter() - t0 > seconds_hint or n >= max_steps:
             break
     dt = (time.perf_counter() - t0) / n
+    if limiter is not None:
+        limiter.unregister()
     rate_sample = g.seq_len / dt
     rate = rate_sample * f_alg_per_token(g1) / f_alg_per_token(g)
     desc = (f"oracle fp32 numpy fwd+bwd+AdamW on 1 sequence (T={g.seq_len}) of a {L}-block copy of the model "
             f"(d={g.d_model}, V={g.vocab}); {n} step(s), {dt:.1f} s each; tokens/s scaled to L={g.n_layer} by "
             f"algorithmic FLOPs per token")
-    return rate, desc, os.cpu_count(), dt
+    return rate, desc, cores, dt
 
 
 def run_reference(args, g, wl_desc):

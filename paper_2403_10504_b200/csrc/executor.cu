@@ -116,7 +116,7 @@ uint8_t* hfin_ptr(const atom_peer* p, int mb) {
 struct Scratch {
   uint8_t *G, *A, *DA, *DX2, *DO;
   float* Dsum;
-  uint8_t* dsT;
+  uint8_t *G2, *dsT;
   uint8_t *logits, *z, *dz;
   float* hst;
 };
@@ -131,6 +131,8 @@ Scratch scratch_view(const atom_peer* p) {
   s.DO = b; b += al256(ab * M * d);
   s.Dsum = (float*)b;
   b += al256(4LL * p->dm.b * p->dm.h * p->dm.T);
+  s.G2 = b;                                           // [M, 4d]: dL/du while G holds GELU(u)
+  b += al256(ab * M * 4 * d);
   s.dsT = p->dm.dtype == ATOM_BF16 ? b : nullptr;   // [b h][T keys][T queries] bf16
   b = p->scratch;
   s.logits = b; b += al256(ab * M * al(p->dm.V, 8));
@@ -384,22 +386,30 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
     KT(KC_COLSUM, p->s_comp, dropout<T>(dy, (T*)sc.DX2, M * d, d3, p->s_comp));
     dym = (const T*)sc.DX2;
   }
-  // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr)
-  PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d)));
+  // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr).  Its weight gradient reads GELU(u) in G
+  // and dy: on the side stream when the fc pre-activation gradient goes to the second buffer G2
+  // (so nothing on the main stream rewrites G or dy before the join ahead of the attention
+  // backward); on the main stream with dropout (dym lives in DX2), under the re-forward (no
+  // join there) and for a split block (dy is rewritten in place by LN2's backward)
+  const bool wpr_side = side && !rc && !d3.thr && !split;
+  T* Gx = wpr_side ? (T*)sc.G2 : G;   // dL/du
+  if (wpr_side) PEER_OK(fork());
+  PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d),
+                  wpr_side ? sd : p->s_comp));
   KT(KC_COLSUM, p->s_comp, bias_grad<T>(dym, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
   // fc pre-activation gradient: (dy W_pr) with a plain-store epilogue, then the GELU derivative
   // and the fc bias gradient in one pass over it (the GEMM epilogue reading u per row was the
   // slow part of the fused form)
-  PEER_OK(gemm<T>(p, M, 4 * d, d, dym, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, G, 4 * d)));
-  KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(G, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
+  PEER_OK(gemm<T>(p, M, 4 * d, d, dym, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, Gx, 4 * d)));
+  KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(Gx, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
   // MLP fc: u = LN2(x2) W_fc^T + b_fc (under recompute LN2's output is DA, rewritten just below:
   // that gradient stays on the main stream)
   if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));
   if (!rc) PEER_OK(fork());
-  PEER_OK(gemm<T>(p, 4 * d, d, M, G, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d),
+  PEER_OK(gemm<T>(p, 4 * d, d, M, Gx, 4 * d, true, (const T*)ln2, d, true, epi(EPI_ACC_F32, g(T_WFC), d),
                   rc ? p->s_comp : sd));
   if (!rc) PEER_OK(mark(1));
-  PEER_OK(gemm<T>(p, M, d, 4 * d, G, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
+  PEER_OK(gemm<T>(p, M, d, 4 * d, Gx, 4 * d, false, w(T_WFC), d, true, epi(EPI_STORE, sc.DA, d)));
   KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x2, s.st2, w(T_LN2G), dy, dx2, g(T_LN2G), g(T_LN2B), p->red,
                     p->red_ticket, M, d, p->s_comp));
   // the attention half runs in another op: the W_fc gradient has read G / LN2's output by then
@@ -877,7 +887,7 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   p->losses = (float*)a; a += al256(4LL * p->C * M);
   p->scratch = a;
   const int64_t bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T) +
-                        (dm.dtype == ATOM_BF16 ? al256(2LL * dm.b * dm.h * dm.T * dm.T) : 0);
+                        al256(ab * M * 4 * d) + (dm.dtype == ATOM_BF16 ? al256(2LL * dm.b * dm.h * dm.T * dm.T) : 0);
   p->scratch_bytes = std::max(bwd_s, al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
   a += p->scratch_bytes;
   p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);
