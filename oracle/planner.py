@@ -323,8 +323,7 @@ def work_bytes(c: PlanCfg, C: int) -> int:
     tokens = al256(4 * C * b * (T + 1))
     dh = al256(ab * C * M * d)
     losses = al256(4 * C * M)
-    bwd_s = (al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4 * b * h * T) + 2 * al256(ab * M * 4 * d)
-             + 2 * al256(ab * M * d))
+    bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4 * b * h * T) + al256(ab * M * 4 * d)
     if c.dtype == BF16:   # the attention backward's dS^T [b, h, T, T] (bf16) between its dK/dV and dQ kernels
         bwd_s += al256(2 * b * h * T * T)
     head_s = al256(ab * M * Vp) + 2 * al256(ab * M * d) + al256(8 * M)

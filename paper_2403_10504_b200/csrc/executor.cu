@@ -116,7 +116,7 @@ uint8_t* hfin_ptr(const atom_peer* p, int mb) {
 struct Scratch {
   uint8_t *G, *A, *DA, *DX2, *DO;
   float* Dsum;
-  uint8_t *G2, *G_alt, *A_alt, *DX2_alt, *dsT;
+  uint8_t *G2, *dsT;
   uint8_t *logits, *z, *dz;
   float* hst;
 };
@@ -133,12 +133,6 @@ Scratch scratch_view(const atom_peer* p) {
   b += al256(4LL * p->dm.b * p->dm.h * p->dm.T);
   s.G2 = b;                                           // [M, 4d]: dL/du while G holds GELU(u)
   b += al256(ab * M * 4 * d);
-  s.G_alt = b;                                        // odd blocks' G, A, DX2 (deferred side-stream join)
-  b += al256(ab * M * 4 * d);
-  s.A_alt = b;
-  b += al256(ab * M * d);
-  s.DX2_alt = b;
-  b += al256(ab * M * d);
   s.dsT = p->dm.dtype == ATOM_BF16 ? b : nullptr;   // [b h][T keys][T queries] bf16
   b = p->scratch;
   s.logits = b; b += al256(ab * M * al(p->dm.V, 8));
@@ -331,21 +325,14 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   StashView s = stash_view(p, l, mb);
   Scratch sc = scratch_view(p);
   T* dy = (T*)(p->dh + (int64_t)mb * M * d * dm.wb);
+  T* G = (T*)sc.G;
   const bool rc = !p->blk_full[l];   // never in the operator-granular graph (stash only)
   const bool split = part != 0 && p->seg_of_node[blk_node(dm, l, 0)] != p->seg_of_node[blk_node(dm, l, 1)];
-  // G, A and DX2 alternate between consecutive blocks (block parity): the side stream's last weight
-  // gradient of block l (W_qkv, reading G and A) and W_o (reading DX2) may still run while block
-  // l - 1 starts, so the end-of-block join is deferred to the end of the backward op (run_bwd);
-  // block l - 1's first join (ahead of its attention backward) orders them before block l - 2
-  const bool alt = (l & 1) && !split;
-  T* G = (T*)(alt ? sc.G_alt : sc.G);
-  T* Ab = (T*)(alt ? sc.A_alt : sc.A);
-  T* DX2b = (T*)(alt ? sc.DX2_alt : sc.DX2);
-  T* dx2 = split ? dy : DX2b;   // dL/dx2 from LN2's backward to the attention half
+  T* dx2 = split ? dy : (T*)sc.DX2;   // dL/dx2 from LN2's backward to the attention half
   // LN outputs the weight gradients read: re-applied from the stash, or (recompute) kept from the
   // re-run forward -- LN1(x) in A, LN2(x2) in DA (free until the fc data-gradient GEMM)
-  T* ln1 = Ab;
-  T* ln2 = rc ? (T*)sc.DA : Ab;
+  T* ln1 = (T*)sc.A;
+  T* ln2 = rc ? (T*)sc.DA : (T*)sc.A;
   const Drop d3 = mkdrop(p, DS_RESID_MLP, l, mb), d2 = mkdrop(p, DS_RESID_ATTN, l, mb);
   // Weight-gradient GEMMs that nothing later in the block reads run on the side stream (fork after
   // their inputs exist; the main stream waits before overwriting what they read). Buffers: WFC's
@@ -369,7 +356,6 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
     return true;
   };
   if (part != 1) {
-  if (rc) PEER_OK(join(3));   // the shared re-forward entry may still be read by the side stream
   if (rc) {
     // ACT_RECOMPUTE: re-run the block forward from its input checkpoint into the shared entry
     // (same kernels and inputs as the forward: bit-identical tensors); the MLP projection's
@@ -377,7 +363,7 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
     KT(KC_LN, p->s_comp, ln_fwd<T>((const T*)s.x, w(T_LN1G), w(T_LN1B), ln1, s.st1, M, d, p->s_comp));
     Epi e = epi(EPI_BIAS, s.qkv, 3 * d);
     e.bias = w(T_BQKV);
-    PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)Ab, d, false, w(T_WQKV), d, false, e));
+    PEER_OK(gemm<T>(p, M, 3 * d, d, (const T*)sc.A, d, false, w(T_WQKV), d, false, e));
     KT(KC_ATTN_F, p->s_comp, attn_fwd<T>(p, (const T*)s.qkv, (T*)s.o, s.lse, mkdrop(p, DS_ATTN, l, mb)));
     e = epi(EPI_BIAS, s.x2, d);
     e.bias = w(T_BO);
@@ -397,8 +383,8 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   // QKV data gradient rewrites it); the residual paths keep the unmasked ones
   const T* dym = dy;
   if (d3.thr) {
-    KT(KC_COLSUM, p->s_comp, dropout<T>(dy, DX2b, M * d, d3, p->s_comp));
-    dym = (const T*)DX2b;
+    KT(KC_COLSUM, p->s_comp, dropout<T>(dy, (T*)sc.DX2, M * d, d3, p->s_comp));
+    dym = (const T*)sc.DX2;
   }
   // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr).  Its weight gradient reads GELU(u) in G
   // and dy: on the side stream when the fc pre-activation gradient goes to the second buffer G2
@@ -456,9 +442,8 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   if (split && !d2.thr) PEER_OK(join(2));   // W_o's gradient has read DX2 from dh[mb], rewritten next
   KT(KC_LN, p->s_comp, ln_bwd<T>((const T*)sc.DA, (const T*)s.x, s.st1, w(T_LN1G), (const T*)dx2, dy, g(T_LN1G), g(T_LN1B),
                     p->red, p->red_ticket, M, d, p->s_comp));
-  // the side stream is in order: its last mark covers WO and WQKV (and WFC); a split block joins
-  // here (its halves' buffers are not alternated), the others at the end of the backward op
-  if (split || !side) PEER_OK(join(3));
+  // the side stream is in order: its last mark covers WO and WQKV (and WFC)
+  PEER_OK(join(3));
   return true;
 }
 
@@ -548,12 +533,6 @@ bool run_bwd(atom_peer* p, int k, int mb, const SegView& sv) {
     else if (is_block_node(p->dm, node))
       PEER_OK(bwd_block<T>(p, node_block(p->dm, node), mb, sv, node_half(p->dm, node)));
     // the head's backward ran inside its forward op
-  }
-  // the deferred side-stream join of the op's blocks (their weight gradients, before ADAM or the
-  // next op reuses the scratch buffers)
-  if (p->side_wgrad) {
-    PEER_CUDA(cudaEventRecord(p->ev_side[3], p->s_side));
-    PEER_CUDA(cudaStreamWaitEvent(p->s_comp, p->ev_side[3], 0));
   }
   return true;
 }
@@ -908,8 +887,7 @@ bool peer_create(atom_peer* p, const float* init_params, uint64_t seed, const vo
   p->losses = (float*)a; a += al256(4LL * p->C * M);
   p->scratch = a;
   const int64_t bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4LL * dm.b * dm.h * dm.T) +
-                        2 * al256(ab * M * 4 * d) + 2 * al256(ab * M * d) +
-                        (dm.dtype == ATOM_BF16 ? al256(2LL * dm.b * dm.h * dm.T * dm.T) : 0);
+                        al256(ab * M * 4 * d) + (dm.dtype == ATOM_BF16 ? al256(2LL * dm.b * dm.h * dm.T * dm.T) : 0);
   p->scratch_bytes = std::max(bwd_s, al256(ab * M * al(dm.V, 8)) + 2 * al256(ab * M * d) + al256(8 * M));
   a += p->scratch_bytes;
   p->red = (float*)a; a += al256(4 * ceil_div(M, RED_ROWS) * 4 * d);

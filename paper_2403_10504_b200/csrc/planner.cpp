@@ -153,10 +153,8 @@ int64_t work_bytes(const ModelDims& dm, int C) {
   int64_t dh = al256(ab * C * M * d);
   int64_t losses = al256(4LL * C * M);
   // G, A, DA, DX2, DO, D, G2 (dL/du beside GELU(u), so the MLP projection's weight gradient can
-  // run on the side stream), and G, A, DX2 for odd blocks (the side stream's join deferred to the
-  // end of the backward op)
-  int64_t bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4 * b * h * T) + 2 * al256(ab * M * 4 * d) +
-                  2 * al256(ab * M * d);
+  // run on the side stream)
+  int64_t bwd_s = al256(ab * M * 4 * d) + 4 * al256(ab * M * d) + al256(4 * b * h * T) + al256(ab * M * 4 * d);
   if (dm.dtype == ATOM_BF16) bwd_s += al256(2 * b * h * T * T);   // attention dS^T between dK/dV and dQ
   int64_t head_s = al256(ab * M * Vp) + 2 * al256(ab * M * d) + al256(8 * M);
   int64_t scratch = std::max(bwd_s, head_s);
