@@ -916,7 +916,8 @@ static bool launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   }
   kern<<<2 * clusters, 256, Tc2Cfg::SMEM, st>>>(ta, tb, to, to2, M, N, K, e, group_m_for(K, 2, !A_MN && B_MN), sk);
   static const std::string name = "gemm_tc2<" + std::to_string((int)A_MN) + "," + std::to_string((int)B_MN) + ">";
-  count_launch(name.c_str());
+  static const std::string name_sk = "gemm_tc2_splitk<" + std::to_string((int)A_MN) + "," + std::to_string((int)B_MN) + ">";
+  count_launch(sk.P > 1 ? name_sk.c_str() : name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;
 }

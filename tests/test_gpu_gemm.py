@@ -135,16 +135,35 @@ def test_tc_gemm_deterministic():
     assert torch.equal(outs[0], outs[1])
 
 
+_SPLITK_CHILD = r"""
+import sys, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from paper_2403_10504_b200 import atom
+import test_gpu_gemm as t
+M, N, K, amn, bmn = {args}
+ref, got = t._run(atom.IMPL_TC, torch.bfloat16, M, N, K, amn, bmn, atom.EPI_ACC_F32, 512)
+t._close(ref, got, torch.bfloat16, K)
+ref2, got2 = t._run(atom.IMPL_TC, torch.bfloat16, M, N, K, amn, bmn, atom.EPI_ACC_F32, 512)
+assert torch.equal(got, got2)
+log = atom.launch_log()
+assert any(k.startswith("gemm_tc2_splitk<") for k in log), log
+print("splitk ok")
+"""
+
+
 @pytest.mark.parametrize("shape", [(3840, 2560, 2048), (4096, 4096, 1024), (2560 + 200, 2560 + 40, 1536)],
                          ids=["tail2-P8", "tail34-P2", "ragged"])
 @pytest.mark.parametrize("majors", [(True, True), (False, False)], ids=["wgrad", "kmajor"])
 def test_tc_gemm_acc_f32_streamk_tail(shape, majors):
     """Weight-gradient GEMMs (fp32 accumulate) whose last wave is split along K (stream-K tail,
-    gemm_tc.cu SplitK, ATOM_GEMM_SPLITK=1 -- read once per process, so this test runs the split
-    only when the variable is set for the test run): same result as the unsplit math within fp32
-    rounding, and deterministic."""
-    M, N, K = shape
-    ref, got = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, atom.EPI_ACC_F32, 512)
-    _close(ref, got, torch.bfloat16, K)
-    ref2, got2 = _run(atom.IMPL_TC, torch.bfloat16, M, N, K, *majors, atom.EPI_ACC_F32, 512)
-    assert torch.equal(got, got2)
+    gemm_tc.cu SplitK, off by default; ATOM_GEMM_SPLITK=1 is read once per process, so the check
+    runs in a child process with it set): same result as the unsplit math within fp32 rounding,
+    deterministic, and the launch log proves the split kernel ran."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _SPLITK_CHILD.format(root=root, tests=os.path.join(root, "tests"), args=(*shape, *majors))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, ATOM_GEMM_SPLITK="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "splitk ok" in r.stdout, r.stdout + r.stderr
