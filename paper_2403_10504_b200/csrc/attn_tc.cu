@@ -780,8 +780,38 @@ __global__ void __launch_bounds__(384, 1)
       fence_before();
       mbar_arrive(kv_full);
     }
+    // dS^T for the dQ kernel: each warp stages its 32 keys x 32 queries (64B-swizzled rows) in its
+    // own 2 KB smem box and lane 0 stores it with TMA (full-line writes, no block-wide barrier;
+    // per-thread 64-byte global stores had doubled this kernel's time).  The box of block it is
+    // staged at the top of block it + 1, before the waits for its MMAs, so the proxy fence's
+    // latency hides under them; lane 0 waits for its previous box to be read before reuse
+    uint32_t pend[16];
+    int pend_q = -1;
+    auto flush_ds = [&]() {
+      if (!store_ds || pend_q < 0) return;
+      const uint32_t box = smem_u32(sDS) + (uint32_t)(warp - 4) * 2048u;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (uint32_t)lane * 64 + ((((uint32_t)i) ^ swz) << 4)),
+                     "r"(pend[4 * i]), "r"(pend[4 * i + 1]), "r"(pend[4 * i + 2]), "r"(pend[4 * i + 3])
+                     : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tm_dsw)),
+                     "r"(box), "r"(pend_q + 32 * wg), "r"(bh * T_ + k0 + 32 * qw)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      pend_q = -1;
+    };
     for (int it = 0; it < nblk; ++it) {
       const int s = it % NST, u = it & 1, q0 = (i0 + it) * 64;
+      flush_ds();
       mbar_wait(&st_full[s], (it / NST) & 1);   // L / D of this stage visible
       mbar_wait(&s_full[u], (it >> 1) & 1);
       fence_after();
@@ -840,29 +870,10 @@ __global__ void __launch_bounds__(384, 1)
           dk[2 * c4 + h2] = *(uint32_t*)&b2;
         }
       }
-      if (store_ds) {
-        // dS^T for the dQ kernel: each warp stages its 32 keys x 32 queries (64B-swizzled rows) in
-        // its own 2 KB smem box and lane 0 stores it with TMA (full-line writes, no block-wide
-        // barrier; per-thread 64-byte global stores had doubled this kernel's time).  Lane 0 waits
-        // for its previous box to be read before the warp overwrites it
-        const uint32_t box = smem_u32(sDS) + (uint32_t)(warp - 4) * 2048u;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-        const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+      if (store_ds) {   // staged and stored at the top of the next block (flush_ds)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (uint32_t)lane * 64 + ((((uint32_t)i) ^ swz) << 4)),
-                       "r"(dk[4 * i]), "r"(dk[4 * i + 1]), "r"(dk[4 * i + 2]), "r"(dk[4 * i + 3])
-                       : "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                           reinterpret_cast<uint64_t>(&tm_dsw)),
-                       "r"(box), "r"(q0 + 32 * wg), "r"(bh * T_ + k0 + 32 * qw)
-                       : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
+        for (int i = 0; i < 16; ++i) pend[i] = dk[i];
+        pend_q = q0;
       }
       named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
       tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
@@ -871,6 +882,7 @@ __global__ void __launch_bounds__(384, 1)
       fence_before();
       mbar_arrive(&p_full[u]);
     }
+    flush_ds();
     if (store_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     mbar_wait(done, 0);
     fence_after();
