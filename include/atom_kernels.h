@@ -35,8 +35,9 @@ int atom_k_gemm(int impl, int dtype, int M, int N, int K, const void* A, long ld
  * [q | k | v], head j at columns j*dh; o: [B*T, h*dh]; lse: fp32 [B, h, T] (natural log of the
  * softmax normaliser of scores q.k/sqrt(dh)).  impl: ATOM_ATTN_TC (tcgen05/TMEM, dh in {64, 80, 128};
  * the backward's dQ kernel recomputes S and dP), ATOM_ATTN_TC_DS (backward only: the dK/dV kernel
- * writes dS^T to a temporary [B h][T][T] bf16 buffer and dQ = dS K runs over it -- the step's
- * path when T % 64 == 0), ATOM_ATTN_MMA (mma.sync flash attention, dh in
+ * writes dS^T to a [B h][T][T] bf16 buffer and dQ = dS K runs over it -- the step's path when
+ * T % 128 == 0, else as ATOM_ATTN_TC; here the buffer is allocated on first use and kept, growing
+ * only, for later calls on the device), ATOM_ATTN_MMA (mma.sync flash attention, dh in
  * {16, 64, 80, 128}), ATOM_ATTN_SIMT (CUDA cores, dh <= 128).  dtype ATOM_FP32 always uses SIMT.
  * Backward: dout [B*T, h*dh] -> dqkv [B*T, 3*h*dh]; dsum fp32 [B, h, T] is scratch (rowsum(dout*o)). */
 enum { ATOM_ATTN_TC = 0, ATOM_ATTN_MMA = 1, ATOM_ATTN_SIMT = 2, ATOM_ATTN_TC_DS = 3 };
@@ -65,7 +66,7 @@ int atom_k_dropout(int dtype, const void* x, void* y, long n, double p, unsigned
 unsigned long long atom_k_launch_count(void);
 
 /* Launches per kernel family since the library was loaded, as text: one "<family> <count>" line
- * per family (e.g. "gemm_tc2<0,1> 12", "attn_fwd2<80> 4"), written NUL-terminated into the
+ * per family (e.g. "gemm_tc2<0,1> 12", "attn_fwd3<80> 4"), written NUL-terminated into the
  * caller-owned buf of cap bytes; *len = text length.  ATOM_E_INVALID if cap <= *len (nothing
  * written; call again with a larger buffer).  Tests use it to prove which kernels a step ran. */
 int atom_k_launch_log(char* buf, int64_t cap, int64_t* len);

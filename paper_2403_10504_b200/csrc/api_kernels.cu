@@ -4,6 +4,9 @@
 #include "kernels.h"
 #include <string.h>
 
+#include <map>
+#include <mutex>
+
 using namespace atom;
 
 extern "C" {
@@ -56,15 +59,33 @@ int atom_k_attn_bwd(int impl, int dtype, const void* qkv, const void* o, const v
   else if (impl == ATOM_ATTN_TC)
     ok = attn_bwd_tc((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);
   else if (impl == ATOM_ATTN_TC_DS) {
+    // the dS^T scratch (an executor-owned buffer inside atom_step) is kept across calls here and
+    // only grows, so back-to-back calls stay stream-ordered (no allocation or sync per call)
+    static std::mutex mu;
+    static std::map<int, std::pair<bf16*, size_t>> pool;   // device -> (buffer, bytes)
+    const size_t need = (size_t)B * h * T * T * sizeof(bf16);
+    int dev = 0;
+    cudaGetDevice(&dev);
     bf16* dsT = nullptr;
-    if (cudaMalloc((void**)&dsT, (size_t)B * h * T * T * sizeof(bf16)) != cudaSuccess) {
-      set_error("CUDA: dS^T buffer allocation failed");
-      return ATOM_E_CUDA;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto& e = pool[dev];
+      if (e.second < need) {
+        if (e.first) {
+          cudaDeviceSynchronize();
+          cudaFree(e.first);
+        }
+        e = {nullptr, 0};
+        if (cudaMalloc((void**)&e.first, need) != cudaSuccess) {
+          set_error("CUDA: dS^T buffer allocation failed");
+          return ATOM_E_CUDA;
+        }
+        e.second = need;
+      }
+      dsT = e.first;
     }
     ok = attn_bwd_tc((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st,
                      nullptr, Drop(), dsT);
-    cudaStreamSynchronize(st);
-    cudaFree(dsT);
   }
   else if (impl == ATOM_ATTN_MMA)
     ok = attn_bwd_fa((const bf16*)qkv, (const bf16*)o, (const bf16*)dout, lse, dsum, (bf16*)dqkv, B, T, h, dh, st);

@@ -1,18 +1,23 @@
-// Causal attention forward on 5th-gen tensor cores (tcgen05 / TMEM / TMA), flash style.
+// Causal attention on 5th-gen tensor cores (tcgen05 / TMEM / TMA), flash style.
 // minGPT CausalSelfAttention: o_t = sum_{s<=t} softmax_s(q_t.k_s/sqrt(dh)) v_s,
-// LSE stashed for the backward.  One CTA per (b, h, 128-query block):
-//   warp 0     TMA: Q once, then K_j / V_j (two stages) from the qkv activation [tokens, 3d]
-//   warp 1     MMA issuer: S_j = Q K_j^T into TMEM (two S buffers), O += P_j V_j into TMEM
-//   warp 2     TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4-7  softmax: thread i owns query row i = TMEM lane i; reads its S row with tcgen05.ld,
-//              online softmax in the log2 domain with lazy O rescaling (only when the running
-//              max grows by more than 2^8), writes P (bf16) into a 128B-swizzled K-major smem
-//              tile that is the A operand of the P V MMA; finally O / l -> bf16, LSE.
-// K and V tiles are loaded with the same TMA box ([128 keys, 64 features] panels); V is read by
-// the MMA as an MN-major B operand (features contiguous), so no transpose is materialised.
-// Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
+// LSE stashed for the backward.
+//   forward   attn_fwd3_tc_kernel: persistent, one CTA per SM over (b h, query pair) items; two
+//             128-query tiles ping-pong between two softmax warpgroups (thread = query row = TMEM
+//             lane), P written back over S in TMEM as the A operand of O += P V
+//   backward  dsum_tc_kernel (D = rowsum(dO o)), attn_bwd_dkv2_kernel (dK, dV per 128-key block;
+//             optionally writes dS^T), then attn_bwd_dq_ds_kernel (dQ = dS K from dS^T) or, without
+//             the dS^T buffer, attn_bwd_dq2_kernel (dQ recomputing S and dP)
+// K / V / Q tiles are loaded by TMA in [rows, 64 features] 128B-swizzled panels; V (and Q, dO in the
+// backward's second products) are read by the MMA as MN-major B operands, so no transpose is
+// materialised.  Head sizes 64, 80, 128 (80 = two 64-wide panels, the MMAs use K = N = 80).
 #include <cuda.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
+#include <vector>
 #include <stdlib.h>
 #include <type_traits>
 
@@ -231,20 +236,30 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
 }
 
 // ======================================================================================
-// Forward v2: two 128-query tiles per CTA, ping-pong between two softmax warpgroups so the
-// tensor core works on one tile while the other tile's exponentials run.
-//   warp 0      TMA producer: Q0, Q1 once; then K_j, V_j through a ring of NSLOT tile slots
-//   warp 1      MMA issuer, per key block j:  PV0(j-1)... in the order
-//                 S0(0) S1(0) | PV0(0) S0(1) PV1(0) S1(1) | PV0(1) S0(2) PV1(1) S1(2) | ...
+// Forward v3: persistent, two 128-query tiles per work item, ping-pong between two softmax
+// warpgroups so the tensor core works on one tile while the other tile's exponentials run.
+// A work item is (b h, query pair qp): tile t covers queries [128 (2 qp + t), +128) and sees key
+// blocks 0 .. 2 qp + t.  One CTA per SM walks its items (heavy-first order, dealt out in a snake
+// over the CTAs: within ~2 % of a greedy schedule on the GPT-3 shapes), and the next item's
+// start overlaps the current one's end: the producer loads Q_t of the next item as soon as the
+// last S_t MMA of the current one has read Q_t, and the MMA issuer starts S_t(next, 0) right
+// after the current item's last P_t V MMA -- so the next item's first tile runs under the other
+// tile's last (unpaired, diagonal) block and both tiles' output epilogues.  (One CTA per item
+// paid ~6.5 us of fill / drain per item: 30 % of the d_h = 80 forward at T = 2048.)
+//   warp 0      TMA producer: per item Q0, K_0, Q1, then V_0, K_1, V_1, ... through a ring of
+//               NSLOT tile slots (K_j of an item at ring position base + 2j, V_j at base + 2j + 1)
+//   warp 1      MMA issuer, per key block j:  PV0(j) S0(j+1) PV1(j) S1(j+1)
 //   warp 2      TMEM allocator (512 columns: S0/P0 | S1/P1 | O0 | O1)
 //   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1 (thread = query row = TMEM lane)
 // P is written back into TMEM over its own S columns (bf16 pairs) and is the A operand of the
 // O += P V MMA (tcgen05 "TS" form): no shared-memory round trip for P. The MMAs of one tile
 // execute in issue order, so S_t(j+1) overwrites P_t(j) only after PV_t(j) has read it, and
 // the commit that publishes S_t(j+1) also certifies that PV_t(j) finished (O_t is stable for
-// the lazy rescale).
+// the lazy rescale).  The first P V of an item overwrites O_t (accumulate off); it is issued
+// only after the softmax warpgroup has published that item's first P, i.e. after it finished
+// reading the previous item's O_t.
 // ======================================================================================
-template <int DH, bool TSA_ = false>
+template <int DH>
 struct Cfg2 {
   static constexpr int NP = (DH + 63) / 64;
   static constexpr int PANEL = 128 * 128;
@@ -254,19 +269,42 @@ struct Cfg2 {
   static constexpr int NSLOT = NSLOT_FIT > 8 ? 8 : NSLOT_FIT;
   static constexpr int SMEM = Q_BYTES + NSLOT * SLOT + 1024 + 512;
   static constexpr uint32_t S_COL = 0, O_COL = 256;  // tile t: S/P at 128t, O at 256 + 128t
-  // d_h <= 80: Q_t lives in TMEM after O_t and S = Q K^T is a TS MMA (no smem A reads)
-  static constexpr bool TSA = TSA_ && DH <= 80;
-  static constexpr uint32_t Q_COL = O_COL + (DH + 15) / 16 * 16;   // tile t: + 128t
-  static_assert(!TSA || Q_COL + 128 + DH / 2 <= 512, "TMEM budget");
+  static_assert(NSLOT >= 4, "the item hand-over keeps four ring slots in flight");
 };
+
+// Work items in groups of `grp` heads (the host picks grp, fwd_group): within a group, heavy-first
+// by query pair, then by head -- the items running at the same time share the K / V of a few heads
+// in L2, and the lightest items of a group fill the idle tail of the CTAs.  Item i of the ordered
+// list goes to CTA c in a snake deal: round r = i / G, CTA c takes the c-th (r even) or the
+// (G - 1 - c)-th (r odd) item of the round.
+__device__ __forceinline__ int fwd_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
+struct FwdItem {
+  int bh, qb0, nkb0, nkb1, nkb;
+};
+__host__ __device__ inline void fwd_item_pos(int i, int BH, int npair, int grp, int* bh, int* qp) {
+  const int g0 = i / (grp * npair) * grp, rem = i - g0 * npair;
+  const int gs = BH - g0 < grp ? BH - g0 : grp;
+  *qp = npair - 1 - rem / gs;
+  *bh = g0 + rem % gs;
+}
+__device__ __forceinline__ FwdItem fwd_decode(int i, int BH, int npair, int grp, int nkb_all, int T_) {
+  FwdItem it;
+  int qp;
+  fwd_item_pos(i, BH, npair, grp, &it.bh, &qp);
+  it.qb0 = 2 * qp;
+  it.nkb0 = min(it.qb0 + 1, nkb_all);
+  it.nkb1 = (it.qb0 + 1) * BQ < T_ ? min(it.qb0 + 2, nkb_all) : 0;
+  it.nkb = max(it.nkb0, it.nkb1);
+  return it;
+}
 
 // DROP: attention-probability dropout (R38): the P stored for P V is D(P) (one Philox call
 // per 8 keys of the thread's query row), the normaliser l and the LSE keep the undropped P
-template <int DH, bool TSA, bool DROP>
+template <int DH, bool DROP>
 __global__ void __launch_bounds__(384, 1)
-    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap tm, const bf16* __restrict__ qkv, bf16* __restrict__ o,
-                        float* __restrict__ lse, int T_, int h, const Drop drop) {
-  using C = Cfg2<DH, TSA>;
+    attn_fwd3_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o, float* __restrict__ lse, int T_,
+                        int h, int BH, int grp, const Drop drop) {
+  using C = Cfg2<DH>;
   constexpr int NS = C::NSLOT;
   (void)drop;
   // of 8 pairs on the FMA pipe: MUFU.EX2 (16/clk/SM) keeps pace with the MMAs at d_h = 128 but
@@ -280,34 +318,29 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQ = sm;                        // tile t at + t * NP * PANEL
   uint8_t* sR = sQ + C::Q_BYTES;           // ring slot s at + s * SLOT
   uint64_t* bars = (uint64_t*)(sR + NS * C::SLOT);
-  uint64_t* q_full = bars;                 // [1]
-  uint64_t* r_full = bars + 1;             // [NS]
-  uint64_t* r_empty = bars + 1 + NS;       // [NS]
-  uint64_t* s_full = bars + 1 + 2 * NS;    // [2]
+  uint64_t* r_full = bars;                 // [NS]
+  uint64_t* r_empty = bars + NS;           // [NS]
+  uint64_t* q_full = bars + 2 * NS;        // [2]
+  uint64_t* q_empty = q_full + 2;          // [2]
+  uint64_t* s_full = q_empty + 2;          // [2]
   uint64_t* p_full = s_full + 2;           // [2]
   uint64_t* o_full = p_full + 2;           // [2]
   uint32_t* tmem_slot = (uint32_t*)(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int npair = (T_ + 2 * BQ - 1) / (2 * BQ);
-  const int qp = npair - 1 - blockIdx.x;   // heavy (late) query pairs first
-  const int bh = blockIdx.y, b = bh / h, hh = bh % h;
+  const int n_items = npair * BH, G = gridDim.x, c = blockIdx.x;
   const int d = h * DH;
   const int nkb_all = (T_ + BKV - 1) / BKV;
-  // tile t covers queries [128 (2 qp + t), +128); it sees key blocks 0 .. 2 qp + t
-  const int qb0 = 2 * qp, qb1 = 2 * qp + 1;
-  const int nkb0 = min(qb0 + 1, nkb_all);
-  const int nkb1 = qb1 * BQ < T_ ? min(qb1 + 1, nkb_all) : 0;
-  const int nkb = max(nkb0, nkb1);
-  const int row0 = b * T_;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, C::TSA ? 256 : 1);   // TSA: the softmax threads store their Q rows into TMEM
     for (int s = 0; s < NS; ++s) {
       mbar_init(&r_full[s], 1);
       mbar_init(&r_empty[s], 1);
     }
     for (int t = 0; t < 2; ++t) {
+      mbar_init(&q_full[t], 1);
+      mbar_init(&q_empty[t], 1);
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 128);
       mbar_init(&o_full[t], 1);
@@ -329,21 +362,36 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-      const int ntile = nkb1 > 0 ? 2 : 1;
-      if (!C::TSA) {
-        mbar_expect_tx(q_full, ntile * C::NP * C::PANEL);
-        for (int t = 0; t < ntile; ++t)
-          for (int p = 0; p < C::NP; ++p)
-            tma_load(sQ + (t * C::NP + p) * C::PANEL, &tm, q_full, hh * DH + 64 * p, row0 + (qb0 + t) * BQ);
-      }
-      // ring positions: K_j at 2j, V_j at 2j + 1
-      for (int pos = 0; pos < 2 * nkb; ++pos) {
-        const int s = pos % NS, use = pos / NS, j = pos >> 1;
+      int pos = 0;
+      uint32_t qn[2] = {0, 0};   // Q loads per tile so far
+      auto ring = [&](int col, int row) {
+        const int s = pos % NS, use = pos / NS;
         mbar_wait(&r_empty[s], (use & 1) ^ 1);
         uint8_t* dst = sR + s * C::SLOT;
         mbar_expect_tx(&r_full[s], C::SLOT);
-        const int col = ((pos & 1) ? 2 * d : d) + hh * DH;
-        for (int p = 0; p < C::NP; ++p) tma_load(dst + p * C::PANEL, &tm, &r_full[s], col + 64 * p, row0 + j * BKV);
+        for (int p = 0; p < C::NP; ++p) tma_load(dst + p * C::PANEL, &tm, &r_full[s], col + 64 * p, row);
+        ++pos;
+      };
+      auto load_q = [&](int t, int col, int row) {
+        mbar_wait(&q_empty[t], (qn[t] & 1) ^ 1);   // the previous item's S_t MMAs have read Q_t
+        ++qn[t];
+        mbar_expect_tx(&q_full[t], C::NP * C::PANEL);
+        for (int p = 0; p < C::NP; ++p) tma_load(sQ + (t * C::NP + p) * C::PANEL, &tm, &q_full[t], col + 64 * p, row);
+      };
+      for (int r = 0;; ++r) {
+        const int i = fwd_item(r, c, G);
+        if (i >= n_items) break;
+        const FwdItem it = fwd_decode(i, BH, npair, grp, nkb_all, T_);
+        const int row0 = (it.bh / h) * T_, hh = it.bh % h;
+        const int kc = d + hh * DH, vc = 2 * d + hh * DH;
+        // Q0, K_0, Q1, then V_0, K_1, V_1, ...: the next item's first S needs only its Q_t and K_0
+        load_q(0, hh * DH, row0 + it.qb0 * BQ);
+        ring(kc, row0);
+        if (it.nkb1 > 0) load_q(1, hh * DH, row0 + (it.qb0 + 1) * BQ);
+        for (int j = 0; j < it.nkb; ++j) {
+          ring(vc, row0 + j * BKV);
+          if (j + 1 < it.nkb) ring(kc, row0 + (j + 1) * BKV);
+        }
       }
     }
   } else if (warp == 1) {
@@ -354,62 +402,92 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t dq0 = desc_sw128(smem_u32(sQ), 16, 1024);          // Q tiles, K-major
     const uint64_t dk0 = desc_sw128(smem_u32(sR), 16, 1024);          // ring slots as K (K-major)
     const uint64_t dv0 = desc_sw128(smem_u32(sR), C::PANEL, 1024);    // ring slots as V (MN-major)
+    uint32_t qc[2] = {0, 0}, pc[2] = {0, 0};   // Q tiles / P tiles consumed per tile
     auto wait_pos = [&](int pos) {
       mbar_wait(&r_full[pos % NS], (pos / NS) & 1);
       fence_after();
-    };
-    auto issue_s = [&](int t, int j) {   // S_t(j) = Q_t K_j^T; K_j resident
-      if (elected) {
-        const uint64_t q = dq0 + (uint64_t)((t * C::NP * C::PANEL) >> 4);
-        const uint64_t k = dk0 + (uint64_t)((((2 * j) % NS) * C::SLOT) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * C::PANEL + (kk & 3) * 32) >> 4;
-          if constexpr (C::TSA) mma_ts(tbase + C::S_COL + 128 * t, tbase + C::Q_COL + 128 * t + 8 * kk, k + off, id_s, kk > 0);
-          else mma(tbase + C::S_COL + 128 * t, q + off, k + off, id_s, kk > 0);
-        }
-        commit(&s_full[t]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {   // O_t += P_t(j) V_j
-      mbar_wait(&p_full[t], j & 1);
-      fence_after();
-      if (elected) {
-        const uint64_t v = dv0 + (uint64_t)((((2 * j + 1) % NS) * C::SLOT) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tbase + C::O_COL + 128 * t, tbase + C::S_COL + 128 * t + 8 * kk, v + kk * 128, id_o,
-                 (j > 0 || kk > 0) ? 1u : 0u);
-      }
-      __syncwarp();
     };
     auto release = [&](int pos) {
       if (elected) commit(&r_empty[pos % NS]);
       __syncwarp();
     };
-    mbar_wait(q_full, 0);
-    wait_pos(0);
-    if (nkb0 > 0) issue_s(0, 0);
-    if (nkb1 > 0) issue_s(1, 0);
-    release(0);
-    for (int j = 0; j < nkb; ++j) {
-      wait_pos(2 * j + 1);   // V_j
-      const bool more = j + 1 < nkb;
-      if (more) wait_pos(2 * j + 2);   // K_{j+1}
-      if (j < nkb0) {
-        issue_pv(0, j);
-        if (j + 1 < nkb0) issue_s(0, j + 1);
-        else if (elected) commit(&o_full[0]);
-      }
-      if (j < nkb1) {
-        issue_pv(1, j);
-        if (j + 1 < nkb1) issue_s(1, j + 1);
-        else if (elected) commit(&o_full[1]);
+    auto issue_s = [&](int t, int kpos, bool last) {   // S_t = Q_t K^T, K at ring position kpos (resident)
+      if (elected) {
+        const uint64_t q = dq0 + (uint64_t)((t * C::NP * C::PANEL) >> 4);
+        const uint64_t k = dk0 + (uint64_t)(((kpos % NS) * C::SLOT) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * C::PANEL + (kk & 3) * 32) >> 4;
+          mma(tbase + C::S_COL + 128 * t, q + off, k + off, id_s, kk > 0);
+        }
+        commit(&s_full[t]);
+        if (last) commit(&q_empty[t]);   // Q_t may be replaced once these MMAs are done
       }
       __syncwarp();
-      release(2 * j + 1);
-      if (more) release(2 * j + 2);
+    };
+    auto issue_pv = [&](int t, int vpos, bool first) {   // O_t (+)= P_t V, V at ring position vpos
+      mbar_wait(&p_full[t], pc[t] & 1);
+      ++pc[t];
+      fence_after();
+      if (elected) {
+        const uint64_t v = dv0 + (uint64_t)(((vpos % NS) * C::SLOT) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tbase + C::O_COL + 128 * t, tbase + C::S_COL + 128 * t + 8 * kk, v + kk * 128, id_o,
+                 (!first || kk > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+    };
+    // S_t(0) of an item: its Q_t and K_0 resident; K_0 released once every tile of the item has it
+    int base = 0, s0_cur = 0, s0_next = 0;
+    auto issue_s0 = [&](int t, const FwdItem& it, int kpos, int* done) {
+      mbar_wait(&q_full[t], qc[t] & 1);
+      ++qc[t];
+      wait_pos(kpos);
+      issue_s(t, kpos, (t ? it.nkb1 : it.nkb0) == 1);
+      if (++*done == (it.nkb1 > 0 ? 2 : 1)) release(kpos);
+    };
+    bool pre[2] = {false, false};   // S_t(0) of the current item issued at the end of the previous one
+    for (int r = 0;; ++r) {
+      const int i = fwd_item(r, c, G);
+      if (i >= n_items) break;
+      const FwdItem it = fwd_decode(i, BH, npair, grp, nkb_all, T_);
+      const int ni = fwd_item(r + 1, c, G);
+      const bool has_next = ni < n_items;
+      FwdItem nx = it;
+      if (has_next) nx = fwd_decode(ni, BH, npair, grp, nkb_all, T_);
+      const int nbase = base + 2 * it.nkb;
+      s0_cur = s0_next;
+      s0_next = 0;
+      if (!pre[0]) issue_s0(0, it, base, &s0_cur);
+      if (it.nkb1 > 0 && !pre[1]) issue_s0(1, it, base, &s0_cur);
+      pre[0] = pre[1] = false;
+      for (int j = 0; j < it.nkb; ++j) {
+        wait_pos(base + 2 * j + 1);   // V_j
+        const bool more = j + 1 < it.nkb;
+        if (more) wait_pos(base + 2 * j + 2);   // K_{j+1}
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int nk = t ? it.nkb1 : it.nkb0;
+          if (j < nk) {
+            issue_pv(t, base + 2 * j + 1, j == 0);
+            if (j + 1 < nk) {
+              issue_s(t, base + 2 * j + 2, j + 2 == nk);
+            } else {
+              if (elected) commit(&o_full[t]);
+              __syncwarp();
+              // the next item's S_t(0) under this item's remaining blocks / epilogues
+              if (has_next && (t == 0 || nx.nkb1 > 0)) {
+                issue_s0(t, nx, nbase, &s0_next);
+                pre[t] = true;
+              }
+            }
+          }
+        }
+        release(base + 2 * j + 1);
+        if (more) release(base + 2 * j + 2);
+      }
+      base = nbase;
     }
   }
   } else {
@@ -418,131 +496,133 @@ __global__ void __launch_bounds__(384, 1)
     const int t = (warp - 4) >> 2;
     const int qw = warp & 3;
     const int r = 32 * qw + lane;
-    const int qb = qb0 + t;
-    const int qi = qb * BQ + r;
-    const int my_nkb = t ? nkb1 : nkb0;
     const uint32_t lane_addr = tbase + ((uint32_t)(32 * qw) << 16);
     const uint32_t s_addr = lane_addr + C::S_COL + 128 * t, o_addr = lane_addr + C::O_COL + 128 * t;
     const float sc = rsqrtf((float)DH) * LOG2E;
-    if constexpr (C::TSA) {   // this thread's Q row into TMEM (zeros beyond T_)
-      row_to_tmem<DH>(lane_addr + C::Q_COL + 128 * t, qkv + ((long)row0 + qi) * 3 * d + hh * DH, qi < T_);
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(q_full);
-    }
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < my_nkb; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      fence_after();
-      uint32_t raw[BKV];
+    uint32_t sn = 0, on = 0;   // S tiles / O results consumed
+    for (int rr = 0;; ++rr) {
+      const int i = fwd_item(rr, c, G);
+      if (i >= n_items) break;
+      const FwdItem it = fwd_decode(i, BH, npair, grp, nkb_all, T_);
+      const int my_nkb = t ? it.nkb1 : it.nkb0;
+      if (my_nkb == 0) continue;
+      const int bh = it.bh, b = bh / h, hh = bh % h;
+      const int qb = it.qb0 + t;
+      const int qi = qb * BQ + r;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < my_nkb; ++j) {
+        mbar_wait(&s_full[t], sn & 1);
+        ++sn;
+        fence_after();
+        uint32_t raw[BKV];
 #pragma unroll
-      for (int c = 0; c < BKV; c += 32) tmem_ld32(s_addr + c, raw + c);
-      tmem_wait_ld();
-      const bool masked = j == qb || (j + 1) * BKV > T_;
-      if (masked) {
+        for (int cc = 0; cc < BKV; cc += 32) tmem_ld32(s_addr + cc, raw + cc);
+        tmem_wait_ld();
+        const bool masked = j == qb || (j + 1) * BKV > T_;
+        if (masked) {   // keys j BKV + cc > min(qi, T_ - 1): one compare-select per score
+          const int lim = min(qi, T_ - 1) - j * BKV;
 #pragma unroll
-        for (int c = 0; c < BKV; ++c) {
-          const int kj = j * BKV + c;
-          if (kj > qi || kj >= T_) raw[c] = __float_as_uint(-INFINITY);
+          for (int cc = 0; cc < BKV; ++cc)
+            if (cc > lim) raw[cc] = __float_as_uint(-INFINITY);
         }
-      }
-      // row max of the raw scores (sc > 0, so max and scaling commute), four independent chains
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // row max of the raw scores (sc > 0, so max and scaling commute), four independent chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < BKV; c += 8)
+        for (int cc = 0; cc < BKV; cc += 8)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          m4[q] = fmaxf(m4[q], fmaxf(__uint_as_float(raw[c + 2 * q]), __uint_as_float(raw[c + 2 * q + 1])));
-      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sc;
-      const bool need = mx > m_ref + RESCALE_THRESHOLD;
-      const float new_ref = need ? mx : m_ref;
-      const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
-      // PV_t(j-1) completed before s_full[t] fired for S_t(j): O_t is stable here
-      if (__any_sync(0xffffffffu, need) && j > 0) {
+          for (int q = 0; q < 4; ++q)
+            m4[q] = fmaxf(m4[q], fmaxf(__uint_as_float(raw[cc + 2 * q]), __uint_as_float(raw[cc + 2 * q + 1])));
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sc;
+        const bool need = mx > m_ref + RESCALE_THRESHOLD;
+        const float new_ref = need ? mx : m_ref;
+        const float alpha = (m_ref == -INFINITY) ? 0.f : fast_exp2(m_ref - new_ref);
+        // PV_t(j-1) completed before s_full[t] fired for S_t(j): O_t is stable here
+        if (__any_sync(0xffffffffu, need) && j > 0) {
 #pragma unroll
-        for (int c = 0; c < DH; c += 16) {
-          uint32_t ov[16];
-          tmem_ld16(o_addr + c, ov);
-          tmem_wait_ld();
+          for (int cc = 0; cc < DH; cc += 16) {
+            uint32_t ov[16];
+            tmem_ld16(o_addr + cc, ov);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-          tmem_st16(o_addr + c, ov);
-        }
-      }
-      l *= alpha;
-      m_ref = new_ref;
-      // P = 2^(raw sc - m_ref) on packed fp32 pairs -> bf16 pairs into TMEM over S (16 columns =
-      // 32 keys per store). Unmasked blocks send POLY of every 8 pairs to the FMA-pipe exponential;
-      // the two variants are separate code paths (a shared, predicated loop issued both).
-      const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(-m_ref, -m_ref);
-      auto p_block = [&](auto use_poly) {
-        uint64_t rs2[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c16 = 0; c16 < BKV / 32; ++c16) {
-          uint32_t keep = 0xFFFFFFFFu;   // bit c: key j BKV + 32 c16 + c kept
-          if constexpr (DROP) {
-            const uint64_t g0 = ((((uint64_t)bh * T_ + qi) * T_) >> 3) + (uint64_t)(j * BKV + 32 * c16) / 8;
-            keep = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) keep |= drop_keep8(drop, (uint32_t)(g0 + q)) << (8 * q);
+            for (int q = 0; q < 16; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
+            tmem_st16(o_addr + cc, ov);
           }
-          uint32_t pk[16];
+        }
+        l *= alpha;
+        m_ref = new_ref;
+        // P = 2^(raw sc - m_ref) on packed fp32 pairs -> bf16 pairs into TMEM over S (16 columns =
+        // 32 keys per store). Unmasked blocks send POLY of every 8 pairs to the FMA-pipe exponential;
+        // the two variants are separate code paths (a shared, predicated loop issued both).
+        const uint64_t sc2 = f2pack(sc, sc), nref2 = f2pack(-m_ref, -m_ref);
+        auto p_block = [&](auto use_poly) {
+          uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int c = c16 * 32 + 2 * i;
-            const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[c]), __uint_as_float(raw[c + 1])), sc2, nref2);
-            uint64_t p2;
-            if (decltype(use_poly)::value && (i & 7) < POLY) {
-              p2 = exp2_poly2(x2);
-            } else {
-              float x0, x1;
-              f2unpack(x2, x0, x1);
-              p2 = f2pack(fast_exp2(x0), fast_exp2(x1));
-            }
-            rs2[i & 3] = fadd2(rs2[i & 3], p2);
-            float p0, p1;
-            f2unpack(p2, p0, p1);
+          for (int c16 = 0; c16 < BKV / 32; ++c16) {
+            uint32_t keep = 0xFFFFFFFFu;   // bit c: key j BKV + 32 c16 + c kept
+            (void)keep;
             if constexpr (DROP) {
-              p0 = (keep >> (2 * i)) & 1u ? p0 * drop.scale : 0.f;
-              p1 = (keep >> (2 * i + 1)) & 1u ? p1 * drop.scale : 0.f;
+              const uint64_t g0 = ((((uint64_t)bh * T_ + qi) * T_) >> 3) + (uint64_t)(j * BKV + 32 * c16) / 8;
+              keep = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) keep |= drop_keep8(drop, (uint32_t)(g0 + q)) << (8 * q);
             }
-            __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-            pk[i] = *(uint32_t*)&v2;
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int cc = c16 * 32 + 2 * q;
+              const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[cc]), __uint_as_float(raw[cc + 1])), sc2, nref2);
+              uint64_t p2;
+              if (decltype(use_poly)::value && (q & 7) < POLY) {
+                p2 = exp2_poly2(x2);
+              } else {
+                float x0, x1;
+                f2unpack(x2, x0, x1);
+                p2 = f2pack(fast_exp2(x0), fast_exp2(x1));
+              }
+              rs2[q & 3] = fadd2(rs2[q & 3], p2);
+              float p0, p1;
+              f2unpack(p2, p0, p1);
+              if constexpr (DROP) {
+                p0 = (keep >> (2 * q)) & 1u ? p0 * drop.scale : 0.f;
+                p1 = (keep >> (2 * q + 1)) & 1u ? p1 * drop.scale : 0.f;
+              }
+              __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+              pk[q] = *(uint32_t*)&v2;
+            }
+            tmem_st16(s_addr + 16 * c16, pk);
           }
-          tmem_st16(s_addr + 16 * c16, pk);
-        }
-        const uint64_t r = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
-        float r0, r1;
-        f2unpack(r, r0, r1);
-        return r0 + r1;
-      };
-      if (POLY == 0 || masked) l += p_block(std::false_type{});
-      else l += p_block(std::true_type{});
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(&p_full[t]);
-    }
-    if (my_nkb > 0) {
-      mbar_wait(&o_full[t], 0);
+          const uint64_t rsum = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+          float r0, r1;
+          f2unpack(rsum, r0, r1);
+          return r0 + r1;
+        };
+        if (POLY == 0 || masked) l += p_block(std::false_type{});
+        else l += p_block(std::true_type{});
+        tmem_wait_st();
+        fence_before();
+        mbar_arrive(&p_full[t]);
+      }
+      mbar_wait(&o_full[t], on & 1);
+      ++on;
       fence_after();
       const float inv = 1.f / l;
       bf16* orow = o + ((long)b * T_ + qi) * d + hh * DH;
       uint32_t ov[DH];   // all loads in flight, one wait
 #pragma unroll
-      for (int c = 0; c < DH; c += 16) tmem_ld16(o_addr + c, ov + c);
+      for (int cc = 0; cc < DH; cc += 16) tmem_ld16(o_addr + cc, ov + cc);
       tmem_wait_ld();
       if (qi < T_) {
 #pragma unroll
-        for (int c = 0; c < DH; c += 16) {
+        for (int cc = 0; cc < DH; cc += 16) {
           uint32_t pk[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(ov[c + 2 * i]) * inv,
-                                                      __uint_as_float(ov[c + 2 * i + 1]) * inv);
-            pk[i] = *(uint32_t*)&v2;
+          for (int q = 0; q < 8; ++q) {
+            __nv_bfloat162 v2 = __floats2bfloat162_rn(__uint_as_float(ov[cc + 2 * q]) * inv,
+                                                      __uint_as_float(ov[cc + 2 * q + 1]) * inv);
+            pk[q] = *(uint32_t*)&v2;
           }
-          *(uint4*)(orow + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *(uint4*)(orow + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          *(uint4*)(orow + cc) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *(uint4*)(orow + cc + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
         lse[((long)b * h + hh) * T_ + qi] = (m_ref + log2f(l)) / LOG2E;
       }
@@ -1291,8 +1371,9 @@ __global__ void dsum_tc_kernel(const bf16* __restrict__ o, const bf16* __restric
   Dsum[(b * h + hh) * T_ + t] = s;
 }
 
-// Fixed MMA operands in TMEM (TS MMAs, d_h <= 80) per kernel: bit 0 forward Q, bit 1 dK/dV K,V,
-// bit 2 dQ Q,dO. Default: dQ only (measured: it helps the dQ kernel, slows the other two).
+// Fixed MMA operands in TMEM (TS MMAs, d_h <= 80) per backward kernel: bit 1 dK/dV K,V, bit 2 the
+// recomputing dQ kernel's Q,dO. Default: dQ only (measured: it helps that kernel, slows dK/dV; the
+// persistent forward keeps Q in shared memory, where the next item's Q is loaded while it runs).
 // ATOM_ATTN_TSA=<mask> overrides for A/B runs.
 static bool tsa_mask(int bit) {
   const char* e = getenv("ATOM_ATTN_TSA");
@@ -1313,6 +1394,43 @@ static PFN_encodeTiled encoder() {
       fn = (PFN_encodeTiled)p;
   }
   return fn;
+}
+
+// Heads per item group of the persistent forward: among power-of-two group sizes whose K / V
+// (128 padded columns x 2 B x 2 tensors per key) fit in 32 MB of L2, the one whose snake deal
+// gives the smallest per-CTA maximum of (key blocks + 2.5 blocks of per-item cost) -- a host-side
+// simulation of the kernel's own item order, cached per shape
+static int fwd_group(int BH, int npair, int T_, int G) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, int> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(BH, npair, T_, G);
+  auto f = memo.find(key);
+  if (f != memo.end()) return f->second;
+  const int nkb_all = (T_ + BKV - 1) / BKV;
+  const long n = (long)BH * npair;
+  std::vector<double> load(G);
+  int best = 1;
+  double best_max = 1e300;
+  for (int grp = 1; grp <= BH; grp *= 2) {
+    if (grp > 1 && (double)grp * T_ * 512.0 > 32.0 * (1 << 20)) break;
+    std::fill(load.begin(), load.end(), 0.0);
+    for (long i = 0; i < n; ++i) {
+      int bh, qp;
+      fwd_item_pos((int)i, BH, npair, grp, &bh, &qp);
+      const int nkb0 = std::min(2 * qp + 1, nkb_all);
+      const int nkb1 = (2 * qp + 1) * BQ < T_ ? std::min(2 * qp + 2, nkb_all) : 0;
+      const long r = i / G, c = i % G;
+      load[(r & 1) ? G - 1 - c : c] += nkb0 + nkb1 + 2.5;
+    }
+    const double mx = *std::max_element(load.begin(), load.end());
+    if (mx < best_max * 0.999) {
+      best_max = mx;
+      best = grp;
+    }
+  }
+  memo[key] = best;
+  return best;
 }
 
 template <int DH>
@@ -1339,23 +1457,28 @@ bool fwd(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, cudaStream_
     return false;
   }
   static bool once = false;
-  static bool tsa = false;
+  static int sms = 0;
   if (!once) {
-#define ATOM_FWD_ATTR(TS, DR)                                                                                      \
-  ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd2_tc_kernel<DH, TS, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                    Cfg2<DH>::SMEM));
-    ATOM_FWD_ATTR(false, false) ATOM_FWD_ATTR(true, false) ATOM_FWD_ATTR(false, true) ATOM_FWD_ATTR(true, true)
-#undef ATOM_FWD_ATTR
-    tsa = tsa_mask(0);
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd3_tc_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg2<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_fwd3_tc_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg2<DH>::SMEM));
+    int dev = 0;
+    ATOM_CUDA_OK(cudaGetDevice(&dev));
+    ATOM_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     once = true;
   }
-  dim3 grid((T_ + 2 * BQ - 1) / (2 * BQ), B * h);
-  const bool dr = drop.thr != 0;
-  if (tsa && dr) attn_fwd2_tc_kernel<DH, true, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
-  else if (tsa) attn_fwd2_tc_kernel<DH, true, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
-  else if (dr) attn_fwd2_tc_kernel<DH, false, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
-  else attn_fwd2_tc_kernel<DH, false, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, qkv, o, lse, T_, h, drop);
-  static const std::string name = std::string("attn_fwd2<") + std::to_string(DH) + ">";
+  // persistent: one CTA per SM (or per item when there are fewer items)
+  const int npair = (T_ + 2 * BQ - 1) / (2 * BQ);
+  const long n_items = (long)npair * B * h;
+  const int grid = (int)(n_items < sms ? n_items : sms);
+  if (grid == 0) return true;
+  const int grp = fwd_group(B * h, npair, T_, grid);
+  if (drop.thr)
+    attn_fwd3_tc_kernel<DH, true><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, o, lse, T_, h, B * h, grp, drop);
+  else
+    attn_fwd3_tc_kernel<DH, false><<<grid, 384, Cfg2<DH>::SMEM, st>>>(tm, o, lse, T_, h, B * h, grp, drop);
+  static const std::string name = std::string("attn_fwd3<") + std::to_string(DH) + ">";
   count_launch(name.c_str());
   ATOM_CUDA_OK(cudaGetLastError());
   return true;

@@ -22,7 +22,10 @@ def ref_attention(qkv, B, T, h, dh):
 
 CASES = [(2, 128, 2, 64), (1, 300, 3, 64), (2, 256, 2, 128), (1, 384, 2, 128), (1, 200, 2, 80), (2, 256, 4, 80),
          (1, 2048, 2, 128), (2, 50, 2, 64), (3, 640, 2, 80), (1, 1, 1, 128), (1, 1024, 2, 64),
-         (2, 1024, 2, 80)]
+         (2, 1024, 2, 80),
+         # more work items than SMs: the persistent forward walks several items per CTA, including
+         # pairs whose second tile lies beyond T (T % 256 in (0, 128]) and ragged last blocks
+         (8, 640, 16, 80), (16, 300, 8, 80), (4, 1000, 12, 64), (2, 2048, 24, 128)]
 
 
 @pytest.mark.parametrize("impl", [atom.ATTN_TC, atom.ATTN_MMA], ids=["tcgen05", "mma_sync"])
@@ -49,7 +52,7 @@ BWD_CASES = [(2, 256, 2, 64), (1, 200, 2, 80), (1, 384, 2, 128), (1, 300, 3, 64)
 def test_attention_backward(impl, case):
     B, T, h, dh = case
     if impl == atom.ATTN_TC_DS and T % 64:
-        pytest.skip("the dS^T path needs T % 64 == 0 (the step falls back to the recomputing dQ kernel)")
+        pytest.skip("ragged T: the dS^T kernels run at T % 128 == 0 (else the recomputing dQ kernel)")
     g = torch.Generator(device="cuda").manual_seed(2)
     qkv = (torch.randn(B * T, 3 * h * dh, generator=g, device="cuda")).bfloat16()
     dout = torch.randn(B * T, h * dh, generator=g, device="cuda").bfloat16()

@@ -71,9 +71,9 @@ def wide_step():
 
 def test_wide_step_ran_the_bench_kernels(wide_step):
     ran = wide_step["ran"]
-    for k in ("gemm_tc2<0,0>", "gemm_tc2<0,1>", "gemm_tc2<1,1>", "attn_fwd2<80>", "attn_bwd_dkv2<80>"):
+    for k in ("gemm_tc2<0,0>", "gemm_tc2<0,1>", "gemm_tc2<1,1>", "attn_fwd3<80>", "attn_bwd_dkv2<80>"):
         assert ran.get(k, 0) > 0, (k, ran)
-    # the dQ kernel of the step's path (whichever atom_step uses at T % 64 == 0)
+    # the dQ kernel of the step's path (dQ from dS^T at T % 128 == 0, else the recomputing one)
     assert ran.get("attn_bwd_dq_ds<80>", 0) + ran.get("attn_bwd_dq2<80>", 0) > 0, ran
     assert not any(k.startswith(("gemm_tc<", "gemm_simt", "attn_fwd_v1")) for k, v in ran.items() if v), ran
 
