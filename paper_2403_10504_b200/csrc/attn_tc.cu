@@ -4,7 +4,7 @@
 //   forward   attn_fwd3_tc_kernel: persistent, one CTA per SM over (b h, query pair) items; two
 //             128-query tiles ping-pong between two softmax warpgroups (thread = query row = TMEM
 //             lane), P written back over S in TMEM as the A operand of O += P V
-//   backward  dsum_tc_kernel (D = rowsum(dO o)), attn_bwd_dkv2_kernel (dK, dV per 128-key block;
+//   backward  dsum_tc_kernel (D = rowsum(dO o)), attn_bwd_dkv4_kernel (dK, dV per 128-key block;
 //             optionally writes dS^T), then attn_bwd_dq_ds_kernel (dQ = dS K from dS^T) or, without
 //             the dS^T buffer, attn_bwd_dq2_kernel (dQ recomputing S and dP)
 // K / V / Q tiles are loaded by TMA in [rows, 64 features] 128B-swizzled panels; V (and Q, dO in the
@@ -640,25 +640,25 @@ __global__ void __launch_bounds__(384, 1)
 // Backward (deterministic, no atomics), P and dS recomputed from the stashed LSE:
 //   dK/dV kernel, one CTA per (b, h, 128-key block), loops over 64-query blocks i >= it:
 //     S^T = K Q_i^T, dP^T = V dO_i^T (TMEM); thread = key row: P^T = exp(S^T/sqrt(dh) - lse_q),
-//     dS^T = P^T (dP^T - D_q) -> bf16 swizzled smem; dV += P^T dO_i, dK += dS^T Q_i (TMEM)
-//   dQ kernel, one CTA per (b, h, 128-query block), loops over 64-key blocks j <= it:
+//     dS^T = P^T (dP^T - D_q); dV += P^T dO_i, dK += dS^T Q_i (TMEM); optionally dS^T -> HBM
+//   dQ kernel: dQ = dS K from that dS^T (attn_bwd_dq_ds_kernel), or, without the dS^T buffer,
+//     one CTA per (b, h, 128-query block) looping over 64-key blocks j <= it:
 //     S = Q K_j^T, dP = dO V_j^T; thread = query row: dS = P (dP - D); dQ += dS K_j
-// D = rowsum(dO * O) comes from fa::dsum_kernel.
+// D = rowsum(dO * O) comes from dsum_tc_kernel.
 // ======================================================================================
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // ======================================================================================
-// Backward v2. Same math and block shapes as above, re-organised for the tensor core:
-//   * P^T / dS^T (dK/dV kernel) and dS (dQ kernel) go back into TMEM over the S / dP columns
-//     they were computed from and feed the next MMAs as TMEM A operands (no smem round trip);
-//   * 4-stage TMA rings for the streamed tiles (a 2-stage ring left TMA latency exposed);
+// Recomputing dQ kernel (the path without the dS^T buffer), organised for the tensor core:
+//   * dS goes back into TMEM over the S / dP columns it was computed from and feeds dQ += dS K as
+//     the TMEM A operand (no smem round trip);
+//   * 4-stage TMA rings for the streamed K, V tiles (a 2-stage ring left TMA latency exposed);
 //   * two elementwise warpgroups, each on half of the 64 columns of a block (warps w and w+4
 //     share TMEM lanes; a 64-thread named barrier per lane quarter orders their loads before
 //     the in-place stores);
-//   * the streamed per-query LSE / D values are staged by the producer warp with the tiles;
 //   * the causal mask is applied only on the blocks that straddle the diagonal.
-// Key rows beyond T_ (dK/dV kernel) and query rows beyond T_ (dQ kernel) produce values that
-// are never stored; every result row depends only on its own TMEM lane.
+// Query rows beyond T_ produce values that are never stored; every result row depends only on
+// its own TMEM lane.
 // ======================================================================================
 constexpr int BW_NST = 4;   // ring stages
 
@@ -666,12 +666,11 @@ template <int DH, bool TSA_ = false>
 struct BCfg2 {
   static constexpr int NP = (DH + 63) / 64;
   static constexpr int P128 = 128 * 128, P64 = 64 * 128;
-  static constexpr int FIX = 2 * NP * P128;          // K,V (dK/dV kernel) or Q,dO (dQ kernel)
-  static constexpr int STG = 2 * NP * P64;           // Q_i,dO_i or K_j,V_j: 64 rows each
-  static constexpr int DS_STG = 128 * 128;           // dK/dV kernel: one dS^T tile (128 keys x 64 queries) for its TMA store
-  static constexpr int SMEM = FIX + BW_NST * STG + DS_STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
-  // d_h <= 80: the per-CTA fixed operands (K, V or Q, dO) live in TMEM as A operands of S / dP
-  // (TS MMAs: no shared-memory A reads, which bound the SS MMAs); d_h = 128 has no TMEM room
+  static constexpr int FIX = 2 * NP * P128;          // Q, dO of the CTA's 128 queries
+  static constexpr int STG = 2 * NP * P64;           // K_j, V_j: 64 rows each
+  static constexpr int SMEM = FIX + BW_NST * STG + BW_NST * 2 * 64 * 4 + 1024 + 512;
+  // d_h <= 80: the per-CTA fixed operands (Q, dO) live in TMEM as A operands of S / dP (TS MMAs:
+  // no shared-memory A reads, which bound the SS MMAs); d_h = 128 has no TMEM room
   static constexpr bool TSA = TSA_ && DH <= 80;
   static constexpr uint32_t AL16(uint32_t x) { return (x + 15) / 16 * 16; }
   static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256;   // buffer u: +128u
@@ -707,29 +706,52 @@ __device__ __forceinline__ uint32_t drop_keep_keyrow(const Drop& dr, uint64_t ro
   return w;
 }
 
-// DROP: dV += D(P)^T dO and dS^T = P^T (D(dP^T) - D_q) with the forward's mask regenerated
-// (drop_keep_keyrow: the mask's groups run along keys, this kernel's thread is a key row)
-template <int DH, bool TSA, bool DROP>
+// ======================================================================================
+// dK / dV kernel v4: the two elementwise warpgroups ping-pong over the 64-query blocks instead of
+// splitting each block: warpgroup u owns TMEM buffer u (S^T | dP^T, 64 + 64 columns) and takes the
+// blocks it with it % 2 == u, each thread (= key row = TMEM lane) all 64 queries of the block in
+// two halves of 32.  One warpgroup's exponentials run while the other's block is on the tensor
+// core, with no barrier between them (v2 split each block across both warpgroups, which had to
+// meet at a named barrier before writing P^T / dS^T over the shared columns).  The MMA issuer
+// keeps the in-order accumulation of dV, dK (block order; deterministic): per block it waits for
+// that block's P^T / dS^T, issues dV += P^T dO and dK += dS^T Q, then S^T / dP^T of the block two
+// ahead into the freed buffer.  dS^T (store_ds) leaves through a per-warp 32-key x 64-query smem
+// box and a TMA store, staged at the top of the warpgroup's next block.
+// ======================================================================================
+constexpr int BW4_NST = 3;   // ring stages (the dS^T staging takes the fourth one's room)
+template <int DH>
+struct BCfg4 {
+  static constexpr int NP = (DH + 63) / 64;
+  static constexpr int P128 = 128 * 128, P64 = 64 * 128;
+  static constexpr int FIX = 2 * NP * P128;          // K, V of the CTA's 128 keys
+  static constexpr int STG = 2 * NP * P64;           // Q_i, dO_i: 64 rows each
+  static constexpr int DS_STG = 8 * 32 * 128;        // per elementwise warp: 32 keys x 64 queries bf16
+  static constexpr int SMEM = FIX + BW4_NST * STG + DS_STG + BW4_NST * 2 * 64 * 4 + 1024 + 512;
+  static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256, ACC1 = 384;   // buffer u: +128u
+  static_assert(SMEM <= 232448, "shared memory");
+};
+
+template <int DH, bool DROP>
 __global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkv2_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                         const __grid_constant__ CUtensorMap tm_do, const bf16* __restrict__ qkv,
-                         const float* __restrict__ lse, const float* __restrict__ Dsum, bf16* __restrict__ dqkv,
-                         int T_, int h, const Drop drop, const bool store_ds, const __grid_constant__ CUtensorMap tm_dsw) {
-  using C = BCfg2<DH, TSA>;
-  constexpr int NST = BW_NST;
+    attn_bwd_dkv4_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                         const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h, const Drop drop,
+                         const bool store_ds, const __grid_constant__ CUtensorMap tm_dsw) {
+  using C = BCfg4<DH>;
+  constexpr int NST = BW4_NST;
   constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
   uint8_t* sS = sm + C::FIX;                           // stage s: Q at + s*STG, dO at + NP*P64
-  uint8_t* sDS = sS + NST * C::STG;                    // dS^T tile staging for its TMA store (1024-aligned)
+  uint8_t* sDS = sS + NST * C::STG;                    // dS^T staging, 4 KB per elementwise warp (1024-aligned)
   float* sLD = (float*)(sDS + C::DS_STG);              // stage s: L[64] at + 128 s, D[64] at + 128 s + 64
   uint64_t* bars = (uint64_t*)(sLD + NST * 128);
   uint64_t* kv_full = bars;
   uint64_t* st_full = bars + 1;           // [NST]  TMA tx + 32 producer lanes
-  uint64_t* st_empty = bars + 1 + NST;    // [NST]
-  uint64_t* s_full = bars + 1 + 2 * NST;  // [2]
+  uint64_t* st_empty = st_full + NST;     // [NST]
+  uint64_t* s_full = st_empty + NST;      // [2]
   uint64_t* p_full = s_full + 2;          // [2]
   uint64_t* done = p_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(done + 1);
@@ -745,14 +767,14 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = b * T_;
 
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, C::TSA ? 256 : 1);   // TSA: the elementwise threads store K, V rows into TMEM
+    mbar_init(kv_full, 1);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&st_full[s], 33);
       mbar_init(&st_empty[s], 1);
     }
     for (int u = 0; u < 2; ++u) {
       mbar_init(&s_full[u], 1);
-      mbar_init(&p_full[u], 256);
+      mbar_init(&p_full[u], 128);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -770,7 +792,7 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     const float* lrow = lse + ((long)b * h + hh) * T_;
     const float* drow = Dsum + ((long)b * h + hh) * T_;
-    if (!C::TSA && lane == 0) {
+    if (lane == 0) {
       mbar_expect_tx(kv_full, C::FIX);
       for (int p = 0; p < C::NP; ++p) {
         tma_load(sK + p * C::P128, &tm_kv, kv_full, d + hh * DH + 64 * p, row0 + k0);
@@ -807,7 +829,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t dk = desc_sw128(smem_u32(sK), 16, 1024), dv = desc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t ds_k = desc_sw128(smem_u32(sS), 16, 1024);       // stage tiles, K-major
     const uint64_t ds_mn = desc_sw128(smem_u32(sS), C::P64, 1024);  // stage tiles, MN-major
-    auto issue_s = [&](int it) {
+    auto issue_s = [&](int it) {   // S^T / dP^T of block it into buffer it % 2
       const int s = it % NST, u = it & 1;
       mbar_wait(&st_full[s], (it / NST) & 1);
       fence_after();
@@ -817,22 +839,17 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
           const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
-          if constexpr (C::TSA) {
-            mma_ts(tbase + C::ST_COL + 128 * u, tbase + C::FA_COL + 8 * kk, q + ob, id_s, kk > 0);
-            mma_ts(tbase + C::DPT_COL + 128 * u, tbase + C::FB_COL + 8 * kk, g + ob, id_s, kk > 0);
-          } else {
-            mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
-            mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
-          }
+          mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
+          mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
         }
         commit(&s_full[u]);
       }
       __syncwarp();
     };
     issue_s(0);
+    if (nblk > 1) issue_s(1);
     for (int it = 0; it < nblk; ++it) {
       const int s = it % NST, u = it & 1;
-      if (it + 1 < nblk) issue_s(it + 1);
       mbar_wait(&p_full[u], (it >> 1) & 1);
       fence_after();
       if (elected) {
@@ -847,35 +864,27 @@ __global__ void __launch_bounds__(384, 1)
         if (it == nblk - 1) commit(done);
       }
       __syncwarp();
+      // buffer u is free once these products have read it (in-order execution)
+      if (it + 2 < nblk) issue_s(it + 2);
     }
   } else if (warp >= 4) {
     const int wg = (warp - 4) >> 2, qw = warp & 3;
     const int r = 32 * qw + lane, kj = k0 + r;
     const uint32_t la = tbase + ((uint32_t)(32 * qw) << 16);
+    const uint32_t st_col = la + C::ST_COL + 128 * wg, dp_col = la + C::DPT_COL + 128 * wg;
     const float sc = rsqrtf((float)DH) * LOG2E;
-    if constexpr (C::TSA) {   // K row (warpgroup 0) / V row (warpgroup 1) of this thread's key
-      row_to_tmem<DH>(la + (wg ? C::FB_COL : C::FA_COL),
-                      qkv + ((long)row0 + kj) * 3 * d + (wg ? 2 * d : d) + hh * DH, kj < T_);
-      tmem_wait_st();
-      fence_before();
-      mbar_arrive(kv_full);
-    }
-    // dS^T for the dQ kernel: each warp stages its 32 keys x 32 queries (64B-swizzled rows) in its
-    // own 2 KB smem box and lane 0 stores it with TMA (full-line writes, no block-wide barrier;
-    // per-thread 64-byte global stores had doubled this kernel's time).  The box of block it is
-    // staged at the top of block it + 1, before the waits for its MMAs, so the proxy fence's
-    // latency hides under them; lane 0 waits for its previous box to be read before reuse
-    uint32_t pend[16];
+    const uint64_t sc2 = f2pack(sc, sc);
+    const uint32_t box = smem_u32(sDS) + (uint32_t)(warp - 4) * 4096u;
+    uint32_t pend[32];   // dS^T of the warpgroup's previous block (64 queries, bf16 pairs)
     int pend_q = -1;
     auto flush_ds = [&]() {
       if (!store_ds || pend_q < 0) return;
-      const uint32_t box = smem_u32(sDS) + (uint32_t)(warp - 4) * 2048u;
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
-      const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+      const uint32_t swz = (uint32_t)(lane & 7);   // 128B swizzle: 16-byte chunk i of row l at i ^ (l % 8)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (uint32_t)lane * 64 + ((((uint32_t)i) ^ swz) << 4)),
+      for (int i = 0; i < 8; ++i)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + (uint32_t)lane * 128 + ((((uint32_t)i) ^ swz) << 4)),
                      "r"(pend[4 * i]), "r"(pend[4 * i + 1]), "r"(pend[4 * i + 2]), "r"(pend[4 * i + 3])
                      : "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -883,84 +892,88 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) {
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                          reinterpret_cast<uint64_t>(&tm_dsw)),
-                     "r"(box), "r"(pend_q + 32 * wg), "r"(bh * T_ + k0 + 32 * qw)
+                     "r"(box), "r"(pend_q), "r"(bh * T_ + k0 + 32 * qw)
                      : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       pend_q = -1;
     };
-    for (int it = 0; it < nblk; ++it) {
-      const int s = it % NST, u = it & 1, q0 = (i0 + it) * 64;
+    for (int it = wg; it < nblk; it += 2) {
+      const int s = it % NST, q0 = (i0 + it) * 64;
       flush_ds();
       mbar_wait(&st_full[s], (it / NST) & 1);   // L / D of this stage visible
-      mbar_wait(&s_full[u], (it >> 1) & 1);
+      mbar_wait(&s_full[wg], (it >> 1) & 1);
       fence_after();
-      uint32_t sv[32], dv[32];
-      tmem_ld32(la + C::ST_COL + 128 * u + 32 * wg, sv);
-      tmem_ld32(la + C::DPT_COL + 128 * u + 32 * wg, dv);
-      tmem_wait_ld();
-      const float* L = sLD + 128 * s + 32 * wg;
-      const float* D = L + 64;
       const bool masked = q0 < k0 + 128;   // block straddles the diagonal
-      uint32_t pk[16], dk[16];
-      const uint64_t sc2 = f2pack(sc, sc);
-      uint32_t keep = 0xFFFFFFFFu;   // bit c: query q0 + 32 wg + c kept at this key
-      if constexpr (DROP) keep = drop_keep_keyrow(drop, (uint64_t)bh * T_, q0 + 32 * wg, T_, kj);
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 l4 = *(const float4*)(L + 4 * c4);   // -L
-        const float4 d4 = *(const float4*)(D + 4 * c4);
+      for (int hf = 0; hf < 2; ++hf) {   // queries q0 + 32 hf .. + 31
+        uint32_t sv[32], dv[32];
+        tmem_ld32(st_col + 32 * hf, sv);
+        tmem_ld32(dp_col + 32 * hf, dv);
+        tmem_wait_ld();
+        const float* L = sLD + 128 * s + 32 * hf;
+        const float* D = L + 64;
+        uint32_t pk[16], dk[16];
+        uint32_t keep = 0xFFFFFFFFu;   // bit c: query q0 + 32 hf + c kept at this key
+        (void)keep;
+        if constexpr (DROP) keep = drop_keep_keyrow(drop, (uint64_t)bh * T_, q0 + 32 * hf, T_, kj);
+        const int lim = kj - q0 - 32 * hf;   // masked block: query c of this half is visible iff c >= lim
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c = 4 * c4 + 2 * h2;
-          const uint64_t nl2 = h2 ? f2pack(l4.z, l4.w) : f2pack(l4.x, l4.y);
-          const uint64_t d2 = h2 ? f2pack(d4.z, d4.w) : f2pack(d4.x, d4.y);
-          const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
-          uint64_t p2;
-          if (!masked && POLY && poly_pick(2 * c4 + h2, ATOM_BWD_POLY_KV)) {
-            p2 = exp2_poly2(x2);
-          } else {
-            float x0, x1;
-            f2unpack(x2, x0, x1);
-            float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
-            if (masked) {
-              if (q0 + 32 * wg + c < kj) p0 = 0.f;
-              if (q0 + 32 * wg + c + 1 < kj) p1 = 0.f;
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 l4 = *(const float4*)(L + 4 * c4);   // -L
+          const float4 d4 = *(const float4*)(D + 4 * c4);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int c = 4 * c4 + 2 * h2;
+            const uint64_t nl2 = h2 ? f2pack(l4.z, l4.w) : f2pack(l4.x, l4.y);
+            const uint64_t d2 = h2 ? f2pack(d4.z, d4.w) : f2pack(d4.x, d4.y);
+            const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
+            uint64_t p2;
+            if (!masked && POLY && poly_pick(2 * c4 + h2, ATOM_BWD_POLY_KV)) {
+              p2 = exp2_poly2(x2);
+            } else {
+              float x0, x1;
+              f2unpack(x2, x0, x1);
+              float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+              if (masked) {
+                if (c < lim) p0 = 0.f;
+                if (c + 1 < lim) p1 = 0.f;
+              }
+              p2 = f2pack(p0, p1);
             }
-            p2 = f2pack(p0, p1);
+            float e0 = __uint_as_float(dv[c]), e1 = __uint_as_float(dv[c + 1]);
+            float m0 = 1.f, m1 = 1.f;
+            if constexpr (DROP) {
+              m0 = (keep >> c) & 1u ? drop.scale : 0.f;
+              m1 = (keep >> (c + 1)) & 1u ? drop.scale : 0.f;
+              e0 *= m0;
+              e1 *= m1;
+            }
+            const uint64_t ds2 = fmul2(p2, fsub2(f2pack(e0, e1), d2));
+            float p0, p1, g0, g1;
+            f2unpack(p2, p0, p1);
+            f2unpack(ds2, g0, g1);
+            if constexpr (DROP) {   // dV takes D(P)^T
+              p0 *= m0;
+              p1 *= m1;
+            }
+            __nv_bfloat162 a2 = __floats2bfloat162_rn(p0, p1), b2 = __floats2bfloat162_rn(g0, g1);
+            pk[2 * c4 + h2] = *(uint32_t*)&a2;
+            dk[2 * c4 + h2] = *(uint32_t*)&b2;
           }
-          float e0 = __uint_as_float(dv[c]), e1 = __uint_as_float(dv[c + 1]);
-          float m0 = 1.f, m1 = 1.f;
-          if constexpr (DROP) {
-            m0 = (keep >> c) & 1u ? drop.scale : 0.f;
-            m1 = (keep >> (c + 1)) & 1u ? drop.scale : 0.f;
-            e0 *= m0;
-            e1 *= m1;
-          }
-          const uint64_t ds2 = fmul2(p2, fsub2(f2pack(e0, e1), d2));
-          float p0, p1, g0, g1;
-          f2unpack(p2, p0, p1);
-          f2unpack(ds2, g0, g1);
-          if constexpr (DROP) {   // dV takes D(P)^T
-            p0 *= m0;
-            p1 *= m1;
-          }
-          __nv_bfloat162 a2 = __floats2bfloat162_rn(p0, p1), b2 = __floats2bfloat162_rn(g0, g1);
-          pk[2 * c4 + h2] = *(uint32_t*)&a2;
-          dk[2 * c4 + h2] = *(uint32_t*)&b2;
+        }
+        // packed over this thread's own fp32 columns (read above; the other half's lie beyond)
+        tmem_st16(st_col + 16 * hf, pk);
+        tmem_st16(dp_col + 16 * hf, dk);
+        if (store_ds) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pend[16 * hf + i] = dk[i];
         }
       }
-      if (store_ds) {   // staged and stored at the top of the next block (flush_ds)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pend[i] = dk[i];
-        pend_q = q0;
-      }
-      named_sync(1 + qw, 64);   // the other warpgroup's loads of these lanes are done
-      tmem_st16(la + C::ST_COL + 128 * u + 16 * wg, pk);
-      tmem_st16(la + C::DPT_COL + 128 * u + 16 * wg, dk);
+      if (store_ds) pend_q = q0;   // staged and stored at the top of this warpgroup's next block
       tmem_wait_st();
       fence_before();
-      mbar_arrive(&p_full[u]);
+      mbar_arrive(&p_full[wg]);
     }
     flush_ds();
     if (store_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1371,10 +1384,10 @@ __global__ void dsum_tc_kernel(const bf16* __restrict__ o, const bf16* __restric
   Dsum[(b * h + hh) * T_ + t] = s;
 }
 
-// Fixed MMA operands in TMEM (TS MMAs, d_h <= 80) per backward kernel: bit 1 dK/dV K,V, bit 2 the
-// recomputing dQ kernel's Q,dO. Default: dQ only (measured: it helps that kernel, slows dK/dV; the
-// persistent forward keeps Q in shared memory, where the next item's Q is loaded while it runs).
-// ATOM_ATTN_TSA=<mask> overrides for A/B runs.
+// Fixed MMA operands in TMEM (TS MMAs, d_h <= 80): bit 2 = the recomputing dQ kernel's Q, dO rows
+// in TMEM, on by default (measured: it helps that kernel; the same form slowed the dK/dV kernel,
+// and the persistent forward keeps Q in shared memory, where the next item's Q is loaded while it
+// runs).  ATOM_ATTN_TSA=<mask> overrides for A/B runs.
 static bool tsa_mask(int bit) {
   const char* e = getenv("ATOM_ATTN_TSA");
   const int m = e ? atoi(e) : 4;
@@ -1518,18 +1531,19 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     return false;
   }
   static bool once = false;
-  static bool tsa_kv = false, tsa_q = false;
+  static bool tsa_q = false;
   if (!once) {
 #define ATOM_BWD_ATTR(K, TS, DR)                                                                                   \
   ATOM_CUDA_OK(cudaFuncSetAttribute(K<DH, TS, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize, BCfg2<DH>::SMEM));
-    ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, false, false) ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, true, false)
-    ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, false, true) ATOM_BWD_ATTR(attn_bwd_dkv2_kernel, true, true)
     ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, false) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, false)
     ATOM_BWD_ATTR(attn_bwd_dq2_kernel, false, true) ATOM_BWD_ATTR(attn_bwd_dq2_kernel, true, true)
 #undef ATOM_BWD_ATTR
     ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dq_ds_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       DqCfg<DH>::SMEM));
-    tsa_kv = tsa_mask(1);
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv4_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg4<DH>::SMEM));
+    ATOM_CUDA_OK(cudaFuncSetAttribute(attn_bwd_dkv4_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      BCfg4<DH>::SMEM));
     tsa_q = tsa_mask(2);
     once = true;
   }
@@ -1547,24 +1561,24 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     cuuint64_t strides[1] = {(cuuint64_t)T_ * 2};
     cuuint32_t box[2] = {64, 64};
     cuuint32_t es[2] = {1, 1};
-    CUtensorMap tm_dsw;   // the dK/dV kernel's stores: one warp's 32 keys x 32 queries per box
-    cuuint32_t boxw[2] = {32, 32};
+    CUtensorMap tm_dsw;   // the dK/dV kernel's stores: one warp's 32 keys x 64 queries per box
+    cuuint32_t boxw[2] = {64, 32};
     if (!enc || enc(&tm_ds, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dsT, dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
         enc(&tm_dsw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dsT, dims, strides, boxw, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       set_error("attention: dS tensor map encode failed");
       return false;
     }
-#define ATOM_DKV_DS(TS, DR)                                                                                       \
-  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
-                                                                      drop, true, tm_dsw)
-    if (tsa_kv) { if (dr) ATOM_DKV_DS(true, true); else ATOM_DKV_DS(true, false); }
-    else { if (dr) ATOM_DKV_DS(false, true); else ATOM_DKV_DS(false, false); }
-#undef ATOM_DKV_DS
-    static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
+    if (dr)
+      attn_bwd_dkv4_kernel<DH, true><<<grid, 384, BCfg4<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h,
+                                                                       drop, true, tm_dsw);
+    else
+      attn_bwd_dkv4_kernel<DH, false><<<grid, 384, BCfg4<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h,
+                                                                        drop, true, tm_dsw);
+    static const std::string nkv = "attn_bwd_dkv4<" + std::to_string(DH) + ">";
     count_launch(nkv.c_str());
     attn_bwd_dq_ds_kernel<DH><<<grid, 256, DqCfg<DH>::SMEM, st>>>(tm_ds, qkv64, dqkv, T_, h);
     static const std::string nq = "attn_bwd_dq_ds<" + std::to_string(DH) + ">";
@@ -1587,19 +1601,19 @@ bool bwd(const bf16* qkv, const bf16* o, const bf16* dout, const float* lse, flo
     ATOM_CUDA_OK(cudaStreamWaitEvent(st2, ev_fork[dev], 0));
   }
   const cudaStream_t sq = st2 ? st2 : st;
-#define ATOM_DKV(TS, DR)                                                                                          \
-  attn_bwd_dkv2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, st>>>(qkv128, qkv64, do64, qkv, lse, Dsum, dqkv, T_, h, \
-                                                                      drop, false, qkv64)
 #define ATOM_DQ(TS, DR)                                                                                         \
   attn_bwd_dq2_kernel<DH, TS, DR><<<grid, 384, BCfg2<DH>::SMEM, sq>>>(qkv128, do128, qkv64, qkv, dout, lse, Dsum, \
                                                                        dqkv, T_, h, drop)
-  if (tsa_kv) { if (dr) ATOM_DKV(true, true); else ATOM_DKV(true, false); }
-  else { if (dr) ATOM_DKV(false, true); else ATOM_DKV(false, false); }
-  static const std::string nkv = "attn_bwd_dkv2<" + std::to_string(DH) + ">";
+  if (dr)
+    attn_bwd_dkv4_kernel<DH, true><<<grid, 384, BCfg4<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h,
+                                                                     drop, false, qkv64);
+  else
+    attn_bwd_dkv4_kernel<DH, false><<<grid, 384, BCfg4<DH>::SMEM, st>>>(qkv128, qkv64, do64, lse, Dsum, dqkv, T_, h,
+                                                                      drop, false, qkv64);
+  static const std::string nkv = "attn_bwd_dkv4<" + std::to_string(DH) + ">";
   count_launch(nkv.c_str());
   if (tsa_q) { if (dr) ATOM_DQ(true, true); else ATOM_DQ(true, false); }
   else { if (dr) ATOM_DQ(false, true); else ATOM_DQ(false, false); }
-#undef ATOM_DKV
 #undef ATOM_DQ
   if (st2) {
     ATOM_CUDA_OK(cudaGetLastError());

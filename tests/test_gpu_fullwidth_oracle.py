@@ -71,7 +71,7 @@ def wide_step():
 
 def test_wide_step_ran_the_bench_kernels(wide_step):
     ran = wide_step["ran"]
-    for k in ("gemm_tc2<0,0>", "gemm_tc2<0,1>", "gemm_tc2<1,1>", "attn_fwd3<80>", "attn_bwd_dkv2<80>"):
+    for k in ("gemm_tc2<0,0>", "gemm_tc2<0,1>", "gemm_tc2<1,1>", "attn_fwd3<80>", "attn_bwd_dkv4<80>"):
         assert ran.get(k, 0) > 0, (k, ran)
     # the dQ kernel of the step's path (dQ from dS^T at T % 128 == 0, else the recomputing one)
     assert ran.get("attn_bwd_dq_ds<80>", 0) + ran.get("attn_bwd_dq2<80>", 0) > 0, ran

@@ -2,6 +2,7 @@
 the kernels' time into a per-CTA fixed cost and a per-key-block cost (least squares over the
 sweep), next to library kernels on the same shapes (cuDNN SDPA, flash_attn) as reference points.
 FLOPs counted causally: fwd 4 B h T^2/2 dh, bwd 2x fwd (algorithmic, S recompute not counted)."""
+import os
 import sys
 
 import numpy as np
@@ -29,7 +30,8 @@ h, dh = (int(a) for a in sys.argv[1:3]) if len(sys.argv) > 2 else (32, 80)
 tokens = 16384
 d = h * dh
 rows = []
-for T in (512, 1024, 2048, 4096, 8192):
+TS = [int(t) for t in os.environ.get("ATOM_SWEEP_T", "512,1024,2048,4096,8192").split(",")]
+for T in TS:
     B = tokens // T
     qkv = (torch.randn(B * T, 3 * d, device="cuda") * 0.5).bfloat16()
     o = torch.empty(B * T, d, device="cuda", dtype=torch.bfloat16)
