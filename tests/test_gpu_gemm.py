@@ -151,7 +151,8 @@ print("splitk ok")
 """
 
 
-@pytest.mark.parametrize("shape", [(3840, 2560, 2048), (4096, 4096, 1024), (2560 + 200, 2560 + 40, 1536)],
+# ragged: 11 x 9 = 99 tiles of 256 x 256 on 74 CTA pairs, a 25-tile tail split in two (ragged M and N)
+@pytest.mark.parametrize("shape", [(3840, 2560, 2048), (4096, 4096, 1024), (2560 + 200, 2048 + 52, 1536)],
                          ids=["tail2-P8", "tail34-P2", "ragged"])
 @pytest.mark.parametrize("majors", [(True, True), (False, False)], ids=["wgrad", "kmajor"])
 def test_tc_gemm_acc_f32_streamk_tail(shape, majors):
