@@ -37,6 +37,17 @@ UNIT = "tokens/s"
 H2D_GBS, D2H_GBS, BIDIR_GBS = 55.5, 57.2, 49.7
 
 
+def attention_roofline(g, tok_step, klog, peak_tf):
+    f_fwd = tok_step * 2.0 * g.n_layer * g.d_model * (g.seq_len + 1)
+    out = {"bound": "tensor", "unit": "TFLOP/s", "peak": peak_tf,
+           "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernels timed inside the step)"}
+    for k, f in (("attn_fwd", f_fwd), ("attn_bwd", 2.0 * f_fwd)):
+        ms = klog.get(k, (0, 0.0))[1]
+        tf = f / (ms / 1000.0) / 1e12 if ms > 0 else None
+        out[k] = {"flops_per_step": f, "ms_per_step": ms, "achieved": tf, "frac": tf / peak_tf if tf else None}
+    return out
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -511,6 +522,11 @@ def main():
             # device time per kernel category in one extra (untimed) step: CUDA events around each
             # launch group on its stream (the side streams overlap the main one: the sum exceeds the step)
             "kernel_ms_per_step": {k: round(v[1], 2) for k, v in klog.items()},
+            # the attention kernels (the furthest below peak): algorithmic FLOPs of one step's causal
+            # attention, forward 2 L d (T + 1) per token and backward twice that (its recomputed S is
+            # not counted), over the same per-category event times (concurrent streams: an upper
+            # bound on the kernels' time, so a lower bound on their rate)
+            "attention_roofline": attention_roofline(g, tok_step, klog, peak_tf),
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
             "swap_hidden": {"h2d_pct": 100.0 * st["h2d_hidden_ms"] / st["h2d_ms"] if st["h2d_ms"] else None,
                             "d2h_pct": 100.0 * st["d2h_hidden_ms"] / st["d2h_ms"] if st["d2h_ms"] else None,

@@ -68,14 +68,31 @@ __global__ void __launch_bounds__(LN_THREADS) ln_fwd_kernel(const T* __restrict_
   const T* xr = x + row * d;
   float v[NC][VW];
   float s = 0.f;
+  // every 16-byte load of the row in flight before any use (the in-place residual stores below
+  // would otherwise keep the compiler from hoisting the next chunk's loads above them)
+  uint4 xraw[NC], rraw[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
-      load_vec<T>(xr + ch * VW, v[c]);
+      xraw[c] = *(const uint4*)(xr + ch * VW);
+      if (res) rraw[c] = *(const uint4*)(res + row * d + ch * VW);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch) {
+      {
+        const T* e = (const T*)&xraw[c];
+#pragma unroll
+        for (int i = 0; i < VW; ++i) v[c][i] = to_f(e[i]);
+      }
       if (res) {
         float r[VW];
-        load_vec<T>(res + row * d + ch * VW, r);
+        const T* e = (const T*)&rraw[c];
+#pragma unroll
+        for (int i = 0; i < VW; ++i) r[i] = to_f(e[i]);
         if (drop.thr) {   // VW consecutive elements of the site tensor from one Philox group (VW <= 8)
           const uint64_t i0 = (uint64_t)row * d + (uint64_t)ch * VW;
           const uint32_t keep = drop_keep8(drop, (uint32_t)(i0 >> 3)) >> (i0 & 7);
@@ -154,7 +171,13 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
   const int nch = d / VW;
   const float mean = stats[2 * row], rstd = stats[2 * row + 1];
   float xh[NC][VW], dg[NC][VW];
+  uint4 rraw[NC];   // the residual gradient, loaded with the rest (its latency off the second phase)
   float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = c * LN_THREADS + threadIdx.x;
+    if (ch < nch && dres) rraw[c] = *(const uint4*)(dres + row * d + ch * VW);
+  }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const int ch = c * LN_THREADS + threadIdx.x;
@@ -179,7 +202,11 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
     const int ch = c * LN_THREADS + threadIdx.x;
     if (ch < nch) {
       float o[VW], r[VW];
-      if (dres) load_vec<T>(dres + row * d + ch * VW, r);
+      if (dres) {
+        const T* e = (const T*)&rraw[c];
+#pragma unroll
+        for (int i = 0; i < VW; ++i) r[i] = to_f(e[i]);
+      }
 #pragma unroll
       for (int i = 0; i < VW; ++i) {
         o[i] = rstd * (dg[c][i] - m1 - xh[c][i] * m2);
@@ -193,7 +220,8 @@ __global__ void __launch_bounds__(LN_THREADS) ln_bwd_kernel(const T* __restrict_
 // Column sums over rows in a fixed order (bias gradients, LN gain / shift gradients):
 //   mode 0: out0[j] += sum_r a[r][j]
 //   mode 1: out0[j] += sum_r a[r][j] * xhat[r][j],  out1[j] += sum_r a[r][j]
-//   mode 2: a[r][j] <- T(a[r][j] * gelu'(x[r][j])) in place, out0[j] += sum_r of the stored values
+//   mode 2: a[r][j] <- T(a[r][j] * gelu'(x[r][j])) in place, out0[j] += sum_r of the stored values;
+//           with gout, gout[r][j] <- T(GELU(x[r][j])) as well (same pitch as x)
 // Grid (column blocks of 64 x VW columns) x (G row ranges), sized by the host to one wave of
 // resident CTAs (CP_PER_SM per SM): a CTA's four thread groups sum contiguous quarters of its row range
 // (UNR 16-byte loads in flight per thread), combined in group order into one partial per range.
@@ -209,7 +237,8 @@ __global__ void __launch_bounds__(CP_TX * CP_GROUPS, CP_PER_SM) col_sums_kernel(
                                                                         float* __restrict__ part1,
                                                                         float* __restrict__ out0,
                                                                         float* __restrict__ out1,
-                                                                        int* __restrict__ ticket) {
+                                                                        int* __restrict__ ticket,
+                                                                        T* __restrict__ gout) {
   constexpr int VW = Vec<T>::N;
   constexpr int UNR = MODE == 0 ? 8 : 4;
   constexpr int NS = MODE == 1 ? 2 : 1;
@@ -251,6 +280,12 @@ __global__ void __launch_bounds__(CP_TX * CP_GROUPS, CP_PER_SM) col_sums_kernel(
               s0[i] += o[i];
             }
             store_vec<T>(const_cast<T*>(a) + (rb + u) * lda + j, o);
+            if (gout) {
+              float gl[VW];
+#pragma unroll
+              for (int i = 0; i < VW; ++i) gl[i] = gelu_t<T>(to_f(xp[i]));
+              store_vec<T>(gout + (rb + u) * ncols + j, gl);
+            }
           } else if constexpr (MODE == 1) {
             const T* xp = (const T*)&rx[u];
             const float mean = stats[2 * (rb + u)], rstd = stats[2 * (rb + u) + 1];
@@ -747,14 +782,15 @@ bool ln_bwd(const T* dy, const T* x, const float* stats, const T* g, const T* dr
   }
   const int nch = cs_ranges(rows, nb);
   col_sums_kernel<T, 1><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
-      dy, d, x, stats, rows, d, part, part + (long)nch * d, dg, db, ticket);
+      dy, d, x, stats, rows, d, part, part + (long)nch * d, dg, db, ticket, nullptr);
   LAUNCH_OK();
   return true;
 }
 // dy <- T(dy * gelu'(u)) in place (dy [rows, n] at pitch n, u likewise) and db += column sums of
 // the result: the fc pre-activation gradient and its bias gradient in one pass
 template <typename T>
-bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st) {
+bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part, int* ticket, cudaStream_t st,
+                     T* gelu_out) {
   constexpr int VW = Vec<T>::N;
   const int nb = (n / VW + CP_TX - 1) / CP_TX;
   if (n % VW || nb > CS_TICKETS) {
@@ -763,7 +799,7 @@ bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part
   }
   const int nch = cs_ranges(rows, nb);
   col_sums_kernel<T, 2><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
-      dy, n, u, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
+      dy, n, u, nullptr, rows, n, part, nullptr, db, nullptr, ticket, gelu_out);
   LAUNCH_OK();
   return true;
 }
@@ -781,7 +817,7 @@ bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, i
   }
   const int nch = cs_ranges(rows, nb);
   col_sums_kernel<T, 0><<<dim3(nb, nch), dim3(CP_TX, CP_GROUPS), 0, st>>>(
-      dy, ld, nullptr, nullptr, rows, n, part, nullptr, db, nullptr, ticket);
+      dy, ld, nullptr, nullptr, rows, n, part, nullptr, db, nullptr, ticket, nullptr);
   LAUNCH_OK();
   return true;
 }
@@ -882,7 +918,7 @@ bool loss_sum(const float* l, long n, float scale, float* out, cudaStream_t st) 
   template bool ln_bwd<T>(const T*, const T*, const float*, const T*, const T*, T*, float*, float*, float*, int*, long, \
                           int, cudaStream_t);                                                                   \
   template bool bias_grad<T>(const T*, long, long, int, float*, float*, int*, cudaStream_t);                    \
-  template bool dgelu_bias_grad<T>(T*, const T*, long, int, float*, float*, int*, cudaStream_t);              \
+  template bool dgelu_bias_grad<T>(T*, const T*, long, int, float*, float*, int*, cudaStream_t, T*);              \
   template bool cross_entropy<T>(T*, long, int, const int32_t*, long, int, long, float, float*, cudaStream_t);  \
   template bool embed_fwd<T>(const int32_t*, long, int, long, const T*, const T*, T*, int, cudaStream_t);       \
   template bool embed_bwd<T>(const int32_t*, long, int, int, const T*, int, int, float*, float*, int*,         \

@@ -339,6 +339,12 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
   // LN2 output (A under stash) is rewritten by LN1's re-apply after the attention backward, which
   // also rewrites G; WO reads DX2 / o, WQKV reads G / A; the next block rewrites G, A, DX2.
   const bool side = p->side_wgrad;
+  // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr).  Its weight gradient reads GELU(u) in G
+  // and dy: on the side stream when the fc pre-activation gradient goes to the second buffer G2
+  // (so nothing on the main stream rewrites G or dy before the join ahead of the attention
+  // backward); on the main stream with dropout (dym lives in DX2), under the re-forward (no
+  // join there) and for a split block (dy is rewritten in place by LN2's backward)
+  const bool wpr_side = side && !rc && !d3.thr && !split;
   const cudaStream_t sd = side ? p->s_side : p->s_comp;
   auto fork = [&]() -> bool {
     if (side) {
@@ -375,7 +381,7 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
     e.out2 = G;
     e.ldo2 = 4 * d;
     PEER_OK(gemm<T>(p, M, 4 * d, d, (const T*)ln2, d, false, w(T_WFC), d, false, e));
-  } else {
+  } else if (!wpr_side) {
     KT(KC_GELU, p->s_comp, gelu_apply<T>((const T*)s.u, G, M * 4 * d, p->s_comp));
   }
   // residual dropout (R38): the projections' branches see the masked gradients
@@ -386,22 +392,21 @@ bool bwd_block(atom_peer* p, int l, int mb, const SegView& sv, int part = 0) {
     KT(KC_COLSUM, p->s_comp, dropout<T>(dy, (T*)sc.DX2, M * d, d3, p->s_comp));
     dym = (const T*)sc.DX2;
   }
-  // MLP projection: out = x2 + D3(GELU(u) W_pr^T + b_pr).  Its weight gradient reads GELU(u) in G
-  // and dy: on the side stream when the fc pre-activation gradient goes to the second buffer G2
-  // (so nothing on the main stream rewrites G or dy before the join ahead of the attention
-  // backward); on the main stream with dropout (dym lives in DX2), under the re-forward (no
-  // join there) and for a split block (dy is rewritten in place by LN2's backward)
-  const bool wpr_side = side && !rc && !d3.thr && !split;
   T* Gx = wpr_side ? (T*)sc.G2 : G;   // dL/du
-  if (wpr_side) PEER_OK(fork());
-  PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d),
-                  wpr_side ? sd : p->s_comp));
+  if (!wpr_side)
+    PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d), p->s_comp));
   KT(KC_COLSUM, p->s_comp, bias_grad<T>(dym, d, M, d, g(T_BPR), p->red, p->red_ticket, p->s_comp));
   // fc pre-activation gradient: (dy W_pr) with a plain-store epilogue, then the GELU derivative
   // and the fc bias gradient in one pass over it (the GEMM epilogue reading u per row was the
-  // slow part of the fused form)
+  // slow part of the fused form).  With W_pr's gradient on the side stream the same pass also
+  // re-applies GELU(u) into G (one read of u instead of two), and that gradient starts after it
   PEER_OK(gemm<T>(p, M, 4 * d, d, dym, d, false, w(T_WPR), 4 * d, true, epi(EPI_STORE, Gx, 4 * d)));
-  KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(Gx, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp));
+  KT(KC_COLSUM, p->s_comp, dgelu_bias_grad<T>(Gx, (const T*)s.u, M, 4 * d, g(T_BFC), p->red, p->red_ticket, p->s_comp,
+                                              wpr_side ? G : nullptr));
+  if (wpr_side) {
+    PEER_OK(fork());
+    PEER_OK(gemm<T>(p, d, 4 * d, M, dym, d, true, G, 4 * d, true, epi(EPI_ACC_F32, g(T_WPR), 4 * d), sd));
+  }
   // MLP fc: u = LN2(x2) W_fc^T + b_fc (under recompute LN2's output is DA, rewritten just below:
   // that gradient stays on the main stream)
   if (!rc) KT(KC_LN, p->s_comp, ln_apply<T>((const T*)s.x2, w(T_LN2G), w(T_LN2B), s.st2, ln2, M, d, p->s_comp));

@@ -40,8 +40,9 @@ template <typename T> bool ln_bwd(const T* dy, const T* x, const float* stats, c
                                   float* db, float* part, int* ticket, long rows, int d, cudaStream_t st);
 template <typename T> bool bias_grad(const T* dy, long ld, long rows, int n, float* db, float* part, int* ticket,
                                      cudaStream_t st);
+// gelu_out != NULL: also writes T(GELU(u)) there (the backward's re-apply of the fc activation)
 template <typename T> bool dgelu_bias_grad(T* dy, const T* u, long rows, int n, float* db, float* part, int* ticket,
-                                           cudaStream_t st);
+                                           cudaStream_t st, T* gelu_out = nullptr);
 template <typename T> bool cross_entropy(T* logits, long ld, int V, const int32_t* targets, long tstride, int T_, long rows,
                                          float scale, float* loss, cudaStream_t st);
 template <typename T> bool embed_fwd(const int32_t* tok, long tstride, int T_, long rows, const T* wte, const T* wpe, T* h,
