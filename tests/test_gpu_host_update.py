@@ -51,9 +51,12 @@ def test_fp32_rounds_match_oracle(g, ends, R):
         assert abs(loss - rl) <= 1e-4 * abs(rl), (s, loss, rl)
     assert peer.info()["step"] == ref.t == 2
     got = peer.params()
-    for key, want in (("master", ref.p), ("m", ref.m), ("v", ref.v)):
-        rel = np.linalg.norm(got[key] - want) / np.linalg.norm(want)
-        assert rel <= (1e-4 if key != "v" else 2e-4), (key, rel)
+    # v = (1 - beta2) g^2 doubles the relative error of g: the 1e-4 bar applies to sqrt(v)
+    # (R39, as in test_gpu_step.py)
+    for key, x, want in (("master", got["master"], ref.p), ("m", got["m"], ref.m),
+                         ("sqrt(v)", np.sqrt(got["v"].astype(np.float64)), np.sqrt(ref.v))):
+        rel = np.linalg.norm(x - want) / np.linalg.norm(want)
+        assert rel <= 1e-4, (key, rel)
     peer.destroy()
 
 
