@@ -275,28 +275,26 @@ def run_reference(args, g, wl_desc):
     print(json.dumps(line), flush=True)
 
 
-GEMM_NCU = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01j_gemm_step_ncu.json")
-GEMM_NCU_SHAPES = [("qkv", 16384, 7680, 2560, 0), ("proj", 16384, 2560, 2560, 0), ("fc", 16384, 10240, 2560, 0),
-                   ("fc2", 16384, 2560, 10240, 1)]
+GEMM_NCU = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_shapes_ncu.json")
 
 
 def gemm_traffic():
-    """DRAM bytes per GEMM launch from the committed `ncu --set full` capture of the first four
-    GEMMs of a 2.7B step (one block forward: QKV, projection, fc, fc2), next to their algorithmic
-    bytes (A + B + outputs + residual)."""
+    """DRAM bytes per GEMM launch from the committed `ncu --set full` captures of the twelve 2.7B
+    block GEMM shapes (forward, data gradient, weight gradient of QKV, projection, fc, fc2; one
+    launch each, cold L2: tools/runs/gpu_r2_51.sh), averaged like `achieved` over the step's GEMM
+    mix (each shape once per block and micro-batch), next to their algorithmic bytes (A + B + C)."""
     try:
         with open(GEMM_NCU) as f:
             caps = json.load(f)
     except OSError:
         return {"traffic": None}
-    per, alg = [], []
-    for c, (name, M, N, K, extra) in zip(caps, GEMM_NCU_SHAPES):
-        per.append(c["dram_read"] + c["dram_write"])
-        outs = 2 if name == "fc" else 1   # fc stores the pre-activation and GELU(u)
-        alg.append(2.0 * (M * K + N * K + outs * M * N + extra * M * N))
+    per = [c["dram_read"] + c["dram_write"] for c in caps]
+    alg = [c["algorithmic_bytes"] for c in caps]
     return {"traffic": sum(per) / len(per),
-            "traffic_detail": {"shapes": [s[0] for s in GEMM_NCU_SHAPES], "dram_bytes": per,
-                               "algorithmic_bytes": alg, "source": os.path.relpath(GEMM_NCU, os.path.dirname(GEMM_NCU) + "/..")}}
+            "traffic_detail": {"shapes": [c["shape"] for c in caps], "dram_bytes": per, "algorithmic_bytes": alg,
+                               "mean_over_algorithmic": sum(per) / sum(alg),
+                               "tensor_pipe_pct": [round(c["tensor_pipe_pct"], 1) for c in caps],
+                               "source": os.path.relpath(GEMM_NCU, os.path.dirname(os.path.abspath(__file__)))}}
 
 
 def host_link(st, plan, probe_gbs):
