@@ -59,6 +59,13 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* m, uint64
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 1-D bulk copy global -> shared (16-byte aligned, size % 16 == 0), completing on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void commit(uint64_t* b) {
@@ -718,18 +725,54 @@ __device__ __forceinline__ uint32_t drop_keep_keyrow(const Drop& dr, uint64_t ro
 // ahead into the freed buffer.  dS^T (store_ds) leaves through a per-warp 32-key x 64-query smem
 // box and a TMA store, staged at the top of the warpgroup's next block.
 // ======================================================================================
-constexpr int BW4_NST = 3;   // ring stages (the dS^T staging takes the fourth one's room)
+#ifndef ATOM_DKV_NST
+#define ATOM_DKV_NST 3
+#endif
+#ifndef ATOM_DKV_DSBOX
+#define ATOM_DKV_DSBOX 1
+#endif
+constexpr int BW4_NST = ATOM_DKV_NST;   // ring stages (the dS^T staging takes the fourth one's room)
+#ifdef ATOM_DKV_TRACE   // timing experiment only: per-warp clock64 stamps of the first CTAs' pipeline events
+__device__ unsigned long long g_dkv_trace[8][12][64][4];
+#define DKV_STAMP(it, ev)                                                                               \
+  do {                                                                                                  \
+    if (blockIdx.x == 0 && blockIdx.y < 8 && (threadIdx.x & 31) == 0 && (it) < 64)                      \
+      g_dkv_trace[blockIdx.y][threadIdx.x >> 5][(it)][(ev)] = clock64();                                \
+  } while (0)
+#else
+#define DKV_STAMP(it, ev) \
+  do {                    \
+  } while (0)
+#endif
 template <int DH>
 struct BCfg4 {
   static constexpr int NP = (DH + 63) / 64;
   static constexpr int P128 = 128 * 128, P64 = 64 * 128;
   static constexpr int FIX = 2 * NP * P128;          // K, V of the CTA's 128 keys
   static constexpr int STG = 2 * NP * P64;           // Q_i, dO_i: 64 rows each
-  static constexpr int DS_STG = 8 * 32 * 128;        // per elementwise warp: 32 keys x 64 queries bf16
-  static constexpr int SMEM = FIX + BW4_NST * STG + DS_STG + BW4_NST * 2 * 64 * 4 + 1024 + 512;
+  static constexpr int DS_STG = ATOM_DKV_DSBOX * 8 * 32 * 128;   // per elementwise warp: 32 keys x 64 queries bf16
   static constexpr uint32_t ST_COL = 0, DPT_COL = 64, ACC0 = 256, ACC1 = 384;   // buffer u: +128u
+  // d_h <= 80: K and V are also copied from shared memory into TMEM (tcgen05.cp, after the dV / dK
+  // accumulators) and S^T = K Q^T, dP^T = V dO^T run as TS MMAs: an SS MMA at N = 64 reads 6 KB of
+  // shared memory per 128 x 64 x 16 product and is bound by it (74 cycles, tools/tmem_bw.cu), the
+  // TS form reads 2 KB (42 cycles) -- these products set this kernel's pace (clock64 trace,
+  // tools/dkv_trace.py: ~1100 tensor-pipe cycles per 64-query block)
+  static constexpr bool KVT = DH <= 80;
+  static constexpr uint32_t FA_COL = ACC0 + (DH + 15) / 16 * 16, FB_COL = ACC1 + (DH + 15) / 16 * 16;
+  static_assert(!KVT || FB_COL + DH / 2 <= 512, "TMEM budget");
+  // ring stages: BW4_NST after the fixed K, V tiles; with K, V in TMEM the fixed tiles' room becomes
+  // FIX / STG more stages once the copies have read it (a 3-stage ring left the TMA latency of the
+  // Q / dO refill, ~1600 cycles under this kernel's dS^T stores, on the critical path)
+  static constexpr int NST_X = KVT ? FIX / STG : 0;
+  static constexpr int NST = BW4_NST + NST_X;
+  static constexpr int SMEM = FIX + BW4_NST * STG + DS_STG + NST * 2 * 64 * 4 + 1024 + 512;
   static_assert(SMEM <= 232448, "shared memory");
 };
+
+// smem -> TMEM copy of a 128-row x 32-byte slab (16 bf16 of each row, as an MMA A-operand K step)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 
 template <int DH, bool DROP>
 __global__ void __launch_bounds__(384, 1)
@@ -738,14 +781,16 @@ __global__ void __launch_bounds__(384, 1)
                          const float* __restrict__ Dsum, bf16* __restrict__ dqkv, int T_, int h, const Drop drop,
                          const bool store_ds, const __grid_constant__ CUtensorMap tm_dsw) {
   using C = BCfg4<DH>;
-  constexpr int NST = BW4_NST;
+  constexpr int NST = C::NST;
   constexpr int POLY = DH < 128;   // the FMA-pipe share (ATOM_BWD_POLY_KV of 8 pairs) applies when the MMAs are short
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sK = sm;
   uint8_t* sV = sK + C::NP * C::P128;
-  uint8_t* sS = sm + C::FIX;                           // stage s: Q at + s*STG, dO at + NP*P64
-  uint8_t* sDS = sS + NST * C::STG;                    // dS^T staging, 4 KB per elementwise warp (1024-aligned)
+  uint8_t* sS = sm + C::FIX;                           // stage s < BW4_NST: Q at + s*STG, dO at + NP*P64
+  // stage s >= BW4_NST (K, V in TMEM): in the fixed tiles' room, free once the copies have read it
+  auto stage_ptr = [&](int s) { return s < BW4_NST ? sS + s * C::STG : sm + (s - BW4_NST) * C::STG; };
+  uint8_t* sDS = sS + BW4_NST * C::STG;                // dS^T staging, 4 KB per elementwise warp (1024-aligned)
   float* sLD = (float*)(sDS + C::DS_STG);              // stage s: L[64] at + 128 s, D[64] at + 128 s + 64
   uint64_t* bars = (uint64_t*)(sLD + NST * 128);
   uint64_t* kv_full = bars;
@@ -754,7 +799,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = st_empty + NST;      // [2]
   uint64_t* p_full = s_full + 2;          // [2]
   uint64_t* done = p_full + 2;
-  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  uint64_t* kv_free = done + 1;           // the K, V copies into TMEM have read the fixed tiles
+  uint32_t* tmem_slot = (uint32_t*)(kv_free + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
@@ -777,6 +823,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&p_full[u], 128);
     }
     mbar_init(done, 1);
+    mbar_init(kv_free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -799,27 +846,40 @@ __global__ void __launch_bounds__(384, 1)
         tma_load(sV + p * C::P128, &tm_kv, kv_full, 2 * d + hh * DH + 64 * p, row0 + k0);
       }
     }
+    // the L / D values of a block (raw LSE; queries beyond T_ get L = +inf, so P and dS are exactly
+    // 0): with T % 64 == 0 two 256-byte bulk copies on the stage's barrier, else this warp's lanes
+    // (their global-load latency, ~900 cycles, in every stage's fill made this warp the pacer)
+    const bool bulk_ld = T_ % 64 == 0;
     for (int it = 0; it < nblk; ++it) {
       const int s = it % NST, q0 = (i0 + it) * 64;
+      DKV_STAMP(it, 0);
       mbar_wait(&st_empty[s], ((it / NST) & 1) ^ 1);
+      if (C::NST_X > 0 && it == BW4_NST) mbar_wait(kv_free, 0);   // first use of the fixed tiles' room
+      DKV_STAMP(it, 1);
+      float* L = sLD + 128 * s;
       if (lane == 0) {
-        uint8_t* q = sS + s * C::STG;
+        uint8_t* q = stage_ptr(s);
         uint8_t* g = q + C::NP * C::P64;
-        mbar_expect_tx(&st_full[s], C::STG);
+        mbar_expect_tx(&st_full[s], C::STG + (bulk_ld ? 512 : 0));
         for (int p = 0; p < C::NP; ++p) {
           tma_load(q + p * C::P64, &tm_q, &st_full[s], hh * DH + 64 * p, row0 + q0);
           tma_load(g + p * C::P64, &tm_do, &st_full[s], hh * DH + 64 * p, row0 + q0);
         }
+        if (bulk_ld) {
+          bulk_load(L, lrow + q0, 256, &st_full[s]);
+          bulk_load(L + 64, drow + q0, 256, &st_full[s]);
+        }
       }
-      // queries beyond T_: L = +inf makes P (and so dS) exactly 0 (the ring holds -L)
-      float* L = sLD + 128 * s;
+      if (!bulk_ld) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int qi = q0 + lane + 32 * e;
-        L[lane + 32 * e] = qi < T_ ? -lrow[qi] * LOG2E : -INFINITY;   // stored negated
-        L[64 + lane + 32 * e] = qi < T_ ? drow[qi] : 0.f;
+        for (int e = 0; e < 2; ++e) {
+          const int qi = q0 + lane + 32 * e;
+          L[lane + 32 * e] = qi < T_ ? lrow[qi] : INFINITY;
+          L[64 + lane + 32 * e] = qi < T_ ? drow[qi] : 0.f;
+        }
       }
       mbar_arrive(&st_full[s]);
+      DKV_STAMP(it, 2);
     }
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16(128, 64, false, false);   // S^T = K Q^T, dP^T = V dO^T
@@ -827,20 +887,37 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(kv_full, 0);
     const bool elected = elect_one();
     const uint64_t dk = desc_sw128(smem_u32(sK), 16, 1024), dv = desc_sw128(smem_u32(sV), 16, 1024);
-    const uint64_t ds_k = desc_sw128(smem_u32(sS), 16, 1024);       // stage tiles, K-major
-    const uint64_t ds_mn = desc_sw128(smem_u32(sS), C::P64, 1024);  // stage tiles, MN-major
+    auto ds_k = [&](int s) { return desc_sw128(smem_u32(stage_ptr(s)), 16, 1024); };       // stage tiles, K-major
+    auto ds_mn = [&](int s) { return desc_sw128(smem_u32(stage_ptr(s)), C::P64, 1024); };  // stage tiles, MN-major
+    if constexpr (C::KVT) {   // K, V into TMEM; executes before the MMAs issued after it
+      if (elected) {
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
+          tmem_cp_128x256b(tbase + C::FA_COL + 8 * kk, dk + oa);
+          tmem_cp_128x256b(tbase + C::FB_COL + 8 * kk, dv + oa);
+        }
+        commit(kv_free);   // arrives when the copies (and nothing after them) are done
+      }
+      __syncwarp();
+    }
     auto issue_s = [&](int it) {   // S^T / dP^T of block it into buffer it % 2
       const int s = it % NST, u = it & 1;
       mbar_wait(&st_full[s], (it / NST) & 1);
       fence_after();
       if (elected) {
-        const uint64_t q = ds_k + (uint64_t)((s * C::STG) >> 4), g = q + ((C::NP * C::P64) >> 4);
+        const uint64_t q = ds_k(s), g = q + ((C::NP * C::P64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t oa = ((kk >> 2) * C::P128 + (kk & 3) * 32) >> 4;
           const uint32_t ob = ((kk >> 2) * C::P64 + (kk & 3) * 32) >> 4;
-          mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
-          mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
+          if constexpr (C::KVT) {
+            mma_ts(tbase + C::ST_COL + 128 * u, tbase + C::FA_COL + 8 * kk, q + ob, id_s, kk > 0);
+            mma_ts(tbase + C::DPT_COL + 128 * u, tbase + C::FB_COL + 8 * kk, g + ob, id_s, kk > 0);
+          } else {
+            mma(tbase + C::ST_COL + 128 * u, dk + oa, q + ob, id_s, kk > 0);
+            mma(tbase + C::DPT_COL + 128 * u, dv + oa, g + ob, id_s, kk > 0);
+          }
         }
         commit(&s_full[u]);
       }
@@ -850,10 +927,12 @@ __global__ void __launch_bounds__(384, 1)
     if (nblk > 1) issue_s(1);
     for (int it = 0; it < nblk; ++it) {
       const int s = it % NST, u = it & 1;
+      DKV_STAMP(it, 0);
       mbar_wait(&p_full[u], (it >> 1) & 1);
+      DKV_STAMP(it, 1);
       fence_after();
       if (elected) {
-        const uint64_t q = ds_mn + (uint64_t)((s * C::STG) >> 4), g = q + ((C::NP * C::P64) >> 4);
+        const uint64_t q = ds_mn(s), g = q + ((C::NP * C::P64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // 64 queries = 4 x 16
           const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
@@ -866,6 +945,7 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       // buffer u is free once these products have read it (in-order execution)
       if (it + 2 < nblk) issue_s(it + 2);
+      DKV_STAMP(it, 2);
     }
   } else if (warp >= 4) {
     const int wg = (warp - 4) >> 2, qw = warp & 3;
@@ -901,8 +981,11 @@ __global__ void __launch_bounds__(384, 1)
     for (int it = wg; it < nblk; it += 2) {
       const int s = it % NST, q0 = (i0 + it) * 64;
       flush_ds();
+      DKV_STAMP(it, 0);
       mbar_wait(&st_full[s], (it / NST) & 1);   // L / D of this stage visible
+      DKV_STAMP(it, 1);
       mbar_wait(&s_full[wg], (it >> 1) & 1);
+      DKV_STAMP(it, 2);
       fence_after();
       const bool masked = q0 < k0 + 128;   // block straddles the diagonal
 #pragma unroll
@@ -911,8 +994,9 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(st_col + 32 * hf, sv);
         tmem_ld32(dp_col + 32 * hf, dv);
         tmem_wait_ld();
-        const float* L = sLD + 128 * s + 32 * hf;
+        const float* L = sLD + 128 * s + 32 * hf;   // raw LSE (x = s sc - L log2 e)
         const float* D = L + 64;
+        const uint64_t nlog2e2 = f2pack(-LOG2E, -LOG2E);
         uint32_t pk[16], dk[16];
         uint32_t keep = 0xFFFFFFFFu;   // bit c: query q0 + 32 hf + c kept at this key
         (void)keep;
@@ -920,12 +1004,12 @@ __global__ void __launch_bounds__(384, 1)
         const int lim = kj - q0 - 32 * hf;   // masked block: query c of this half is visible iff c >= lim
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 l4 = *(const float4*)(L + 4 * c4);   // -L
+          const float4 l4 = *(const float4*)(L + 4 * c4);
           const float4 d4 = *(const float4*)(D + 4 * c4);
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const int c = 4 * c4 + 2 * h2;
-            const uint64_t nl2 = h2 ? f2pack(l4.z, l4.w) : f2pack(l4.x, l4.y);
+            const uint64_t nl2 = fmul2(h2 ? f2pack(l4.z, l4.w) : f2pack(l4.x, l4.y), nlog2e2);
             const uint64_t d2 = h2 ? f2pack(d4.z, d4.w) : f2pack(d4.x, d4.y);
             const uint64_t x2 = ffma2(f2pack(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sc2, nl2);
             uint64_t p2;
@@ -974,6 +1058,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_st();
       fence_before();
       mbar_arrive(&p_full[wg]);
+      DKV_STAMP(it, 3);
     }
     flush_ds();
     if (store_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1652,3 +1737,9 @@ bool attn_fwd_tc(const bf16* qkv, bf16* o, float* lse, int B, int T_, int h, int
 }
 
 }  // namespace atom
+
+#ifdef ATOM_DKV_TRACE
+extern "C" int atom_k_dkv_trace(void* dst) {
+  return cudaMemcpyFromSymbol(dst, atom::atc::g_dkv_trace, sizeof(atom::atc::g_dkv_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif

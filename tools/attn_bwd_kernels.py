@@ -18,7 +18,11 @@ lse = torch.empty(B * h * T, device="cuda")
 ds = torch.empty(B * h * T, device="cuda")
 dqkv = torch.empty_like(qkv)
 atom.k_attn_fwd(atom.ATTN_TC, atom.BF16, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, h, dh)
-for impl, nm in ((atom.ATTN_TC, "recompute dQ"), (atom.ATTN_TC_DS, "dQ from dS^T")):
+import os
+IMPLS = [(atom.ATTN_TC, "recompute dQ"), (atom.ATTN_TC_DS, "dQ from dS^T")]
+if os.environ.get("ATOM_BWD_ONLY"):   # "tc" or "ds": one path only (e.g. builds without the dS^T staging)
+    IMPLS = IMPLS[:1] if os.environ["ATOM_BWD_ONLY"] == "tc" else IMPLS[1:]
+for impl, nm in IMPLS:
     for _ in range(3):
         atom.k_attn_bwd(impl, atom.BF16, qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), ds.data_ptr(),
                         dqkv.data_ptr(), B, T, h, dh)
