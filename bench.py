@@ -499,7 +499,7 @@ def main():
             # value is the whole-job aggregate over all peers (the bench contract); per B200 here
             "value_per_gpu": value / world,
             "gpu_launches": st["kernel_launches"],
-            "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05)", "achieved": gemm_tf,
+            "roofline": {"bound": "tensor", "kernel": "gemm_tc2_kernel (tcgen05, 2-CTA 256x256 tiles; all GEMM launches of the timed steps)", "achieved": gemm_tf,
                          "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": (gemm_tf / peak_tf) if gemm_tf else None, **gemm_traffic(),
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
