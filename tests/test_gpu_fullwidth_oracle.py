@@ -119,3 +119,32 @@ def test_wide_step_gradient_as_accurate_as_torch_bf16(wide_step):
     torch_bf16 = gradient_errors(wide_step["g_torch"], wide_step["g_ref"], WIDE)
     for k in ours:
         assert ours[k][1] <= 1.25 * torch_bf16[k][1], (k, ours[k], torch_bf16[k])
+
+
+# GPT-3 XL's width (the other BASELINE single-GPU config): d = 2048, 16 heads x 128 -- the d_h = 128
+# kernels (K, V stay in shared memory in the dK/dV kernel, no FMA-pipe exponentials in the forward)
+WIDE_XL = synth.GPTConfig("wide-xl", n_layer=2, d_model=2048, n_head=16, seq_len=2048, vocab=50257, micro_batch=1)
+
+
+def test_wide_xl_step_matches_oracle():
+    """One swapped bf16 step at XL width (L = 2, b = 1, C = 2, sub-models [E B0 | B1 | H]) against the
+    fp64 oracle: the loss within 5e-4 relative and the step-1 gradient within the bf16 bounds of
+    tests/grad_check.py, with the launch log proving the d_h = 128 attention kernels ran."""
+    cfg = atom.make_cfg(WIDE_XL, dtype=atom.BF16, C_=C, overlap_check=0, forced_ends=ENDS, lr=LR, beta1=B1,
+                        warmup_steps=0)
+    plan = atom.atom_plan(cfg, 10 ** 12, 10 ** 10)
+    assert plan.ends() == ENDS
+    init = synth.init_params(WIDE_XL, seed=1234, perturb=True)
+    toks = synth.tokens(WIDE_XL, C * WIDE_XL.micro_batch, synth.step_seed(0, 0))
+    peer = atom.Peer(cfg, plan, init_params=init)
+    before = atom.launch_log()
+    loss = peer.step(toks)
+    after = atom.launch_log()
+    g = peer.params()["m"] / (1.0 - B1)
+    peer.destroy()
+    ran = {k: after.get(k, 0) - before.get(k, 0) for k in after}
+    for k in ("attn_fwd3<128>", "attn_bwd_dkv4<128>", "attn_bwd_dq_ds<128>"):
+        assert ran.get(k, 0) > 0, (k, ran)
+    ref_loss, g_ref = ogpt.loss_and_grad(WIDE_XL, init.astype(np.float64), toks)
+    assert abs(loss - ref_loss) <= 5e-4 * abs(ref_loss), (loss, ref_loss)
+    check_bf16_gradient(g, g_ref, WIDE_XL)
