@@ -126,12 +126,15 @@ def test_wide_step_gradient_as_accurate_as_torch_bf16(wide_step):
 WIDE_XL = synth.GPTConfig("wide-xl", n_layer=2, d_model=2048, n_head=16, seq_len=2048, vocab=50257, micro_batch=1)
 
 
-def test_wide_xl_step_matches_oracle():
+@pytest.mark.parametrize("p_drop", [0.0, 0.1], ids=["no-dropout", "dropout"])
+def test_wide_xl_step_matches_oracle(p_drop):
     """One swapped bf16 step at XL width (L = 2, b = 1, C = 2, sub-models [E B0 | B1 | H]) against the
     fp64 oracle: the loss within 5e-4 relative and the step-1 gradient within the bf16 bounds of
-    tests/grad_check.py, with the launch log proving the d_h = 128 attention kernels ran."""
+    tests/grad_check.py, with the launch log proving the d_h = 128 attention kernels ran; with dropout
+    the oracle averages the per-micro-batch Philox streams (R38)."""
+    seed = 99
     cfg = atom.make_cfg(WIDE_XL, dtype=atom.BF16, C_=C, overlap_check=0, forced_ends=ENDS, lr=LR, beta1=B1,
-                        warmup_steps=0)
+                        warmup_steps=0, dropout_p=p_drop, dropout_seed=seed)
     plan = atom.atom_plan(cfg, 10 ** 12, 10 ** 10)
     assert plan.ends() == ENDS
     init = synth.init_params(WIDE_XL, seed=1234, perturb=True)
@@ -145,6 +148,14 @@ def test_wide_xl_step_matches_oracle():
     ran = {k: after.get(k, 0) - before.get(k, 0) for k in after}
     for k in ("attn_fwd3<128>", "attn_bwd_dkv4<128>", "attn_bwd_dq_ds<128>"):
         assert ran.get(k, 0) > 0, (k, ran)
-    ref_loss, g_ref = ogpt.loss_and_grad(WIDE_XL, init.astype(np.float64), toks)
+    if p_drop == 0:
+        ref_loss, g_ref = ogpt.loss_and_grad(WIDE_XL, init.astype(np.float64), toks)
+    else:
+        b = WIDE_XL.micro_batch
+        ref_loss, g_ref = 0.0, 0.0
+        for mb in range(C):
+            lo, gr = ogpt.loss_and_grad(WIDE_XL, init.astype(np.float64), toks[mb * b:(mb + 1) * b],
+                                        drop=ogpt.Dropout(p_drop, seed, micro_step=mb))
+            ref_loss, g_ref = ref_loss + lo / C, g_ref + gr / C
     assert abs(loss - ref_loss) <= 5e-4 * abs(ref_loss), (loss, ref_loss)
     check_bf16_gradient(g, g_ref, WIDE_XL)
