@@ -48,6 +48,46 @@ def attention_roofline(g, tok_step, klog, peak_tf):
     return out
 
 
+def attention_standalone(g, device, burst_tf):
+    """The step's attention kernels timed alone at one micro-batch's shape (b, T, h, d_h): the
+    persistent forward and the dS^T backward (dK/dV + dQ + D), CUDA events on the launching stream,
+    against the burst peak (a kernel timed alone)."""
+    import torch
+    from paper_2403_10504_b200 import atom
+    b, T, h, d = g.micro_batch, g.seq_len, g.n_head, g.d_model
+    dh = d // h
+    gen = torch.Generator(device=device).manual_seed(5)
+    qkv = (torch.randn(b * T, 3 * d, generator=gen, device=device) * 0.5).bfloat16()
+    o = torch.empty(b * T, d, device=device, dtype=torch.bfloat16)
+    dout = torch.randn(b * T, d, generator=gen, device=device).bfloat16()
+    lse = torch.empty(b * h * T, device=device)
+    dsum = torch.empty(b * h * T, device=device)
+    dqkv = torch.empty_like(qkv)
+    st = torch.cuda.current_stream(device).cuda_stream
+    f_fwd = 4.0 * b * h * dh * T * (T + 1) / 2
+    fwd = lambda: atom.k_attn_fwd(atom.ATTN_TC, atom.BF16, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), b, T, h,
+                                  dh, stream=st)
+    bwd = lambda: atom.k_attn_bwd(atom.ATTN_TC_DS, atom.BF16, qkv.data_ptr(), o.data_ptr(), dout.data_ptr(),
+                                  lse.data_ptr(), dsum.data_ptr(), dqkv.data_ptr(), b, T, h, dh, stream=st)
+    out = {"shape": {"b": b, "T": T, "h": h, "d_h": dh}, "unit": "TFLOP/s", "peak": burst_tf,
+           "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: kernels timed alone)"}
+    for name, fn, f in (("fwd", fwd, f_fwd), ("bwd", bwd, 2.0 * f_fwd)):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(device)
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(device)
+        us = e0.elapsed_time(e1) / 10 * 1000.0
+        tf = f / (us * 1e-6) / 1e12
+        out[name] = {"us": us, "achieved": tf, "frac": tf / burst_tf}
+    del qkv, o, dout, lse, dsum, dqkv
+    return out
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -307,6 +347,8 @@ def host_link(st, plan, probe_gbs):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--no-attn-standalone", action="store_true",
+                    help="skip the attention kernels' standalone timing (attention_roofline.standalone)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="2.7b", choices=sorted(WORKLOADS))
@@ -452,6 +494,12 @@ def main():
     peer.reset_stats(timing=2)
     peer.step_device(dev_batches[0])
     klog = peer.kernel_log()
+    attn_alone = None
+    if rank == 0 and not args.no_attn_standalone:
+        try:
+            attn_alone = attention_standalone(g, f"cuda:{local}", pk["bf16_tflops"])
+        except Exception as ex:  # noqa: BLE001 -- a report field, never a reason to lose the line
+            attn_alone = {"error": f"{type(ex).__name__}: {ex}"[:200]}
     value = world * args.steps * tok_step / (ms / 1000.0)
     e2e = world * args.steps * tok_step / (ms_e2e / 1000.0)
 
@@ -524,7 +572,8 @@ def main():
             # attention, forward 2 L d (T + 1) per token and backward twice that (its recomputed S is
             # not counted), over the same per-category event times (concurrent streams: an upper
             # bound on the kernels' time, so a lower bound on their rate)
-            "attention_roofline": attention_roofline(g, tok_step, klog, peak_tf),
+            "attention_roofline": {**attention_roofline(g, tok_step, klog, peak_tf),
+                                   "standalone": attn_alone},
             "swap_hidden_pct": (100.0 * st["copy_hidden_ms"] / st["copy_ms"]) if st["copy_ms"] else None,
             "swap_hidden": {"h2d_pct": 100.0 * st["h2d_hidden_ms"] / st["h2d_ms"] if st["h2d_ms"] else None,
                             "d2h_pct": 100.0 * st["d2h_hidden_ms"] / st["d2h_ms"] if st["d2h_ms"] else None,
